@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 stencil_tb hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "cfg2"): isotropic acoustic, space order
+8, fp32, 512^3 physical grid + 40-point sponge inside the grid (592^3
+computational points), h = 10 m, v = 1.5 + 1.0 z/zmax km/s +
+N(0, 0.05) seeded, one 15 Hz Ricker source at a seeded off-grid position,
+512 x 512 receivers at 20 m depth on fractional offsets, dt = 0.8 ms.
+A "step" is one time step (stencil + fused injection + receiver gather) over
+the whole grid.  GPts/s counts the computational grid incl. sponge, as
+stencil_tb's RunReport does (engine.py:445-447).
+
+Arms:
+  default          this repo's CUDA path; inputs resident in HBM for `value`,
+                   public API `run()` with host buffers for `e2e`.
+  --impl reference the reference algorithm on the host's CPU cores (the
+                   oracle port in oracle/, NumPy, all threads), same workload.
+
+Multi-GPU: launched with torchrun (one rank per GPU), the grid is split in
+x-slabs (paper_2010_10248_b200.slabs) with a depth-k*R halo exchange over
+NCCL; value = all updates / max-over-ranks device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GPts/s (grid-point updates/s), 512^3 acoustic so=8; % of HBM roofline"
+PHYS = 512
+BL = 40
+SHAPE = (PHYS + 2 * BL,) * 3
+H = 10.0
+DT = 0.8e-3
+SO = 8
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cfg2_inputs(seed: int = 2):
+    """Seeded synthetic stand-in for BASELINE configs[1] (no public dataset)."""
+    rng = np.random.default_rng(seed)
+    nz = SHAPE[2]
+    z = np.arange(nz, dtype=np.float64) / (nz - 1)
+    v = (1500.0 + 1000.0 * z)[None, None, :] + rng.normal(0.0, 50.0, SHAPE)
+    src = rng.uniform(0.0, (PHYS - 1) * H, size=(1, 3))
+    xs = np.arange(PHYS) * H + rng.uniform(0.0, 9.99, size=PHYS)
+    ys = np.arange(PHYS) * H + rng.uniform(0.0, 9.99, size=PHYS)
+    X, Y = np.meshgrid(np.clip(xs, 0, (PHYS - 1) * H), np.clip(ys, 0, (PHYS - 1) * H),
+                       indexing="ij")
+    rec = np.stack([X.ravel(), Y.ravel(), np.full(X.size, 20.0)], axis=1)
+    return v, src, rec
+
+
+def make_config(stb, v, src, rec, nt, k):
+    grid = stb.GridSpec(SHAPE, (H, H, H), (-BL * H,) * 3, boundary_layers=BL)
+    return stb.RunConfig(physics="acoustic", grid=grid, space_order=SO, nt=nt, dt=DT,
+                         medium={"velocity": v}, sources=stb.SourceSpec(src, f0=15.0),
+                         receiver_coords=rec,
+                         schedule=stb.ScheduleSpec("gpu", time_height=k))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                self.out = ""
+        return False
+
+    def summary(self, busy_threshold: float = 0.0):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        sm, smax, reasons, power = [], [], set(), []
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [s for s, p in zip(sm, power) if p >= busy_threshold] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+def dist_setup(n_gpus: int):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return rank, world, local
+
+
+def cpu_baseline(steps: int, threads: int):
+    """Oracle port (NumPy, reference IEEE order) on the host cores: a bounded
+    sample of the same cfg2 workload."""
+    from types import SimpleNamespace
+    from oracle import stencil_oracle as so
+    v, src, rec = cfg2_inputs()
+    grid = SimpleNamespace(shape=SHAPE, spacing=(H,) * 3, origin=(-BL * H,) * 3,
+                           boundary_layers=BL)
+    cfg = SimpleNamespace(physics="acoustic", grid=grid, space_order=SO, medium={"velocity": v},
+                          nt=steps, time_ms=None, dt=DT, cfl_safety=0.9,
+                          sources=SimpleNamespace(coords=src, f0=15.0, t0=None, amplitude=1.0,
+                                                  wavelets=None),
+                          receiver_coords=rec, precision=32, damping_decay=None)
+    res = so.run(cfg, threads=threads)
+    npts = int(np.prod(SHAPE))
+    return npts * res.steps / res.elapsed_s / 1e9, res.elapsed_s, res.steps
+
+
+def run_reference_arm(args):
+    rank, world, _ = (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+                      0)
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    # each "step" of this arm is one time step of the oracle over the full
+    # 592^3 grid; warmup steps are run and discarded inside one oracle run
+    total = args.warmup + args.steps
+    from types import SimpleNamespace  # noqa: F401
+    gps, elapsed, steps = cpu_baseline(total, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gps, "unit": "GPts/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * elapsed / max(steps, 1), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "cfg2 (BASELINE configs[1]) 592^3 incl. sponge, acoustic so=8",
+                   "grid": list(SHAPE)},
+        "cpu_baseline": {"value": gps, "unit": "GPts/s", "cores": threads, "kind": "port",
+                         "sample": f"{steps} time steps of cfg2 (592^3) through the oracle "
+                                   f"port (NumPy, {threads} threads, x-chunked; warmup "
+                                   f"included: the port has no warm-up effect)"},
+        "e2e": {"value": gps, "unit": "GPts/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=512)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--k", type=int, default=0, help="fused steps per pass (0 = library default)")
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2010_10248_b200 as stb
+    from paper_2010_10248_b200 import engine, slabs
+
+    rank, world, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    stb._lib.check(stb._lib.lib().stb_set_device(local))
+    v, src, rec = cfg2_inputs()
+    nt_series = args.warmup + args.steps
+    cfg = make_config(stb, v, src, rec, nt_series, args.k)
+    npts = int(np.prod(SHAPE))
+
+    # ------------------------------------------------------------ value
+    runner = slabs.SlabRunner(cfg, rank=rank, world=world)
+    k_used = runner.time_height
+    runner.run(0, args.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        runner.run(args.warmup, args.steps)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    st = runner.stats()
+    dev_ms = torch.tensor([st["run_ms"]], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(dev_ms, op=dist.ReduceOp.MAX)
+    t_ms = float(dev_ms.item())
+    value = npts * args.steps / (t_ms / 1e3) / 1e9
+
+    # ------------------------------------------------------------ roofline
+    peak, peak_src = measured_hbm()
+    bpp = runner.bytes_per_point()
+    steps_per_launch = max(k_used, 1)
+    avg_launch_ms = st["stencil_ms"] / max(st["stencil_launches"], 1)
+    local_pts = runner.local_points()
+    achieved = bpp * local_pts / (avg_launch_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    if os.path.exists(prof):
+        try:
+            p = json.load(open(prof))
+            if p.get("kernel_tag") == runner.kernel_tag():
+                traffic = p.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": runner.kernel_tag(), "peak_source": peak_src,
+                "algorithmic_bytes_per_point_per_launch": bpp,
+                "steps_per_launch": steps_per_launch,
+                "avg_launch_ms": avg_launch_ms,
+                "stencil_share_of_step": st["stencil_ms"] / max(st["run_ms"], 1e-9)}
+    clocks = clk.summary()
+
+    # ------------------------------------------------------------ e2e
+    e2e = None
+    if not args.no_e2e and world == 1:
+        cfg_e = make_config(stb, v, src, rec, args.steps, args.k)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = stb.run(cfg_e)
+        e2e_s = time.perf_counter() - t0
+        h2d = v.nbytes + src.nbytes + rec.nbytes + 8 * sum(SHAPE) + 8 * args.steps
+        d2h = res.fields["u"].nbytes + res.receivers.nbytes
+        e2e = {"value": npts * args.steps / e2e_s / 1e9, "unit": "GPts/s",
+               "h2d_bytes_per_step": int(h2d / args.steps),
+               "d2h_bytes_per_step": int(d2h / args.steps),
+               "wall_s": e2e_s, "api": "paper_2010_10248_b200.run(RunConfig) (host numpy in/out)",
+               "note": "includes model upload, GPU inspector, stepping, field+trace download"}
+        del res
+    elif world > 1:
+        e2e = {"value": None, "unit": "GPts/s", "h2d_bytes_per_step": None,
+               "d2h_bytes_per_step": None, "note": "e2e measured at N=1 only"}
+
+    # ------------------------------------------------------------ cpu baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        gps, el, n = cpu_baseline(args.cpu_steps, threads)
+        cpu = {"value": gps, "unit": "GPts/s", "cores": threads, "kind": "port",
+               "sample": f"{n} time steps of cfg2 (592^3) through the oracle port "
+                         f"(NumPy, {threads} threads), stepping only ({el:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GPts/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "cfg2 (BASELINE configs[1]): 512^3 + 2x40 sponge = 592^3 "
+                                   "computational grid, acoustic so=8, 1 Ricker 15 Hz, "
+                                   "512x512 receivers, dt=0.8 ms",
+                       "grid": list(SHAPE), "time_height": k_used,
+                       "parallelism": f"x-slab{world}",
+                       "l2": "inputs larger than L2 (each 592^3 f32 field ~0.85 GB >> 126 MB)",
+                       "gpts_counting": "computational grid incl. sponge (engine.py:445-447)",
+                       "value_physical_512": PHYS ** 3 * args.steps / (t_ms / 1e3) / 1e9,
+                       "kernel": runner.describe()},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": st["launches"], "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,194 @@
+/*
+ * stb200.h -- C ABI of the B200-native stencil_tb hot path (libstb200.so).
+ *
+ * Drop-in boundary for the reference package `stencil_tb`
+ * (/root/reference/pkg/src/stencil_tb).  The reference is pure Python/NumPy,
+ * so its "plugin interface" for this path is the set of Python functions
+ * named beside each entry point below; the host mirror in
+ * paper_2010_10248_b200/ (Python, same names, same argument meaning and
+ * exceptions) binds these symbols with ctypes.  See INTEGRATION.md for the
+ * binding a stencil_tb maintainer would add.
+ *
+ * Conventions
+ *  - extern "C", POD arguments only; every call returns an int status
+ *    (STB_OK == 0).  No C++ exception or CUDA error crosses the ABI; the
+ *    message of the last failure on the calling thread is returned by
+ *    stb_last_error().
+ *  - Host arrays are caller-owned (NumPy) and C-contiguous; they are read or
+ *    filled only during the call.  Device memory is owned by the opaque
+ *    handles and released by the matching *_destroy.
+ *  - Grid index (i, j, k) <-> C-order (x, y, z), z fastest, exactly the
+ *    interior layout of grid.py:173-225 (the zero halo of the reference is
+ *    realised on the device by zero-fill, never stored on the host side).
+ *  - Calls on one handle are not re-entrant; different handles may be used
+ *    from different threads (one CUDA device per thread via stb_set_device).
+ */
+#ifndef STB200_H
+#define STB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STB_ABI_VERSION 1
+
+/* Status codes; the Python mirror maps them to stencil_tb.errors
+ * (errors.py:4-28). */
+enum {
+  STB_OK = 0,
+  STB_ERR_ARG = 1,      /* ValueError                                      */
+  STB_ERR_DOMAIN = 2,   /* OutOfDomainError  (sparse.py:146-150, 224-238)   */
+  STB_ERR_CUDA = 3,     /* RuntimeError: CUDA failure / no device           */
+  STB_ERR_UNSTABLE = 4, /* StabilityError    (engine.py:354-360)            */
+  STB_ERR_PLAN = 5,     /* InvalidPlanError  (schedule.py:181-199)          */
+  STB_ERR_NOMEM = 6,    /* MemoryError       (grid.py:193-198)              */
+  STB_ERR_CONFIG = 7    /* ConfigError       (engine.py:102-117)            */
+};
+
+int stb_abi_version(void);
+const char* stb_last_error(void);
+int stb_device_count(int* count);
+int stb_set_device(int device);
+
+/* ------------------------------------------------------------------------
+ * Geometry of a regular grid: index i sits at origin + i * spacing
+ * (grid.py:22-74).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int64_t shape[3];
+  double spacing[3];
+  double origin[3];
+} stb_geometry;
+
+/* Trilinear 2x2x2 stencils of n off-grid points, computed on the GPU.
+ * Replaces sparse.interp_stencil (sparse.py:136-173) for many points at
+ * once; with margin >= 0 it also applies validate_coords_in_extent
+ * (sparse.py:224-238) with that margin.  idx_out: n*8*3 int64, w_out: n*8
+ * f64, corners in (bx, by, bz) lexicographic order.  Out-of-extent ->
+ * STB_ERR_DOMAIN (message names the first offending point). */
+int stb_interp_stencils(const double* coords, int64_t n, const stb_geometry* g,
+                        int64_t margin, int64_t* idx_out, double* w_out);
+
+/* ------------------------------------------------------------------------
+ * Inspector: the paper's Alg. 2-3/5 (precompute.py:103-316) on the GPU.
+ * ---------------------------------------------------------------------- */
+typedef struct stb_support_s* stb_support_t;
+
+/* Build the on-grid footprint of n sparse points: stencils, the union of
+ * corners with weight > 0 (keep_zero_weights = 0; find_support "geometric",
+ * precompute.py:114-125) or of all 8 corners (keep_zero_weights = 1),
+ * lexicographic point ids and the per-(x, y) column compression
+ * (build_masks + compress, precompute.py:150-180). */
+int stb_support_create(const double* coords, int64_t n, const stb_geometry* g,
+                       int32_t keep_zero_weights, stb_support_t* out);
+/* Support of an explicit set of grid points (build_masks on a given set,
+ * precompute.py:150-165): duplicates are merged, ids are lexicographic.
+ * Indices outside the interior -> STB_ERR_ARG (ValueError). */
+int stb_support_from_points(const int64_t* points, int64_t n, const stb_geometry* g,
+                            stb_support_t* out);
+/* K = number of affected points, M = number of kept (point, owner) entries. */
+int stb_support_info(stb_support_t s, int64_t* n_affected, int64_t* n_entries);
+/* points: K*3 int64, lexicographically sorted (SparseSupport.points). */
+int stb_support_points(stb_support_t s, int64_t* points);
+/* compress(): nnz_mask (nx*ny int32), _row_ptr (nx*ny+1 int64), _flat_z (K
+ * int64), _flat_id (K int32).  Any pointer may be NULL to skip it. */
+int stb_support_compress(stb_support_t s, int32_t* nnz_mask, int64_t* row_ptr,
+                         int64_t* flat_z, int32_t* flat_id);
+/* build_masks(): dense sm (uint8) and sid (int32, -1 sentinel), nx*ny*nz. */
+int stb_support_masks(stb_support_t s, uint8_t* sm, int32_t* sid);
+/* precompute_receivers() entry table (precompute.py:267-284): M entries
+ * sorted by (point, owner): point (M*3 int64), owner id (M int64), w (M f64). */
+int stb_support_entries(stb_support_t s, int64_t* entry_points, int64_t* entry_owner,
+                        double* entry_w);
+/* decompose_wavefields() (precompute.py:183-206): src_dcmp (nt*K f64) with
+ * src_dcmp[t, id] = sum over kept entries in source-major order of
+ * (w * scale[s]) * wavelets[t, s]; wavelets is (nt_w, n) f64, nt >= nt_w,
+ * rows >= nt_w are zero. */
+int stb_support_decompose(stb_support_t s, const double* wavelets, int64_t nt_w,
+                          const double* scale, int64_t nt, double* src_dcmp);
+int stb_support_destroy(stb_support_t s);
+
+/* ------------------------------------------------------------------------
+ * Propagators: the engine.run hot loop (engine.py:362-376, 426-434).
+ * ---------------------------------------------------------------------- */
+typedef struct stb_prop_s* stb_prop_t;
+
+/* Isotropic acoustic (AcousticModel / acoustic_update, physics.py:124-213).
+ * All coefficients are passed in f64 exactly as the reference computes
+ * them in Python and are rounded once to the field dtype on the device. */
+typedef struct {
+  stb_geometry geom;
+  int32_t space_order;       /* even, 2..16                                  */
+  int32_t precision;         /* 32 or 64                                     */
+  double dt;
+  double center;             /* sum_{active a} w_0 / h_a^2   (physics.py:159) */
+  double coef[3][8];         /* w_r / h_a^2, r = 1..R; 0 on inactive axes    */
+  int32_t active[3];         /* axis has more than one point                 */
+  double dt2;                /* dt**2 as evaluated by the host (Python float) */
+  const double* velocity;    /* per-point velocity (nx*ny*nz, f64): the device
+                                forms m = 1/v**2 and dt2/m (engine.py:243,
+                                physics.py:151) -- or NULL                    */
+  const double* m;           /* per-point squared slowness, used when
+                                velocity == NULL; NULL -> inv_scalar         */
+  double inv_scalar;         /* dt**2/m of a homogeneous medium              */
+  const double* damp[3];     /* per-axis 1/(1+dt*profile_a) tables (f64), or
+                                NULL for no sponge (physics.py:66-115)       */
+} stb_acoustic_desc;
+
+/* Isotropic elastic velocity-stress (ElasticModel, physics.py:216-429). */
+typedef struct {
+  stb_geometry geom;
+  int32_t space_order;
+  int32_t precision;
+  double dt;
+  double d1[3][8];           /* c_j / h_a, j = 1..R; 0 on inactive axes      */
+  int32_t active[3];
+  const double* lam;         /* Lame lambda per point (Pa) or NULL -> scalar */
+  const double* mu;          /* shear modulus per point or NULL -> scalar    */
+  const double* rho;         /* density per point or NULL -> scalar          */
+  double lam_scalar, mu_scalar, rho_scalar;
+  /* the device forms dt/rho, dt*lam, dt*mu, 2*dt*mu (physics.py:251-257);
+     f32(2*dt*mu) == 2*f32(dt*mu) exactly, so only three streams are kept. */
+  const double* damp[3];
+} stb_elastic_desc;
+
+int stb_acoustic_create(const stb_acoustic_desc* d, stb_prop_t* out);
+int stb_elastic_create(const stb_elastic_desc* d, stb_prop_t* out);
+
+/* Sources: fused injection of the decomposed series (Alg. 4/5,
+ * precompute.py:209-252).  Decomposition runs on the device from the
+ * support handle (which must come from the same geometry). */
+int stb_prop_set_sources(stb_prop_t p, stb_support_t s, const double* wavelets,
+                         int64_t nt_w, const double* scale, int64_t nt);
+/* Receivers: per-step trilinear gather (record_receivers, sparse.py:197-207),
+ * summed per receiver with NumPy's 8-wide pairwise order.  Coordinates
+ * must already be validated (margin = boundary_layers, engine.py:282-290). */
+int stb_prop_set_receivers(stb_prop_t p, const double* coords, int64_t nrec);
+
+/* Advance steps [t0, t0 + nsteps), time_height steps fused per HBM pass
+ * (schedule.py:171-207 semantics; 0 = library default).  rec_out, when not
+ * NULL, receives the (nsteps, nrec) f64 traces.  On a non-finite field at a
+ * guard step (multiple of 32) returns STB_ERR_UNSTABLE and sets *bad_step. */
+int stb_prop_run(stb_prop_t p, int64_t t0, int64_t nsteps, int32_t time_height,
+                 double* rec_out, int64_t* bad_step);
+/* Field `field` (acoustic: 0 = u; elastic: 0..8 = vx vy vz txx tyy tzz txy
+ * txz tyz) at time level t (the last two written levels are resident),
+ * copied to a host (nx, ny, nz) array of the handle's dtype. */
+int stb_prop_read_field(stb_prop_t p, int32_t field, int64_t t, void* out);
+/* Zero all time levels (reuse a handle for another shot). */
+int stb_prop_reset(stb_prop_t p);
+/* Device-side timing of the last stb_prop_run (CUDA events on the launching
+ * stream), for bench.py: stencil-kernel launches and their summed duration,
+ * grid-point updates, all kernels launched, and the whole run's duration. */
+int stb_prop_stats(stb_prop_t p, int64_t* launches, double* kernel_ms,
+                   int64_t* updates, int64_t* all_launches, double* run_ms);
+/* Kernel configuration chosen for time_height k (name, bytes per point). */
+int stb_prop_describe(stb_prop_t p, int32_t time_height, char* buf, int64_t buflen);
+int stb_prop_destroy(stb_prop_t p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STB200_H */

@@ -1,0 +1,313 @@
+// Isotropic acoustic propagator (AcousticModel / acoustic_update,
+// physics.py:124-213) with fused sparse operators.
+//
+// Per point, in the reference's exact IEEE order (physics.py:199-213):
+//   lap = u1*c0;  for a in (x,y,z) active: for r in 1..R:
+//                 lap = lap + (u1[+r] + u1[-r]) * c[a][r]
+//   lap = lap*inv;  o = ((u1*2) - u0) + lap;  o = o*fac
+// with fac = min(fx[x], fy[y], fz[z]) == f(1/(1+dt*max_a profile_a)) bit for
+// bit (1-D tables), so the sponge costs no HBM stream.
+#include <cstdio>
+#include <memory>
+#include <sstream>
+
+#include "acoustic_kernels.cuh"
+#include "sparse_ops.cuh"
+
+namespace stb {
+
+namespace {
+
+inline unsigned g1(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
+
+template <typename T>
+__global__ void inv_from_velocity_kernel(const double* __restrict__ v, const double* __restrict__ m,
+                                         double dt2, Dims d, T* __restrict__ inv) {
+  const int64_t n = d.nx * d.ny * d.nz;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double mm;
+    if (v) {
+      const double vi = v[i];
+      mm = rdiv(1.0, rmul(vi, vi));            // engine.py:243: 1/v**2
+    } else {
+      mm = m[i];
+    }
+    const int64_t z = i % d.nz, xy = i / d.nz;
+    inv[xy * d.pitch + z] = from_f64<T>(rdiv(dt2, mm));   // physics.py:151
+  }
+}
+
+template <typename T>
+__global__ void table_kernel(const double* __restrict__ src, int64_t n, T* __restrict__ dst) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src ? from_f64<T>(src[i]) : T(1);
+}
+
+template <typename T>
+__global__ void to_dtype_kernel(const double* __restrict__ src, int64_t n, T* __restrict__ dst) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = from_f64<T>(src[i]);
+}
+
+__global__ void keys_to_offsets_kernel(const int64_t* __restrict__ keys, int64_t n, Dims d,
+                                       int64_t* __restrict__ off) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t k = keys[i];
+  const int64_t z = k % d.nz, xy = k / d.nz;
+  off[i] = xy * d.pitch + z;
+}
+
+__global__ void idx_to_offsets_kernel(const int64_t* __restrict__ idx, int64_t n8, Dims d,
+                                      int64_t* __restrict__ off) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n8) return;
+  off[i] = (idx[i * 3] * d.ny + idx[i * 3 + 1]) * d.pitch + idx[i * 3 + 2];
+}
+
+}  // namespace
+
+template <typename T>
+class AcousticProp final : public stb_prop_s {
+ public:
+  explicit AcousticProp(const stb_acoustic_desc& desc) {
+    R_ = desc.space_order / 2;
+    d_ = make_dims(desc.geom.shape, sizeof(T));
+    geom_ = desc.geom;
+    STB_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    for (int a = 0; a < 3; ++a) active_[a] = desc.active[a] != 0;
+    // coefficients, rounded once to T exactly as NumPy's weak-scalar rule
+    // rounds the Python floats _center/_lap_terms (physics.py:158-164).
+    cf_.c0 = (T)desc.center;
+    for (int a = 0; a < 3; ++a)
+      for (int r = 0; r < 8; ++r) cf_.c[a][r] = (T)desc.coef[a][r];
+    for (int a = 0; a < 3; ++a) cf_.active[a] = active_[a] ? 1 : 0;
+    for (auto& b : lvl_) {
+      b.alloc(d_.total());
+      b.zero(st_);
+    }
+    // inv = dt^2/m
+    if (desc.velocity || desc.m) {
+      const int64_t n = d_.npoints();
+      DevBuf<double> tmp(n);
+      tmp.upload(desc.velocity ? desc.velocity : desc.m, n, st_);
+      inv_.alloc(d_.total());
+      inv_.zero(st_);
+      inv_from_velocity_kernel<T><<<1184, 256, 0, st_>>>(desc.velocity ? tmp.p : nullptr,
+                                                         desc.velocity ? nullptr : tmp.p,
+                                                         desc.dt2, d_, inv_.p);
+      STB_CHECK_LAUNCH();
+      STB_CUDA(cudaStreamSynchronize(st_));
+    } else {
+      inv_scalar_ = (T)desc.inv_scalar;
+    }
+    // damping tables
+    has_fac_ = desc.damp[0] || desc.damp[1] || desc.damp[2];
+    const int64_t n3[3] = {d_.nx, d_.ny, d_.nz};
+    for (int a = 0; a < 3; ++a) {
+      fac_[a].alloc(n3[a]);
+      DevBuf<double> tmp(desc.damp[a] ? n3[a] : 0);
+      if (desc.damp[a]) tmp.upload(desc.damp[a], n3[a], st_);
+      table_kernel<T><<<g1(n3[a]), 256, 0, st_>>>(desc.damp[a] ? tmp.p : nullptr, n3[a],
+                                                  fac_[a].p);
+      STB_CHECK_LAUNCH();
+      STB_CUDA(cudaStreamSynchronize(st_));
+    }
+    STB_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  ~AcousticProp() override {
+    for (auto& e : events_) cudaEventDestroy(e);
+    for (auto& e : run_ev_)
+      if (e) cudaEventDestroy(e);
+    if (st_) cudaStreamDestroy(st_);
+  }
+
+  void set_sources(Support& s, const double* wav, int64_t nt_w, const double* scale,
+                   int64_t nt) override {
+    check_same_geometry(s);
+    K_ = s.K;
+    src_nt_ = nt;
+    if (K_ == 0) return;
+    DevBuf<double> dwav(nt_w * s.n_points), dscale(s.n_points), dc(nt * K_);
+    dwav.upload(wav, nt_w * s.n_points, st_);
+    dscale.upload(scale, s.n_points, st_);
+    support_decompose_dev(s, dwav.p, nt_w, dscale.p, nt, dc.p, st_);
+    series_.alloc(nt * K_);
+    to_dtype_kernel<T><<<g1(nt * K_), 256, 0, st_>>>(dc.p, nt * K_, series_.p);
+    src_off_.alloc(K_);
+    keys_to_offsets_kernel<<<g1(K_), 256, 0, st_>>>(s.keys.p, K_, d_, src_off_.p);
+    STB_CHECK_LAUNCH();
+    STB_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  void set_receivers(const double* coords, int64_t nrec) override {
+    nrec_ = nrec;
+    if (nrec == 0) return;
+    DevBuf<double> dc(nrec * 3);
+    dc.upload(coords, nrec * 3, st_);
+    DevBuf<int64_t> idx(nrec * 24);
+    rec_w_.alloc(nrec * 8);
+    stencils_compute(dc.p, nrec, geom_, -1, idx.p, rec_w_.p, st_);
+    rec_off_.alloc(nrec * 8);
+    idx_to_offsets_kernel<<<g1(nrec * 8), 256, 0, st_>>>(idx.p, nrec * 8, d_, rec_off_.p);
+    STB_CHECK_LAUNCH();
+    STB_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  void run(int64_t t0, int64_t nsteps, int k, double* rec_out, int64_t* bad_step) override {
+    if (bad_step) *bad_step = -1;
+    launches_ = all_launches_ = 0;
+    updates_ = 0;
+    run_ms_ = 0.0;
+    if (nsteps <= 0) return;
+    STB_REQUIRE(k >= 0, STB_ERR_PLAN, "time_height must be >= 1");
+    STB_REQUIRE(K_ == 0 || t0 + nsteps <= src_nt_, STB_ERR_ARG,
+                "run extends past the decomposed source series");
+    // receivers are gathered on the device every step (part of the hot
+    // path); rec_out only controls the final copy to the host
+    if (nrec_ && (int64_t)rec_dev_.n < nsteps * nrec_) rec_dev_.alloc(nsteps * nrec_);
+    std::vector<int64_t> guard_steps;
+    for (int64_t t = t0; t < t0 + nsteps; ++t)
+      if (t > 0 && t % 32 == 0) guard_steps.push_back(t);
+    if ((int64_t)guards_.n < (int64_t)guard_steps.size() + 1) guards_.alloc(guard_steps.size() + 1);
+    guards_.zero(st_);
+    ensure_events(nsteps + 1);
+    STB_CUDA(cudaEventRecord(run_ev_[0], st_));
+    size_t gi = 0;
+    for (int64_t t = t0; t < t0 + nsteps; ++t) {
+      T* dst = lvl_[slot(t)].p;
+      const T* u1 = lvl_[slot(t - 1)].p;
+      const T* u0 = lvl_[slot(t - 2)].p;
+      STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
+      launch_reference_step<T>(R_, st_, u1, u0, dst, inv_.p, inv_scalar_, fac_[0].p, fac_[1].p,
+                               fac_[2].p, has_fac_, cf_, d_);
+      STB_CUDA(cudaEventRecord(events_[2 * launches_ + 1], st_));
+      ++launches_;
+      ++all_launches_;
+      if (gi < guard_steps.size() && guard_steps[gi] == t) {
+        nonfinite_kernel<T><<<1184, 256, 0, st_>>>(dst, d_, guards_.p + gi);
+        STB_CHECK_LAUNCH();
+        ++all_launches_;
+        ++gi;
+      }
+      if (K_) {
+        inject_kernel<T><<<g1(K_), 256, 0, st_>>>(dst, src_off_.p, series_.p + t * K_, K_);
+        STB_CHECK_LAUNCH();
+        ++all_launches_;
+      }
+      if (nrec_) {
+        gather_kernel<T><<<g1(nrec_), 256, 0, st_>>>(dst, rec_off_.p, rec_w_.p, nrec_,
+                                                     rec_dev_.p + (t - t0) * nrec_);
+        STB_CHECK_LAUNCH();
+        ++all_launches_;
+      }
+    }
+    STB_CUDA(cudaEventRecord(run_ev_[1], st_));
+    updates_ = nsteps * d_.npoints();
+    if (nrec_ && rec_out) rec_dev_.download(rec_out, nsteps * nrec_, st_);
+    std::vector<int> gh(guard_steps.size() + 1, 0);
+    if (!guard_steps.empty()) guards_.download(gh.data(), guard_steps.size(), st_);
+    STB_CUDA(cudaStreamSynchronize(st_));
+    float rm = 0.f;
+    STB_CUDA(cudaEventElapsedTime(&rm, run_ev_[0], run_ev_[1]));
+    run_ms_ = rm;
+    for (size_t i = 0; i < guard_steps.size(); ++i) {
+      if (gh[i]) {
+        if (bad_step) *bad_step = guard_steps[i];
+        std::ostringstream os;
+        os << "non-finite values in field group 'u' at step " << guard_steps[i];
+        throw Error(STB_ERR_UNSTABLE, os.str());
+      }
+    }
+  }
+
+  void read_field(int field, int64_t t, void* out) override {
+    STB_REQUIRE(field == 0, STB_ERR_ARG, "acoustic handles have one field (u)");
+    const T* src = lvl_[slot(t)].p;
+    STB_CUDA(cudaMemcpy2DAsync(out, d_.nz * sizeof(T), src, d_.pitch * sizeof(T),
+                               d_.nz * sizeof(T), d_.nx * d_.ny, cudaMemcpyDeviceToHost, st_));
+    STB_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  void reset() override {
+    for (auto& b : lvl_) b.zero(st_);
+    STB_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  void stats(int64_t* launches, double* ms, int64_t* updates, int64_t* all_launches,
+             double* run_ms) override {
+    double total = 0;
+    for (int64_t i = 0; i < launches_; ++i) {
+      float e = 0;
+      STB_CUDA(cudaEventElapsedTime(&e, events_[2 * i], events_[2 * i + 1]));
+      total += e;
+    }
+    if (launches) *launches = launches_;
+    if (ms) *ms = total;
+    if (updates) *updates = updates_;
+    if (all_launches) *all_launches = all_launches_;
+    if (run_ms) *run_ms = run_ms_;
+  }
+
+  std::string describe(int k) override {
+    std::ostringstream os;
+    os << "acoustic_reference_step<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
+       << "> k=" << (k < 1 ? 1 : k) << " bytes_per_point=" << 4 * sizeof(T);
+    return os.str();
+  }
+
+ private:
+  int slot(int64_t t) const { return (int)(((t % 3) + 3) % 3); }
+
+  void check_same_geometry(const Support& s) {
+    for (int a = 0; a < 3; ++a)
+      STB_REQUIRE(s.shape[a] == geom_.shape[a], STB_ERR_ARG,
+                  "support was built for a different grid shape");
+  }
+
+  void ensure_events(int64_t n) {
+    for (auto& e : run_ev_)
+      if (!e) STB_CUDA(cudaEventCreate(&e));
+    while ((int64_t)events_.size() < 2 * n) {
+      cudaEvent_t e;
+      STB_CUDA(cudaEventCreate(&e));
+      events_.push_back(e);
+    }
+  }
+
+  int R_ = 1;
+  Dims d_{};
+  stb_geometry geom_{};
+  bool active_[3]{};
+  cudaStream_t st_ = nullptr;
+  AcCoefs<T> cf_{};
+  DevBuf<T> lvl_[3];
+  DevBuf<T> inv_;
+  T inv_scalar_ = T(0);
+  DevBuf<T> fac_[3];
+  bool has_fac_ = false;
+  // sources
+  int64_t K_ = 0, src_nt_ = 0;
+  DevBuf<T> series_;
+  DevBuf<int64_t> src_off_;
+  // receivers
+  int64_t nrec_ = 0;
+  DevBuf<int64_t> rec_off_;
+  DevBuf<double> rec_w_;
+  DevBuf<double> rec_dev_;
+  DevBuf<int> guards_;
+  // timing
+  std::vector<cudaEvent_t> events_;
+  cudaEvent_t run_ev_[2] = {nullptr, nullptr};
+  int64_t launches_ = 0, all_launches_ = 0, updates_ = 0;
+  double run_ms_ = 0.0;
+};
+
+}  // namespace stb
+
+stb_prop_s* make_acoustic(const stb_acoustic_desc& d) {
+  if (d.precision == 32) return new stb::AcousticProp<float>(d);
+  return new stb::AcousticProp<double>(d);
+}

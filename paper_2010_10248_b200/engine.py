@@ -1,0 +1,555 @@
+"""Forward operator on the B200 (mirror of stencil_tb.engine, engine.py:52-577).
+
+``run(config)`` keeps the reference's config semantics (dt/nt resolution,
+sponge decay, source scales, receiver validation, report fields, checksum)
+and executes the time loop in ``libstb200`` (hand-written sm_100a kernels):
+stencil + fused source injection + per-step receiver gather, k steps fused
+per HBM pass.  There is no CPU fallback.
+
+Schedules: the reference's ``naive``/``space``/``wavefront`` kinds all
+produce bitwise-identical wavefields; on the GPU they map
+to the device plan with ``time_height`` fused steps (1 for naive/space), and
+the extra kind ``"gpu"`` lets the library pick k (``time_height=0``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import math
+import os
+import platform
+import struct
+import time
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, InvalidPlanError
+from .grid import GridSpec, fd_weights, staggered_fd_weights
+from .physics import acoustic_coefficients, damping_tables, elastic_coefficients, ricker
+from .precompute import _Handle
+from .sparse import nearest_scales_from_velocity, validate_coords_in_extent
+
+NAN_GUARD_STRIDE = 32
+SNAPSHOT_MAGIC = b"STBSNAP\x00"
+SNAPSHOT_HEADER = struct.Struct("<8sIiiiI")
+SNAPSHOT_HEADER_SIZE = 32
+
+SCHEDULE_KINDS = ("naive", "space", "wavefront", "gpu")
+
+
+@dataclass
+class ScheduleSpec:
+    """engine.py:52-60, plus kind="gpu" (time_height=0 -> library default)."""
+
+    kind: str = "naive"
+    block_shape: tuple[int, int] | None = None
+    tile_shape: tuple[int, int] | None = None
+    time_height: int = 1
+    force_skew: tuple[int, int] | None = None
+
+
+@dataclass
+class SourceSpec:
+    """engine.py:63-79."""
+
+    coords: np.ndarray
+    f0: float = 10.0
+    t0: float | None = None
+    amplitude: float = 1.0
+    wavelets: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.coords = np.atleast_2d(np.asarray(self.coords, dtype=np.float64))
+
+    @property
+    def nsrc(self) -> int:
+        return self.coords.shape[0]
+
+
+@dataclass
+class RunConfig:
+    """engine.py:82-121 (same fields, same ConfigError fields)."""
+
+    physics: str
+    grid: GridSpec
+    space_order: int
+    schedule: ScheduleSpec = dc_field(default_factory=ScheduleSpec)
+    medium: dict = dc_field(default_factory=dict)
+    nt: int | None = None
+    time_ms: float | None = None
+    dt: float | None = None
+    cfl_safety: float = 0.9
+    sources: SourceSpec | None = None
+    receiver_coords: np.ndarray | None = None
+    precision: int = 32
+    threads: int = 1
+    damping_decay: float | None = None
+    validate: bool = False
+
+    def __post_init__(self):
+        if self.physics not in ("acoustic", "elastic"):
+            raise ConfigError("physics", f"must be acoustic or elastic, got {self.physics!r}")
+        if self.space_order % 2 != 0 or not 2 <= self.space_order <= 16:
+            raise ConfigError("space_order", f"must be even in [2, 16], got {self.space_order}")
+        if self.precision not in (32, 64):
+            raise ConfigError("precision", f"must be 32 or 64, got {self.precision}")
+        if self.threads < 1:
+            raise ConfigError("threads", f"must be >= 1, got {self.threads}")
+        if self.nt is None and self.time_ms is None:
+            raise ConfigError("nt", "either nt or time_ms is required")
+        if self.nt is not None and self.nt < 0:
+            raise ConfigError("nt", f"must be >= 0, got {self.nt}")
+        if self.receiver_coords is not None:
+            self.receiver_coords = np.atleast_2d(np.asarray(self.receiver_coords,
+                                                            dtype=np.float64))
+
+    @property
+    def dtype(self):
+        return np.float32 if self.precision == 32 else np.float64
+
+
+@dataclass
+class RunReport:
+    """engine.py:124-150."""
+
+    physics: str
+    grid_shape: tuple[int, int, int]
+    space_order: int
+    precision: int
+    threads: int
+    schedule: dict
+    nt: int
+    dt: float
+    elapsed_s: float
+    precompute_s: float
+    gpoints_per_s: float
+    arithmetic_intensity: float
+    max_abs: float
+    checksum: str
+    nsrc: int
+    nrec: int
+    source_scale_rule: str
+    machine: dict = dc_field(default_factory=dict)
+
+    def to_dict(self) -> dict:
+        out = dict(self.__dict__)
+        out["grid_shape"] = list(self.grid_shape)
+        return out
+
+
+@dataclass
+class RunResult:
+    fields: dict[str, np.ndarray]
+    receivers: np.ndarray | None
+    report: RunReport
+
+
+def medium_velocity_bounds(physics: str, medium: dict) -> float:
+    """engine.py:160-169."""
+    if physics == "acoustic":
+        if "velocity" not in medium:
+            raise ConfigError("medium.velocity", "acoustic runs need a velocity")
+        return float(np.max(medium["velocity"]))
+    for key in ("vp", "vs", "rho"):
+        if key not in medium:
+            raise ConfigError(f"medium.{key}", "elastic runs need vp, vs, rho")
+    return float(np.max(medium["vp"]))
+
+
+def stable_dt(physics: str, grid: GridSpec, v_max: float, space_order: int,
+              safety: float = 0.9) -> float:
+    """Order-aware CFL bound (engine.py:172-195)."""
+    if v_max <= 0.0:
+        raise ValueError(f"v_max must be > 0, got {v_max}")
+    axes = grid.active_axes or (0,)
+    if physics == "acoustic":
+        w = fd_weights(space_order).weights
+        alt = np.cos(np.pi * np.arange(len(w)))
+        g_max = -(w[0] + 2.0 * float(np.sum(w[1:] * alt[1:])))
+        lam = sum(g_max / grid.spacing[a] ** 2 for a in axes)
+        return safety * 2.0 / (v_max * math.sqrt(lam))
+    csum = float(np.sum(np.abs(staggered_fd_weights(space_order))))
+    h = min(grid.spacing[a] for a in axes)
+    return safety * h / (v_max * math.sqrt(len(axes)) * csum)
+
+
+def resolve_steps(config: RunConfig) -> tuple[float, int]:
+    """engine.py:198-208."""
+    v_max = medium_velocity_bounds(config.physics, config.medium)
+    dt = config.dt if config.dt is not None else stable_dt(
+        config.physics, config.grid, v_max, config.space_order, config.cfl_safety)
+    nt = config.nt if config.nt is not None else math.ceil(config.time_ms / 1000.0 / dt)
+    return dt, nt
+
+
+def default_damping_decay(grid: GridSpec, v_max: float) -> float:
+    """engine.py:211-218."""
+    if grid.boundary_layers == 0:
+        return 0.0
+    h = min(grid.spacing[a] for a in grid.active_axes)
+    return 1.5 * v_max / (grid.boundary_layers * h)
+
+
+def arithmetic_intensity(physics: str, space_order: int, precision: int) -> float:
+    """Analytic flops/byte estimate, same formula as engine.py:221-232."""
+    r = space_order // 2
+    item = 4 if precision == 32 else 8
+    if physics == "acoustic":
+        return (3 * (3 * r + 1) + 8) / (5 * item)
+    return (18 * (3 * r - 1) + 45) / (22 * item)
+
+
+def _gpu_time_height(config: RunConfig) -> int:
+    """Map the reference schedule onto the device plan; mirror its legality
+    errors (engine.py:293-305, schedule.py:181-199)."""
+    s = config.schedule
+    if s.kind not in SCHEDULE_KINDS:
+        raise ConfigError("schedule.kind", f"unknown schedule {s.kind!r}")
+    if s.kind in ("naive", "space"):
+        if s.block_shape is not None and min(s.block_shape) < 1:
+            raise InvalidPlanError(f"block shape must be >= 1, got {s.block_shape}")
+        return 1
+    if s.kind == "gpu":
+        if s.time_height < 0:
+            raise InvalidPlanError(f"time_height must be >= 0, got {s.time_height}")
+        return int(s.time_height)
+    # wavefront: same structural checks as make_wavefront_plan
+    if s.tile_shape is None:
+        raise ConfigError("schedule.tile_shape", "wavefront runs need a tile shape")
+    if s.time_height < 1:
+        raise InvalidPlanError(f"time_height must be >= 1, got {s.time_height}")
+    r = config.space_order // 2
+    skew = (r, r) if config.physics == "acoustic" else (2 * r, 2 * r)
+    if s.force_skew is not None:
+        forced = (int(s.force_skew[0]), int(s.force_skew[1]))
+        if config.validate and any(
+                forced[a] < skew[a] and config.grid.shape[a] > 1 for a in (0, 1)):
+            raise InvalidPlanError(
+                f"schedule validation: forced skew {forced} is below the dependence "
+                f"skew {skew}; reads would precede writes")
+        skew = forced
+    for a in (0, 1):
+        if config.grid.shape[a] > 1 and s.tile_shape[a] <= skew[a] * s.time_height:
+            raise InvalidPlanError(
+                f"tile extent {s.tile_shape[a]} on axis {a} must exceed "
+                f"skew*time_height = {skew[a] * s.time_height}")
+    return int(s.time_height)
+
+
+class _Prop:
+    """Owning wrapper of an stb_prop_t."""
+
+    def __init__(self, raw, dtype, fields):
+        self.raw, self.dtype, self.fields = raw, np.dtype(dtype), fields
+
+    def set_sources(self, handle: _Handle, wavelets, scale, nt):
+        wav = np.ascontiguousarray(wavelets, dtype=np.float64)
+        sc = np.ascontiguousarray(scale, dtype=np.float64)
+        _lib.check(_lib.lib().stb_prop_set_sources(self.raw, handle.raw,
+                                                   _lib.dptr(wav.reshape(-1)), wav.shape[0],
+                                                   _lib.dptr(sc), nt))
+
+    def set_receivers(self, coords):
+        c = np.ascontiguousarray(coords, dtype=np.float64)
+        _lib.check(_lib.lib().stb_prop_set_receivers(self.raw, _lib.dptr(c.reshape(-1)),
+                                                     c.shape[0]))
+
+    def run(self, t0, nsteps, k, rec_out=None):
+        bad = C.c_int64(-1)
+        _lib.check(_lib.lib().stb_prop_run(self.raw, t0, nsteps, k,
+                                           _lib.dptr(rec_out.reshape(-1)) if rec_out is not None
+                                           else _lib.dptr(None), C.byref(bad)))
+
+    def read(self, name, t, shape):
+        out = np.empty(shape, dtype=self.dtype)
+        _lib.check(_lib.lib().stb_prop_read_field(self.raw, self.fields.index(name), t,
+                                                  out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def reset(self):
+        _lib.check(_lib.lib().stb_prop_reset(self.raw))
+
+    def stats(self) -> dict:
+        n, ms, up, al, rm = C.c_int64(), C.c_double(), C.c_int64(), C.c_int64(), C.c_double()
+        _lib.check(_lib.lib().stb_prop_stats(self.raw, C.byref(n), C.byref(ms), C.byref(up),
+                                             C.byref(al), C.byref(rm)))
+        return {"stencil_launches": n.value, "stencil_ms": ms.value, "updates": up.value,
+                "launches": al.value, "run_ms": rm.value}
+
+    def describe(self, k):
+        buf = C.create_string_buffer(512)
+        _lib.check(_lib.lib().stb_prop_describe(self.raw, k, buf, 512))
+        return buf.value.decode()
+
+    def __del__(self):
+        raw, self.raw = getattr(self, "raw", None), None
+        if raw and _lib._lib is not None:
+            _lib.lib().stb_prop_destroy(raw)
+
+
+ACOUSTIC_FIELDS = ("u",)
+ELASTIC_FIELDS = ("vx", "vy", "vz", "txx", "tyy", "tzz", "txy", "txz", "tyz")
+
+
+def _as_f64_grid(values, grid: GridSpec, what: str):
+    arr = np.ascontiguousarray(np.asarray(values, dtype=np.float64))
+    if arr.shape != grid.shape:
+        raise ValueError(f"material shape {arr.shape} != grid shape {grid.shape}")
+    return arr
+
+
+def build_propagator(config: RunConfig, dt: float, v_max: float) -> _Prop:
+    """Device model for a config (engine.py:235-255 + physics.py:124-278)."""
+    grid = config.grid
+    decay = (config.damping_decay if config.damping_decay is not None
+             else default_damping_decay(grid, v_max))
+    tables = damping_tables(grid, decay, dt)
+    keep = []
+    if config.physics == "acoustic":
+        d = _lib.AcousticDesc()
+        d.geom = _lib.geometry(grid)
+        d.space_order, d.precision, d.dt = config.space_order, config.precision, dt
+        center, coef = acoustic_coefficients(grid, config.space_order)
+        d.center = center
+        for a in range(3):
+            d.active[a] = int(grid.shape[a] > 1)
+            for r in range(8):
+                d.coef[a][r] = coef[a, r]
+        d.dt2 = dt ** 2
+        vel = config.medium["velocity"]
+        if np.ndim(vel):
+            v = _as_f64_grid(vel, grid, "velocity")
+            vmax = float(np.max(np.abs(v))) if v.size else 0.0
+            if not vmax * vmax < math.inf and np.any(1.0 / v ** 2 <= 0.0):
+                raise ValueError("m must be positive everywhere")   # physics.py:149-150
+            keep.append(v)
+            d.velocity = _lib.dptr(v.reshape(-1))
+        else:
+            m = 1.0 / float(vel) ** 2
+            if m <= 0.0:
+                raise ValueError("m must be positive")
+            d.inv_scalar = dt ** 2 / m
+        if tables is not None:
+            for a in range(3):
+                keep.append(tables[a])
+                d.damp[a] = _lib.dptr(tables[a])
+        raw = C.c_void_p()
+        _lib.check(_lib.lib().stb_acoustic_create(C.byref(d), C.byref(raw)))
+        return _Prop(raw, config.dtype, ACOUSTIC_FIELDS)
+    vp = np.asarray(config.medium["vp"], dtype=np.float64)
+    vs = np.asarray(config.medium["vs"], dtype=np.float64)
+    rho = np.asarray(config.medium["rho"], dtype=np.float64)
+    mu = rho * vs ** 2
+    lam = rho * vp ** 2 - 2.0 * mu
+    if np.any(rho <= 0.0):
+        raise ValueError("rho must be positive")
+    if np.any(mu < 0.0):
+        raise ValueError("mu must be non-negative")
+    if np.any(lam + 2.0 * mu <= 0.0):
+        raise ValueError("lam + 2*mu must be positive")
+    d = _lib.ElasticDesc()
+    d.geom = _lib.geometry(grid)
+    d.space_order, d.precision, d.dt = config.space_order, config.precision, dt
+    d1 = elastic_coefficients(grid, config.space_order)
+    for a in range(3):
+        d.active[a] = int(grid.shape[a] > 1)
+        for j in range(8):
+            d.d1[a][j] = d1[a, j]
+    for name, arr in (("lam", lam), ("mu", mu), ("rho", rho)):
+        if arr.ndim == 0:
+            setattr(d, f"{name}_scalar", float(arr))
+        else:
+            a3 = np.ascontiguousarray(np.broadcast_to(arr, grid.shape), dtype=np.float64)
+            keep.append(a3)
+            setattr(d, name, _lib.dptr(a3.reshape(-1)))
+    if tables is not None:
+        for a in range(3):
+            keep.append(tables[a])
+            d.damp[a] = _lib.dptr(tables[a])
+    raw = C.c_void_p()
+    _lib.check(_lib.lib().stb_elastic_create(C.byref(d), C.byref(raw)))
+    return _Prop(raw, config.dtype, ELASTIC_FIELDS)
+
+
+def _wavelets(config: RunConfig, dt: float, nt: int) -> np.ndarray:
+    """engine.py:258-272."""
+    spec = config.sources
+    if spec.wavelets is not None:
+        w = np.asarray(spec.wavelets, dtype=np.float64)
+        if w.shape != (nt, spec.nsrc):
+            raise ConfigError("source.wavelets", f"shape must be ({nt}, {spec.nsrc})")
+        return w
+    if nt == 0:
+        return np.zeros((0, spec.nsrc))
+    t0 = spec.t0 if spec.t0 is not None else 1.0 / spec.f0
+    base = ricker(spec.f0, t0, dt, nt, spec.amplitude).samples
+    return np.repeat(base[:, None], spec.nsrc, axis=1)
+
+
+def run(config: RunConfig) -> RunResult:
+    """Execute a configured run on the GPU (engine.py:379-489 semantics)."""
+    _lib.require_device()
+    dt, nt = resolve_steps(config)
+    v_max = medium_velocity_bounds(config.physics, config.medium)
+    k = _gpu_time_height(config)
+    grid = config.grid
+    prop = build_propagator(config, dt, v_max)
+
+    t_pre0 = time.perf_counter()
+    nsrc = nrec = 0
+    spec = config.sources
+    if spec is not None and spec.nsrc > 0:
+        validate_coords_in_extent(spec.coords, grid, what="source")
+        wav = _wavelets(config, dt, nt)
+        if config.physics == "acoustic":
+            scale = nearest_scales_from_velocity(spec.coords, grid, config.medium["velocity"], dt)
+        else:
+            scale = np.full(spec.nsrc, dt)
+        handle = _Handle.from_coords(spec.coords, grid, keep_zero=False)
+        if nt > 0:
+            prop.set_sources(handle, wav, scale, nt)
+        nsrc = spec.nsrc
+    rec = None
+    if config.receiver_coords is not None and len(config.receiver_coords) > 0:
+        rc = config.receiver_coords
+        validate_coords_in_extent(rc, grid, margin_points=grid.boundary_layers,
+                                  what="receiver")
+        prop.set_receivers(rc)
+        nrec = rc.shape[0]
+        rec = np.zeros((nt, nrec), dtype=np.float64)
+    precompute_s = time.perf_counter() - t_pre0
+
+    t0 = time.perf_counter()
+    if nt > 0:
+        prop.run(0, nt, k, rec)
+    elapsed = time.perf_counter() - t0
+
+    names = ACOUSTIC_FIELDS if config.physics == "acoustic" else ELASTIC_FIELDS
+    t_final = nt - 1 if nt > 0 else 0
+    if nt > 0:
+        fields = {n: prop.read(n, t_final, grid.shape) for n in names}
+    else:
+        fields = {n: np.zeros(grid.shape, dtype=config.dtype) for n in names}
+    nf = 1 if config.physics == "acoustic" else 9
+    gpoints = grid.npoints * nt * nf / elapsed / 1e9 if nt > 0 and elapsed > 0 else 0.0
+    max_abs = max((float(np.max(np.abs(a))) for a in fields.values()), default=0.0)
+    digest = hashlib.sha256()
+    for name in sorted(fields):
+        digest.update(name.encode())
+        digest.update(fields[name].tobytes())
+    if rec is not None:
+        digest.update(rec.tobytes())
+    s = config.schedule
+    report = RunReport(
+        physics=config.physics, grid_shape=grid.shape, space_order=config.space_order,
+        precision=config.precision, threads=config.threads,
+        schedule={"kind": s.kind, "block_shape": s.block_shape, "tile_shape": s.tile_shape,
+                  "time_height": s.time_height, "device_plan": prop.describe(k)},
+        nt=nt, dt=dt, elapsed_s=elapsed, precompute_s=precompute_s, gpoints_per_s=gpoints,
+        arithmetic_intensity=arithmetic_intensity(config.physics, config.space_order,
+                                                  config.precision),
+        max_abs=max_abs, checksum=digest.hexdigest(), nsrc=nsrc, nrec=nrec,
+        source_scale_rule=("dt^2/m at nearest grid point" if config.physics == "acoustic"
+                           else "dt"),
+        machine={"platform": platform.platform(),
+                 "processor": platform.processor() or platform.machine(),
+                 "cpus": os.cpu_count(), "device": "cuda"},
+    )
+    return RunResult(fields=fields, receivers=rec, report=report)
+
+
+@dataclass
+class CompareReport:
+    """engine.py:492-517."""
+
+    field_linf: dict
+    field_l2: dict
+    receiver_linf: float | None
+    receiver_l2: float | None
+
+    @property
+    def max_rel_linf(self) -> float:
+        vals = list(self.field_linf.values())
+        if self.receiver_linf is not None:
+            vals.append(self.receiver_linf)
+        return max(vals, default=0.0)
+
+    @property
+    def max_rel_l2(self) -> float:
+        vals = list(self.field_l2.values())
+        if self.receiver_l2 is not None:
+            vals.append(self.receiver_l2)
+        return max(vals, default=0.0)
+
+    def within(self, tolerance: float) -> bool:
+        return self.max_rel_linf <= tolerance
+
+    def lines(self):
+        for name in sorted(self.field_linf):
+            yield f"{name}: rel_linf={self.field_linf[name]:.3e} rel_l2={self.field_l2[name]:.3e}"
+        if self.receiver_linf is not None:
+            yield f"receivers: rel_linf={self.receiver_linf:.3e} rel_l2={self.receiver_l2:.3e}"
+
+
+def _rel_diffs(a: np.ndarray, b: np.ndarray):
+    """rel L-inf and rel L2 in f64 (engine.py:520-533)."""
+    if a.shape != b.shape:
+        raise ValueError(f"shape mismatch {a.shape} vs {b.shape}")
+    x = a.astype(np.float64, copy=False)
+    y = b.astype(np.float64, copy=False)
+    if x.size == 0:
+        return 0.0, 0.0
+    scale = max(float(np.max(np.abs(x))), float(np.max(np.abs(y))))
+    if scale == 0.0:
+        return 0.0, 0.0
+    linf = float(np.max(np.abs(x - y))) / scale
+    l2 = float(np.linalg.norm((x - y).ravel())) / max(np.linalg.norm(x.ravel()),
+                                                       np.linalg.norm(y.ravel()))
+    return linf, l2
+
+
+def compare_runs(a, b) -> CompareReport:
+    """Symmetric relative differences (engine.py:536-550); accepts results
+    of this package, of stencil_tb, or of the oracle."""
+    if set(a.fields) != set(b.fields):
+        raise ValueError(f"field sets differ: {sorted(a.fields)} vs {sorted(b.fields)}")
+    fl, f2 = {}, {}
+    for name in a.fields:
+        fl[name], f2[name] = _rel_diffs(a.fields[name], b.fields[name])
+    if (a.receivers is None) != (b.receivers is None):
+        raise ValueError("one run has receiver data, the other does not")
+    rl = r2 = None
+    if a.receivers is not None:
+        rl, r2 = _rel_diffs(a.receivers, b.receivers)
+    return CompareReport(fl, f2, rl, r2)
+
+
+def save_snapshot(path, array: np.ndarray, time_index: int) -> None:
+    """32-byte header + raw little-endian data (engine.py:553-566)."""
+    arr = np.ascontiguousarray(array)
+    if arr.dtype == np.float32:
+        bits = 32
+    elif arr.dtype == np.float64:
+        bits = 64
+    else:
+        raise ValueError(f"snapshots hold float32/float64, got {arr.dtype}")
+    head = SNAPSHOT_HEADER.pack(SNAPSHOT_MAGIC, bits, *arr.shape, time_index)
+    head += b"\x00" * (SNAPSHOT_HEADER_SIZE - len(head))
+    with open(path, "wb") as fh:
+        fh.write(head)
+        fh.write(arr.astype(arr.dtype.newbyteorder("<"), copy=False).tobytes())
+
+
+def load_snapshot(path):
+    """engine.py:569-577."""
+    with open(path, "rb") as fh:
+        raw = fh.read(SNAPSHOT_HEADER_SIZE)
+        magic, bits, nx, ny, nz, t = SNAPSHOT_HEADER.unpack(raw[:SNAPSHOT_HEADER.size])
+        if magic != SNAPSHOT_MAGIC:
+            raise ValueError(f"{path} is not a snapshot file")
+        dt = np.dtype("<f4") if bits == 32 else np.dtype("<f8")
+        data = np.frombuffer(fh.read(), dtype=dt).reshape(nx, ny, nz)
+    return data.copy(), t

@@ -1,0 +1,102 @@
+"""Host-side physics setup: wavelet, sponge, folded coefficients.
+
+Mirrors the setup half of stencil_tb.physics (physics.py:45-278); the update
+kernels themselves live in ``csrc/acoustic*.cu`` / ``csrc/elastic.cu``.
+All values here are computed in f64 with the reference's operation order and
+handed to the device, which rounds them once to the field dtype.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .grid import GridSpec, fd_weights, staggered_fd_weights
+
+
+@dataclass
+class Wavelet:
+    f0: float
+    t0: float
+    samples: np.ndarray
+
+
+def ricker(f0: float, t0: float, dt: float, nt: int, amplitude: float = 1.0) -> Wavelet:
+    """amplitude * (1 - 2a) * exp(-a), a = (pi f0 (t - t0))^2 (physics.py:54-63)."""
+    if f0 <= 0.0:
+        raise ValueError(f"f0 must be > 0, got {f0}")
+    if nt < 1:
+        raise ValueError(f"nt must be >= 1, got {nt}")
+    tau = np.arange(nt, dtype=np.float64) * dt - t0
+    a = (np.pi * f0 * tau) ** 2
+    return Wavelet(f0=f0, t0=t0, samples=amplitude * (1.0 - 2.0 * a) * np.exp(-a))
+
+
+def damping_profile(n: int, layers: int, decay_max: float) -> np.ndarray:
+    """One axis of the squared-cosine sponge (physics.py:77-84)."""
+    i = np.arange(n, dtype=np.float64)
+    dist = np.minimum(i, n - 1 - i)
+    return np.where(dist < layers, decay_max * np.cos(np.pi * dist / (2.0 * layers)) ** 2, 0.0)
+
+
+def build_damping(grid: GridSpec, decay_max: float) -> np.ndarray:
+    """3-D sponge profile, max over active axes (physics.py:66-89).  API
+    mirror only; the device never stores it (see damping_tables)."""
+    damp = np.zeros(grid.shape, dtype=np.float64)
+    if grid.boundary_layers == 0:
+        return damp
+    for a in grid.active_axes:
+        shape = [1, 1, 1]
+        shape[a] = grid.shape[a]
+        np.maximum(damp, damping_profile(grid.shape[a], grid.boundary_layers,
+                                         decay_max).reshape(shape), out=damp)
+    return damp
+
+
+def damping_tables(grid: GridSpec, decay_max: float, dt: float):
+    """Per-axis factor tables f_a = 1/(1 + dt*profile_a) (f64).
+
+    The reference multiplies by dtype(1/(1+dt*max_a profile_a)) per point
+    (physics.py:107-115).  x -> 1/(1+dt*x) is monotone decreasing and IEEE
+    rounding is monotone, so dtype(min_a f_a) is that factor bit for bit:
+    the device keeps three 1-D tables instead of a 3-D array.  Returns None
+    when the sponge is identically zero (the reference then skips the
+    multiply; the device does too).
+    """
+    if grid.boundary_layers == 0:
+        return None
+    tables = []
+    any_nonzero = False
+    for a in range(3):
+        if a in grid.active_axes:
+            p = damping_profile(grid.shape[a], grid.boundary_layers, decay_max)
+            any_nonzero |= bool(np.any(p))
+        else:
+            p = np.zeros(grid.shape[a])
+        tables.append(np.ascontiguousarray(1.0 / (1.0 + dt * p)))
+    return tables if any_nonzero else None
+
+
+def acoustic_coefficients(grid: GridSpec, space_order: int):
+    """(center, coef[3][8]) exactly as AcousticModel folds them
+    (physics.py:158-164): center = sum_a w0/h_a^2 over active axes (Python
+    float sum from 0), coef[a][r-1] = w_r / h_a^2."""
+    w = fd_weights(space_order).weights
+    R = space_order // 2
+    center = float(sum(w[0] / grid.spacing[a] ** 2 for a in grid.active_axes))
+    coef = np.zeros((3, 8))
+    for a in grid.active_axes:
+        for r in range(1, R + 1):
+            coef[a, r - 1] = float(w[r] / grid.spacing[a] ** 2)
+    return center, coef
+
+
+def elastic_coefficients(grid: GridSpec, space_order: int):
+    """d1[a][j-1] = c_j / h_a (physics.py:259-263)."""
+    c = staggered_fd_weights(space_order)
+    d1 = np.zeros((3, 8))
+    for a in grid.active_axes:
+        for j, cj in enumerate(c):
+            d1[a, j] = float(cj / grid.spacing[a])
+    return d1

@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the C ABI, via the package's public API)
+against the reference's golden outputs and the oracle.
+
+Bar: wavefields and receiver traces BIT-EXACT in EXACT mode (reference IEEE
+op order; sha256 checksum equal to stencil_tb.run's), which implies the
+north-star tolerance (fields / traces within 1e-5 relative L2, asserted too).
+Inspector structures (mask, ids, compression, f64 decomposition) bit-exact.
+"""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import paper_2010_10248_b200 as stb
+from cases import SMALL_CASES, build_case, random_coords, to_config
+from conftest import GOLDEN
+from oracle import stencil_oracle as so
+
+pytestmark = pytest.mark.gpu
+
+L2_TOL = 1e-5   # north_star: fields and traces within 1e-5 relative L2
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def assert_parity(res, fields, receivers, checksum=None):
+    for k, v in fields.items():
+        np.testing.assert_array_equal(res.fields[k], v, err_msg=k)
+    if receivers is not None:
+        np.testing.assert_array_equal(res.receivers, receivers)
+    rep = stb.compare_runs(res, type("R", (), {"fields": fields, "receivers": receivers})())
+    assert rep.max_rel_l2 <= L2_TOL
+    if checksum is not None:
+        assert res.report.checksum == checksum
+
+
+@pytest.mark.parametrize("name", SMALL_CASES)
+def test_run_bitexact_vs_reference(name, golden_runs):
+    arrays, meta = golden_runs
+    res = stb.run(to_config(build_case(name), stb))
+    fields = {k: arrays[f"{name}/field/{k}"] for k in meta[name]["fields"]}
+    assert_parity(res, fields, arrays[f"{name}/receivers"], meta[name]["checksum"])
+    assert res.report.dt == meta[name]["dt"] and res.report.nt == meta[name]["nt"]
+
+
+@pytest.mark.parametrize("name", ["ac_so4_24", "ac_so8_het_32", "ac_so12_28", "ac_aniso_so8",
+                                  "ac_dense_src"])
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_temporal_blocking_is_bitwise_invariant(name, k, golden_runs):
+    """Fusing k steps per HBM pass must not change a single bit."""
+    arrays, meta = golden_runs
+    case = build_case(name)
+    res = stb.run(to_config(case, stb, schedule=stb.ScheduleSpec("gpu", time_height=k)))
+    fields = {kk: arrays[f"{name}/field/{kk}"] for kk in meta[name]["fields"]}
+    assert_parity(res, fields, arrays[f"{name}/receivers"], meta[name]["checksum"])
+
+
+@pytest.mark.slow
+def test_cfg1_full_scale_checksum(golden_big):
+    """BASELINE config 1 in full (148^3 incl. sponge, so=8, nt=200)."""
+    res = stb.run(to_config(build_case("cfg1"), stb))
+    assert res.report.checksum == golden_big["cfg1"]["checksum"]
+    assert sha(res.fields["u"]) == golden_big["cfg1"]["field_sha"]
+    np.testing.assert_array_equal(res.receivers,
+                                  np.load(os.path.join(GOLDEN, "cfg1_receivers.npy")))
+
+
+def test_zero_steps_and_no_sparse_ops():
+    g = stb.GridSpec((24, 24, 24), (10.0,) * 3, boundary_layers=4)
+    cfg = stb.RunConfig(physics="acoustic", grid=g, space_order=4, nt=0,
+                        medium={"velocity": 2500.0}, sources=stb.SourceSpec([[115.0] * 3]),
+                        receiver_coords=[[115.0, 115.0, 75.0], [75.0, 115.0, 115.0]])
+    res = stb.run(cfg)
+    assert not res.fields["u"].any()
+    assert res.receivers.shape == (0, 2)
+    assert res.report.gpoints_per_s == 0.0
+    # no receivers, wavefront-style schedule: the reference crashes here
+    # (SURVEY.md §0.7a); the drop-in must not.
+    cfg = stb.RunConfig(physics="acoustic", grid=g, space_order=4, nt=6,
+                        medium={"velocity": 2500.0}, sources=stb.SourceSpec([[115.0] * 3]),
+                        schedule=stb.ScheduleSpec("wavefront", tile_shape=(12, 12),
+                                                  time_height=2))
+    res = stb.run(cfg)
+    assert res.receivers is None and np.isfinite(res.fields["u"]).all()
+    assert res.fields["u"].any()
+
+
+def test_nan_guard_trips():
+    g = stb.GridSpec((24, 24, 24), (10.0,) * 3)
+    c = [[g.origin[a] + 11 * 10.0 for a in range(3)]]
+    cfg = stb.RunConfig(physics="acoustic", grid=g, space_order=4, nt=64, dt=1.0,
+                        medium={"velocity": 2500.0}, sources=stb.SourceSpec(c, f0=12.0))
+    with pytest.raises(stb.StabilityError):
+        stb.run(cfg)
+
+
+def test_domain_errors():
+    g = stb.GridSpec((24, 24, 24), (10.0,) * 3, boundary_layers=8)
+    cfg = stb.RunConfig(physics="acoustic", grid=g, space_order=4, nt=4,
+                        medium={"velocity": 2500.0}, sources=stb.SourceSpec([[115.0] * 3]),
+                        receiver_coords=[[10.0, 115.0, 115.0]])
+    with pytest.raises(stb.OutOfDomainError):
+        stb.run(cfg)
+    with pytest.raises(stb.OutOfDomainError):
+        stb.interp_stencil((-5.0, 0.0, 0.0), stb.GridSpec((16,) * 3, (10.0,) * 3))
+
+
+def test_repeat_determinism():
+    case = build_case("ac_so8_het_32")
+    a = stb.run(to_config(case, stb))
+    b = stb.run(to_config(case, stb))
+    assert a.report.checksum == b.report.checksum
+
+
+# ------------------------------------------------------------------ inspector
+
+def test_interp_stencils_bitexact(golden_misc):
+    arrays, meta = golden_misc
+    gs = meta["stencil_grid"]
+    grid = stb.GridSpec(tuple(gs["shape"]), tuple(gs["spacing"]), tuple(gs["origin"]))
+    idx, w = stb.sparse.stencils(arrays["stencil/coords"], grid)
+    np.testing.assert_array_equal(idx, arrays["stencil/idx"])
+    np.testing.assert_array_equal(w, arrays["stencil/w"])
+    st = stb.interp_stencil(arrays["stencil/coords"][3], grid)
+    np.testing.assert_array_equal(st.weights, arrays["stencil/w"][3])
+
+
+def test_inspector_small_bitexact(golden_inspector):
+    g = golden_inspector
+    p = "insp_small/"
+    grid = stb.GridSpec((16, 16, 16), (1.0, 1.0, 1.0))
+    src = stb.SourceSet(coords=g[p + "coords"], wavelets=g[p + "wavelets"], scale=g[p + "scale"])
+    sup = stb.compress(stb.build_masks(stb.find_support(src, grid), grid))
+    np.testing.assert_array_equal(sup.points, g[p + "points"])
+    np.testing.assert_array_equal(sup.sm, g[p + "sm"])
+    np.testing.assert_array_equal(sup.sid, g[p + "sid"])
+    np.testing.assert_array_equal(sup.nnz_mask, g[p + "nnz_mask"])
+    np.testing.assert_array_equal(sup._row_ptr, g[p + "_row_ptr"])
+    np.testing.assert_array_equal(sup._flat_z, g[p + "_flat_z"])
+    np.testing.assert_array_equal(sup._flat_id, g[p + "_flat_id"])
+    dc = stb.decompose_wavefields(src, sup, g[p + "src_dcmp"].shape[0])
+    np.testing.assert_array_equal(dc.src_dcmp, g[p + "src_dcmp"])
+    rs = stb.precompute_receivers(stb.ReceiverSet(coords=g[p + "coords"][::2]), grid)
+    np.testing.assert_array_equal(rs.entry_points, g[p + "rec_entry_points"])
+    np.testing.assert_array_equal(rs.entry_rid, g[p + "rec_entry_rid"])
+    np.testing.assert_array_equal(rs.entry_w, g[p + "rec_entry_w"])
+    # build_masks from a plain set (no device handle attached)
+    sup2 = stb.build_masks(set(map(tuple, g[p + "points"].tolist())), grid)
+    np.testing.assert_array_equal(sup2.sid, g[p + "sid"])
+
+
+def test_inspector_numeric_matches_geometric(rng):
+    grid = stb.GridSpec((16, 16, 16), (2.0,) * 3)
+    for _ in range(10):
+        coords = random_coords(rng, grid.shape, grid.spacing, grid.origin, 4,
+                               on_grid_fraction=0.25)
+        wav = rng.normal(size=(5, 4))
+        wav[0] += np.sign(wav[0]) + 0.5
+        src = stb.SourceSet(coords=coords, wavelets=wav, scale=np.ones(4))
+        assert set(stb.find_support(src, grid, "numeric")) == set(stb.find_support(src, grid))
+
+
+def test_inspector_edge_cases():
+    grid = stb.GridSpec((6, 6, 6), (1.0,) * 3)
+    empty = stb.build_masks(set(), grid)
+    assert empty.n_affected == 0 and not empty.sm.any() and np.all(empty.sid == -1)
+    sup = stb.build_masks({(0, 0, 0), (0, 0, 2), (1, 0, 0)}, grid)
+    assert sup.sid[0, 0, 0] == 0 and sup.sid[0, 0, 2] == 1 and sup.sid[1, 0, 0] == 2
+    one = stb.SourceSet(coords=[[5.0, 5.0, 5.0]], wavelets=np.ones((3, 1)))
+    assert set(stb.find_support(one, grid)) == {(5, 5, 5)}
+    two = stb.SourceSet(coords=[[2.5, 2.5, 2.5], [3.5, 2.5, 2.5]], wavelets=np.ones((3, 2)))
+    assert len(stb.find_support(two, grid)) == 12   # face-sharing union
+    with pytest.raises(ValueError):
+        stb.build_masks({(6, 0, 0)}, grid)
+
+
+def test_cfg3_inspector_full_scale_digests(golden_big):
+    meta = golden_big["cfg3_inspector"]
+    rng = np.random.default_rng(meta["seed"])
+    grid = stb.GridSpec((592,) * 3, (10.0,) * 3, (-400.0,) * 3, boundary_layers=40)
+    coords = rng.uniform(0.0, 5110.0, size=(4096, 3))
+    nt, dt = 512, 0.8e-3
+    f0 = rng.uniform(8.0, 20.0, size=4096)
+    t0s = 1.0 / f0 + rng.uniform(0.0, 0.05, size=4096)
+    wav = np.stack([stb.ricker(f, t, dt, nt).samples for f, t in zip(f0, t0s)], axis=1)
+    src = stb.SourceSet(coords=coords, wavelets=wav, scale=np.full(4096, dt ** 2 * 2000.0 ** 2))
+    sup = stb.compress(stb.build_masks(stb.find_support(src, grid), grid))
+    assert sup.n_affected == meta["K"]
+    for key, arr in (("sm", sup.sm), ("sid", sup.sid), ("points", sup.points),
+                     ("nnz_mask", sup.nnz_mask), ("row_ptr", sup._row_ptr),
+                     ("flat_z", sup._flat_z), ("flat_id", sup._flat_id)):
+        assert sha(arr) == meta[key], key
+    assert sha(stb.decompose_wavefields(src, sup, nt).src_dcmp) == meta["src_dcmp"]
+
+
+def test_cfg2_receiver_tables_digests(golden_big):
+    meta = golden_big["cfg2_receivers"]
+    rng = np.random.default_rng(meta["seed"])
+    xs = np.arange(512) * 10.0 + rng.uniform(0.0, 9.99, size=512)
+    ys = np.arange(512) * 10.0 + rng.uniform(0.0, 9.99, size=512)
+    X, Y = np.meshgrid(np.clip(xs, 0, 5110), np.clip(ys, 0, 5110), indexing="ij")
+    rc = np.stack([X.ravel(), Y.ravel(), np.full(X.size, 20.0)], axis=1)
+    grid = stb.GridSpec((592,) * 3, (10.0,) * 3, (-400.0,) * 3, boundary_layers=40)
+    rs = stb.precompute_receivers(stb.ReceiverSet(coords=rc), grid)
+    assert len(rs.entry_w) == meta["M"] and rs.support.n_affected == meta["K"]
+    assert sha(rs.entry_points) == meta["entry_points"]
+    assert sha(rs.entry_rid) == meta["entry_rid"]
+    assert sha(rs.entry_w) == meta["entry_w"]
+    assert sha(rs.support._row_ptr) == meta["row_ptr"]
+
+
+# ------------------------------------------------- oracle at larger sizes
+
+def test_vs_oracle_random_medium_so8():
+    """A config not in the golden set, checked against the (pinned) oracle."""
+    rng = np.random.default_rng(99)
+    shape = (44, 38, 52)
+    v = rng.uniform(1500.0, 3500.0, shape)
+    grid = stb.GridSpec(shape, (10.0, 10.0, 10.0), (5.0, -3.0, 0.0), boundary_layers=7)
+    src = stb.SourceSpec(random_coords(rng, shape, grid.spacing, grid.origin, 5, margin=1),
+                         f0=20.0)
+    rec = random_coords(rng, shape, grid.spacing, grid.origin, 17, margin=8)
+    cfg = stb.RunConfig(physics="acoustic", grid=grid, space_order=8, nt=40,
+                        medium={"velocity": v}, sources=src, receiver_coords=rec)
+    res = stb.run(cfg)
+    ref = so.run(cfg)
+    assert_parity(res, ref.fields, ref.receivers, ref.checksum)
