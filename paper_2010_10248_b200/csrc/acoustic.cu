@@ -11,7 +11,10 @@
 #include <memory>
 #include <sstream>
 
+#include <cstdlib>
+
 #include "acoustic_kernels.cuh"
+#include "acoustic_tiled.cuh"
 #include "sparse_ops.cuh"
 
 namespace stb {
@@ -115,6 +118,7 @@ class AcousticProp final : public stb_prop_s {
       STB_CUDA(cudaStreamSynchronize(st_));
     }
     STB_CUDA(cudaStreamSynchronize(st_));
+    setup_tiled();
   }
 
   ~AcousticProp() override {
@@ -181,15 +185,22 @@ class AcousticProp final : public stb_prop_s {
       const T* u1 = lvl_[slot(t - 1)].p;
       const T* u0 = lvl_[slot(t - 2)].p;
       STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
-      launch_reference_step<T>(R_, st_, u1, u0, dst, inv_.p, inv_scalar_, fac_[0].p, fac_[1].p,
-                               fac_[2].p, has_fac_, cf_, d_);
+      const bool guard_now = gi < guard_steps.size() && guard_steps[gi] == t;
+      if (tiled_) {
+        launch_tiled(slot(t - 1), slot(t - 2), dst, guard_now ? guards_.p + gi : nullptr);
+      } else {
+        launch_reference_step<T>(R_, st_, u1, u0, dst, inv_.p, inv_scalar_, fac_[0].p,
+                                 fac_[1].p, fac_[2].p, has_fac_, cf_, d_);
+      }
       STB_CUDA(cudaEventRecord(events_[2 * launches_ + 1], st_));
       ++launches_;
       ++all_launches_;
-      if (gi < guard_steps.size() && guard_steps[gi] == t) {
-        nonfinite_kernel<T><<<1184, 256, 0, st_>>>(dst, d_, guards_.p + gi);
-        STB_CHECK_LAUNCH();
-        ++all_launches_;
+      if (guard_now) {
+        if (!tiled_) {
+          nonfinite_kernel<T><<<1184, 256, 0, st_>>>(dst, d_, guards_.p + gi);
+          STB_CHECK_LAUNCH();
+          ++all_launches_;
+        }
         ++gi;
       }
       if (K_) {
@@ -253,13 +264,76 @@ class AcousticProp final : public stb_prop_s {
 
   std::string describe(int k) override {
     std::ostringstream os;
-    os << "acoustic_reference_step<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
-       << "> k=" << (k < 1 ? 1 : k) << " bytes_per_point=" << 4 * sizeof(T);
+    if (tiled_)
+      os << "acoustic_tiled_step<f32,R=" << R_ << ",TY=16,TZ=64,PF=2> k=1 cx=" << cx_len_;
+    else
+      os << "acoustic_reference_step<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
+         << "> k=1";
+    os << " requested_k=" << k << " bytes_per_point=" << 4 * sizeof(T);
     return os.str();
   }
 
  private:
   int slot(int64_t t) const { return (int)(((t % 3) + 3) % 3); }
+
+  // The TMA-tiled kernel serves fp32 grids with three active axes; anything
+  // else (fp64, degenerate test grids) runs the reference-order kernel.
+  void setup_tiled() {
+    tiled_ = false;
+    if constexpr (sizeof(T) == 4) {
+      if (!(active_[0] && active_[1] && active_[2])) return;
+      if (R_ != 2 && R_ != 4 && R_ != 6) return;
+      if (const char* e = std::getenv("STB_FORCE_REFERENCE"))
+        if (e[0] == '1') return;
+      const int hz = (R_ + 3) / 4 * 4;
+      for (int l = 0; l < 3; ++l) {
+        map_ext_[l] = make_map3d_f32(lvl_[l].p, d_, 64 + 2 * hz, 16 + 2 * R_, 1);
+        map_tile_[l] = make_map3d_f32(lvl_[l].p, d_, 64, 16, 1);
+      }
+      if (inv_.p) map_inv_ = make_map3d_f32(inv_.p, d_, 64, 16, 1);
+      tcf_.c0 = cf_.c0;
+      for (int r = 0; r < 8; ++r) {
+        tcf_.cx[r] = cf_.c[0][r];
+        tcf_.cy[r] = cf_.c[1][r];
+        tcf_.cz[r] = cf_.c[2][r];
+      }
+      const int64_t ntiles = ((d_.ny + 15) / 16) * ((d_.nz + 63) / 64);
+      int64_t nch = (d_.nx + 149) / 150;   // ~150-plane x chunks (sweep: r01 notes)
+      if (const char* e = std::getenv("STB_NCHUNK")) nch = std::atoi(e);
+      if (nch < 1) nch = 1;
+      cx_len_ = (int)((d_.nx + nch - 1) / nch);
+      if (cx_len_ < 1) cx_len_ = 1;
+      tiled_ = true;
+    }
+  }
+
+  void launch_tiled(int s1, int s0, T* dst, int* nonfinite) {
+    if constexpr (sizeof(T) == 4) {
+      const CUtensorMap& mi = inv_.p ? map_inv_ : map_tile_[s0];
+      switch (R_) {
+        case 2:
+          TiledAcousticLauncher<2, 16, 64, 2>::launch(st_, map_ext_[s1], map_tile_[s0], mi, dst,
+                                                      fac_[0].p, fac_[1].p, fac_[2].p, has_fac_,
+                                                      inv_.p != nullptr, inv_scalar_, tcf_, d_,
+                                                      cx_len_, nonfinite);
+          break;
+        case 4:
+          TiledAcousticLauncher<4, 16, 64, 2>::launch(st_, map_ext_[s1], map_tile_[s0], mi, dst,
+                                                      fac_[0].p, fac_[1].p, fac_[2].p, has_fac_,
+                                                      inv_.p != nullptr, inv_scalar_, tcf_, d_,
+                                                      cx_len_, nonfinite);
+          break;
+        case 6:
+          TiledAcousticLauncher<6, 16, 64, 2>::launch(st_, map_ext_[s1], map_tile_[s0], mi, dst,
+                                                      fac_[0].p, fac_[1].p, fac_[2].p, has_fac_,
+                                                      inv_.p != nullptr, inv_scalar_, tcf_, d_,
+                                                      cx_len_, nonfinite);
+          break;
+        default:
+          throw Error(STB_ERR_ARG, "no tiled kernel for this space order");
+      }
+    }
+  }
 
   void check_same_geometry(const Support& s) {
     for (int a = 0; a < 3; ++a)
@@ -298,6 +372,11 @@ class AcousticProp final : public stb_prop_s {
   DevBuf<double> rec_w_;
   DevBuf<double> rec_dev_;
   DevBuf<int> guards_;
+  // TMA-tiled path
+  bool tiled_ = false;
+  CUtensorMap map_ext_[3]{}, map_tile_[3]{}, map_inv_{};
+  TiledCoefs tcf_{};
+  int cx_len_ = 0;
   // timing
   std::vector<cudaEvent_t> events_;
   cudaEvent_t run_ev_[2] = {nullptr, nullptr};
