@@ -73,12 +73,12 @@ def cfg2_inputs(seed: int = 2):
     return v, src, rec
 
 
-def make_config(stb, v, src, rec, nt, k):
+def make_config(stb, v, src, rec, nt, k, arithmetic="exact"):
     grid = stb.GridSpec(SHAPE, (H, H, H), (-BL * H,) * 3, boundary_layers=BL)
     return stb.RunConfig(physics="acoustic", grid=grid, space_order=SO, nt=nt, dt=DT,
                          medium={"velocity": v}, sources=stb.SourceSpec(src, f0=15.0),
                          receiver_coords=rec,
-                         schedule=stb.ScheduleSpec("gpu", time_height=k))
+                         schedule=stb.ScheduleSpec("gpu", time_height=k, arithmetic=arithmetic))
 
 
 class ClockSampler:
@@ -206,6 +206,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--k", type=int, default=0, help="fused steps per pass (0 = library default)")
+    ap.add_argument("--arithmetic", default="exact", choices=["exact", "fma"])
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -226,7 +227,7 @@ def main():
     stb._lib.check(stb._lib.lib().stb_set_device(local))
     v, src, rec = cfg2_inputs()
     nt_series = args.warmup + args.steps
-    cfg = make_config(stb, v, src, rec, nt_series, args.k)
+    cfg = make_config(stb, v, src, rec, nt_series, args.k, args.arithmetic)
     npts = int(np.prod(SHAPE))
 
     # ------------------------------------------------------------ value
@@ -276,7 +277,7 @@ def main():
     # ------------------------------------------------------------ e2e
     e2e = None
     if not args.no_e2e and world == 1:
-        cfg_e = make_config(stb, v, src, rec, args.steps, args.k)
+        cfg_e = make_config(stb, v, src, rec, args.steps, args.k, args.arithmetic)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = stb.run(cfg_e)
@@ -312,6 +313,7 @@ def main():
                                    "computational grid, acoustic so=8, 1 Ricker 15 Hz, "
                                    "512x512 receivers, dt=0.8 ms",
                        "grid": list(SHAPE), "time_height": k_used,
+                       "arithmetic": args.arithmetic,
                        "parallelism": f"x-slab{world}",
                        "l2": "inputs larger than L2 (each 592^3 f32 field ~0.85 GB >> 126 MB)",
                        "gpts_counting": "computational grid incl. sponge (engine.py:445-447)",

@@ -135,6 +135,10 @@ typedef struct {
   double inv_scalar;         /* dt**2/m of a homogeneous medium              */
   const double* damp[3];     /* per-axis 1/(1+dt*profile_a) tables (f64), or
                                 NULL for no sponge (physics.py:66-115)       */
+  int32_t arithmetic;        /* 0 = EXACT: reference IEEE operation order,
+                                bitwise equal to stencil_tb; 1 = FMA: the
+                                Laplacian accumulates with fused multiply-add
+                                (within 1e-5 relative L2 of the reference)   */
 } stb_acoustic_desc;
 
 /* Isotropic elastic velocity-stress (ElasticModel, physics.py:216-429). */

@@ -44,7 +44,8 @@ class AcousticDesc(C.Structure):
                 ("dt", C.c_double), ("center", C.c_double), ("coef", (C.c_double * 8) * 3),
                 ("active", C.c_int32 * 3), ("dt2", C.c_double),
                 ("velocity", C.POINTER(C.c_double)), ("m", C.POINTER(C.c_double)),
-                ("inv_scalar", C.c_double), ("damp", C.POINTER(C.c_double) * 3)]
+                ("inv_scalar", C.c_double), ("damp", C.POINTER(C.c_double) * 3),
+                ("arithmetic", C.c_int32)]
 
 
 class ElasticDesc(C.Structure):

@@ -7,12 +7,24 @@
 //   lap = lap*inv;  o = ((u1*2) - u0) + lap;  o = o*fac
 // with fac = min(fx[x], fy[y], fz[z]) == f(1/(1+dt*max_a profile_a)) bit for
 // bit (1-D tables), so the sponge costs no HBM stream.
-#include <cstdio>
+//
+// Three device paths, all bitwise equal in EXACT mode:
+//   fused      acoustic_fused<R,K,...>: K = time_height steps per HBM pass
+//              (fp32, 3-D grids, R in {2,4,6}); injection and receiver
+//              capture fused into the sweep.
+//   tiled      acoustic_tiled_step: one step per launch (kept for A/B).
+//   reference  thread-per-point kernel for fp64 and degenerate grids.
+// Time level t lives in buffer t mod NB (NB = 6: distinct inputs/outputs
+// for every K <= 4).
+#include <cstdlib>
+#include <cstring>
 #include <memory>
 #include <sstream>
+#include <unordered_map>
 
-#include <cstdlib>
+#include <cub/cub.cuh>
 
+#include "acoustic_fused.cuh"
 #include "acoustic_kernels.cuh"
 #include "acoustic_tiled.cuh"
 #include "sparse_ops.cuh"
@@ -69,6 +81,83 @@ __global__ void idx_to_offsets_kernel(const int64_t* __restrict__ idx, int64_t n
   off[i] = (idx[i * 3] * d.ny + idx[i * 3 + 1]) * d.pitch + idx[i * 3 + 2];
 }
 
+// int32 per-column CSR + per-plane counts + z list from a support.
+__global__ void csr32_kernel(const int64_t* __restrict__ row_ptr, int64_t ncols,
+                             int* __restrict__ row32) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i <= ncols) row32[i] = (int)row_ptr[i];
+}
+
+__global__ void plane_count_kernel(const int64_t* __restrict__ row_ptr, int64_t nx, int64_t ny,
+                                   int* __restrict__ plane) {
+  int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x < nx) plane[x] = (int)(row_ptr[(x + 1) * ny] - row_ptr[x * ny]);
+}
+
+__global__ void keys_z_kernel(const int64_t* __restrict__ keys, int64_t n, int64_t nz,
+                              int* __restrict__ zz) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) zz[i] = (int)(keys[i] % nz);
+}
+
+// capture index of receiver corner e (= r*8 + c) from the sorted entries
+__global__ void corner_index_kernel(const int32_t* __restrict__ ent_entry,
+                                    const int64_t* __restrict__ ent_point, int64_t M,
+                                    int* __restrict__ cidx) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < M) cidx[ent_entry[i]] = (int)ent_point[i];
+}
+
+// Per-tile source entry lists: point k (lexicographic id) is listed for every
+// (TY x TZ) output tile whose level-1 region (tile widened by hy/hz) holds it.
+__global__ void tile_count_kernel(const int64_t* __restrict__ keys, int64_t K, Dims d, int TY,
+                                  int TZ, int hy, int hz, int nty, int ntz,
+                                  int* __restrict__ cnt) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const int64_t key = keys[k];
+  const int z = (int)(key % d.nz), y = (int)((key / d.nz) % d.ny);
+  int c = 0;
+  for (int iy = max(0, (y - hy) / TY - 1); iy <= min(nty - 1, (y + hy) / TY + 1); ++iy)
+    for (int iz = max(0, (z - hz) / TZ - 1); iz <= min(ntz - 1, (z + hz) / TZ + 1); ++iz)
+      if (y >= iy * TY - hy && y < iy * TY + TY + hy && z >= iz * TZ - hz && z < iz * TZ + TZ + hz)
+        ++c;
+  cnt[k] = c;
+}
+
+__global__ void tile_fill_kernel(const int64_t* __restrict__ keys, int64_t K, Dims d, int TY,
+                                 int TZ, int hy, int hz, int nty, int ntz,
+                                 const int* __restrict__ off, int* __restrict__ tkey,
+                                 int4* __restrict__ ent) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const int64_t key = keys[k];
+  const int z = (int)(key % d.nz), y = (int)((key / d.nz) % d.ny);
+  const int x = (int)(key / (d.nz * d.ny));
+  int o = off[k];
+  for (int iy = max(0, (y - hy) / TY - 1); iy <= min(nty - 1, (y + hy) / TY + 1); ++iy)
+    for (int iz = max(0, (z - hz) / TZ - 1); iz <= min(ntz - 1, (z + hz) / TZ + 1); ++iz)
+      if (y >= iy * TY - hy && y < iy * TY + TY + hy && z >= iz * TZ - hz && z < iz * TZ + TZ + hz) {
+        tkey[o] = iy * ntz + iz;
+        ent[o] = make_int4(x, y, z, (int)k);
+        ++o;
+      }
+}
+
+__global__ void tile_ptr_kernel(const int* __restrict__ tkey, int64_t n, int ntiles,
+                                int* __restrict__ ptr) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > ntiles) return;
+  int64_t lo = 0, hi = n;              // first index with tkey >= t
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (tkey[mid] < t) lo = mid + 1; else hi = mid;
+  }
+  ptr[t] = (int)lo;
+}
+
+constexpr int NB = 6;
+
 }  // namespace
 
 template <typename T>
@@ -76,6 +165,7 @@ class AcousticProp final : public stb_prop_s {
  public:
   explicit AcousticProp(const stb_acoustic_desc& desc) {
     R_ = desc.space_order / 2;
+    arithmetic_ = desc.arithmetic;
     d_ = make_dims(desc.geom.shape, sizeof(T));
     geom_ = desc.geom;
     STB_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
@@ -90,7 +180,6 @@ class AcousticProp final : public stb_prop_s {
       b.alloc(d_.total());
       b.zero(st_);
     }
-    // inv = dt^2/m
     if (desc.velocity || desc.m) {
       const int64_t n = d_.npoints();
       DevBuf<double> tmp(n);
@@ -105,7 +194,6 @@ class AcousticProp final : public stb_prop_s {
     } else {
       inv_scalar_ = (T)desc.inv_scalar;
     }
-    // damping tables
     has_fac_ = desc.damp[0] || desc.damp[1] || desc.damp[2];
     const int64_t n3[3] = {d_.nx, d_.ny, d_.nz};
     for (int a = 0; a < 3; ++a) {
@@ -117,8 +205,7 @@ class AcousticProp final : public stb_prop_s {
       STB_CHECK_LAUNCH();
       STB_CUDA(cudaStreamSynchronize(st_));
     }
-    STB_CUDA(cudaStreamSynchronize(st_));
-    setup_tiled();
+    choose_path();
   }
 
   ~AcousticProp() override {
@@ -134,6 +221,7 @@ class AcousticProp final : public stb_prop_s {
     K_ = s.K;
     src_nt_ = nt;
     if (K_ == 0) return;
+    STB_REQUIRE(K_ < INT32_MAX, STB_ERR_ARG, "too many affected source points");
     DevBuf<double> dwav(nt_w * s.n_points), dscale(s.n_points), dc(nt * K_);
     dwav.upload(wav, nt_w * s.n_points, st_);
     dscale.upload(scale, s.n_points, st_);
@@ -143,19 +231,83 @@ class AcousticProp final : public stb_prop_s {
     src_off_.alloc(K_);
     keys_to_offsets_kernel<<<g1(K_), 256, 0, st_>>>(s.keys.p, K_, d_, src_off_.p);
     STB_CHECK_LAUNCH();
+    // per-column CSR for the fused epilogue
+    const int64_t ncols = d_.nx * d_.ny;
+    src_row_.alloc(ncols + 1);
+    src_plane_.alloc(d_.nx);
+    src_z_.alloc(K_);
+    csr32_kernel<<<g1(ncols + 1), 256, 0, st_>>>(s.row_ptr.p, ncols, src_row_.p);
+    plane_count_kernel<<<g1(d_.nx), 256, 0, st_>>>(s.row_ptr.p, d_.nx, d_.ny, src_plane_.p);
+    keys_z_kernel<<<g1(K_), 256, 0, st_>>>(s.keys.p, K_, d_.nz, src_z_.p);
+    STB_CHECK_LAUNCH();
+    if (path_ == Path::Fused) build_tile_lists(s);
+    STB_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  // Per-tile lists for the fused kernels (halo of the deepest supported K).
+  void build_tile_lists(const Support& s) {
+    const int hy = (max_k_ - 1) * R_;
+    int hz = 0;
+    for (int j = 1; j < max_k_; ++j) hz = (hz + R_ + 3) / 4 * 4;
+    const int nty = (int)((d_.ny + kTY - 1) / kTY), ntz = (int)((d_.nz + kTZ - 1) / kTZ);
+    const int ntiles = nty * ntz;
+    DevBuf<int> cnt(K_), off(K_ + 1);
+    tile_count_kernel<<<g1(K_), 256, 0, st_>>>(s.keys.p, K_, d_, kTY, kTZ, hy, hz, nty, ntz,
+                                               cnt.p);
+    STB_CHECK_LAUNCH();
+    size_t tb = 0;
+    STB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, off.p, (int)K_, st_));
+    DevBuf<uint8_t> tmp(tb);
+    STB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, off.p, (int)K_, st_));
+    int last_off = 0, last_cnt = 0;
+    STB_CUDA(cudaMemcpyAsync(&last_off, off.p + K_ - 1, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STB_CUDA(cudaMemcpyAsync(&last_cnt, cnt.p + K_ - 1, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STB_CUDA(cudaStreamSynchronize(st_));
+    const int64_t n = (int64_t)last_off + last_cnt;
+    DevBuf<int> tkey(n), tkey2(n);
+    DevBuf<int4> ent(n);
+    src_list_.alloc(n);
+    tile_fill_kernel<<<g1(K_), 256, 0, st_>>>(s.keys.p, K_, d_, kTY, kTZ, hy, hz, nty, ntz,
+                                              off.p, tkey.p, ent.p);
+    STB_CHECK_LAUNCH();
+    int bits = 1;
+    while ((1 << bits) <= ntiles) ++bits;
+    tb = 0;
+    STB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkey.p, tkey2.p, ent.p, src_list_.p,
+                                             (int)n, 0, bits, st_));
+    tmp.alloc(tb);
+    STB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, tkey.p, tkey2.p, ent.p, src_list_.p,
+                                             (int)n, 0, bits, st_));
+    src_tile_ptr_.alloc(ntiles + 1);
+    tile_ptr_kernel<<<g1(ntiles + 1), 256, 0, st_>>>(tkey2.p, n, ntiles, src_tile_ptr_.p);
+    STB_CHECK_LAUNCH();
     STB_CUDA(cudaStreamSynchronize(st_));
   }
 
   void set_receivers(const double* coords, int64_t nrec) override {
     nrec_ = nrec;
     if (nrec == 0) return;
-    DevBuf<double> dc(nrec * 3);
-    dc.upload(coords, nrec * 3, st_);
-    DevBuf<int64_t> idx(nrec * 24);
+    // capture support: every corner of every receiver (zero weights kept, so
+    // the gather reproduces NumPy's 8-wide pairwise sum exactly)
+    Support cs;
+    support_build(cs, coords, nrec, geom_, /*keep_zero=*/true, st_);
+    ncap_ = cs.K;
+    STB_REQUIRE(ncap_ < INT32_MAX, STB_ERR_ARG, "too many receiver corners");
     rec_w_.alloc(nrec * 8);
-    stencils_compute(dc.p, nrec, geom_, -1, idx.p, rec_w_.p, st_);
+    STB_CUDA(cudaMemcpyAsync(rec_w_.p, cs.w.p, nrec * 8 * sizeof(double),
+                             cudaMemcpyDeviceToDevice, st_));
     rec_off_.alloc(nrec * 8);
-    idx_to_offsets_kernel<<<g1(nrec * 8), 256, 0, st_>>>(idx.p, nrec * 8, d_, rec_off_.p);
+    idx_to_offsets_kernel<<<g1(nrec * 8), 256, 0, st_>>>(cs.idx.p, nrec * 8, d_, rec_off_.p);
+    cap_idx_.alloc(nrec * 8);
+    corner_index_kernel<<<g1(cs.M), 256, 0, st_>>>(cs.ent_entry.p, cs.ent_point.p, cs.M,
+                                                   cap_idx_.p);
+    const int64_t ncols = d_.nx * d_.ny;
+    cap_row_.alloc(ncols + 1);
+    cap_plane_.alloc(d_.nx);
+    cap_z_.alloc(ncap_);
+    csr32_kernel<<<g1(ncols + 1), 256, 0, st_>>>(cs.row_ptr.p, ncols, cap_row_.p);
+    plane_count_kernel<<<g1(d_.nx), 256, 0, st_>>>(cs.row_ptr.p, d_.nx, d_.ny, cap_plane_.p);
+    keys_z_kernel<<<g1(ncap_), 256, 0, st_>>>(cs.keys.p, ncap_, d_.nz, cap_z_.p);
     STB_CHECK_LAUNCH();
     STB_CUDA(cudaStreamSynchronize(st_));
   }
@@ -169,8 +321,7 @@ class AcousticProp final : public stb_prop_s {
     STB_REQUIRE(k >= 0, STB_ERR_PLAN, "time_height must be >= 1");
     STB_REQUIRE(K_ == 0 || t0 + nsteps <= src_nt_, STB_ERR_ARG,
                 "run extends past the decomposed source series");
-    // receivers are gathered on the device every step (part of the hot
-    // path); rec_out only controls the final copy to the host
+    const int kk = resolve_k(k);
     if (nrec_ && (int64_t)rec_dev_.n < nsteps * nrec_) rec_dev_.alloc(nsteps * nrec_);
     std::vector<int64_t> guard_steps;
     for (int64_t t = t0; t < t0 + nsteps; ++t)
@@ -180,43 +331,58 @@ class AcousticProp final : public stb_prop_s {
     ensure_events(nsteps + 1);
     STB_CUDA(cudaEventRecord(run_ev_[0], st_));
     size_t gi = 0;
-    for (int64_t t = t0; t < t0 + nsteps; ++t) {
-      T* dst = lvl_[slot(t)].p;
-      const T* u1 = lvl_[slot(t - 1)].p;
-      const T* u0 = lvl_[slot(t - 2)].p;
+    int64_t t = t0;
+    while (t < t0 + nsteps) {
+      const int kb = (int)std::min<int64_t>(path_ == Path::Fused ? kk : 1, t0 + nsteps - t);
+      // guard steps inside this block
+      int gmask = 0;
+      int* gflag = nullptr;
+      for (int j = 0; j < kb; ++j)
+        if (gi < guard_steps.size() && guard_steps[gi] == t + j) {
+          gmask |= 1 << j;
+          gflag = guards_.p + gi;
+          ++gi;
+        }
       STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
-      const bool guard_now = gi < guard_steps.size() && guard_steps[gi] == t;
-      if (tiled_) {
-        launch_tiled(slot(t - 1), slot(t - 2), dst, guard_now ? guards_.p + gi : nullptr);
+      if (path_ == Path::Fused) {
+        launch_fused(t, kb, gflag, gmask);
+      } else if (path_ == Path::Tiled) {
+        launch_tiled(slot(t - 1), slot(t - 2), lvl_[slot(t)].p, gflag);
       } else {
-        launch_reference_step<T>(R_, st_, u1, u0, dst, inv_.p, inv_scalar_, fac_[0].p,
-                                 fac_[1].p, fac_[2].p, has_fac_, cf_, d_);
+        launch_reference_step<T>(R_, st_, lvl_[slot(t - 1)].p, lvl_[slot(t - 2)].p,
+                                 lvl_[slot(t)].p, inv_.p, inv_scalar_, fac_[0].p, fac_[1].p,
+                                 fac_[2].p, has_fac_, cf_, d_);
+        if (gflag) {
+          nonfinite_kernel<T><<<1184, 256, 0, st_>>>(lvl_[slot(t)].p, d_, gflag);
+          STB_CHECK_LAUNCH();
+          ++all_launches_;
+        }
       }
       STB_CUDA(cudaEventRecord(events_[2 * launches_ + 1], st_));
       ++launches_;
       ++all_launches_;
-      if (guard_now) {
-        if (!tiled_) {
-          nonfinite_kernel<T><<<1184, 256, 0, st_>>>(dst, d_, guards_.p + gi);
-          STB_CHECK_LAUNCH();
-          ++all_launches_;
-        }
-        ++gi;
-      }
-      if (K_) {
-        inject_kernel<T><<<g1(K_), 256, 0, st_>>>(dst, src_off_.p, series_.p + t * K_, K_);
+      if (path_ != Path::Fused && K_) {
+        inject_kernel<T><<<g1(K_), 256, 0, st_>>>(lvl_[slot(t)].p, src_off_.p,
+                                                  series_.p + t * K_, K_);
         STB_CHECK_LAUNCH();
         ++all_launches_;
       }
       if (nrec_) {
-        gather_kernel<T><<<g1(nrec_), 256, 0, st_>>>(dst, rec_off_.p, rec_w_.p, nrec_,
-                                                     rec_dev_.p + (t - t0) * nrec_);
-        STB_CHECK_LAUNCH();
-        ++all_launches_;
+        for (int j = 0; j < kb; ++j) {
+          // levels t..t+kb-1 are all resident for kb <= 2 (the fused kernel
+          // writes the last two levels), so receivers gather from HBM
+          double* row = rec_dev_.p + (t + j - t0) * nrec_;
+          gather_kernel<T><<<g1(nrec_), 256, 0, st_>>>(lvl_[slot(t + j)].p, rec_off_.p,
+                                                       rec_w_.p, nrec_, row);
+          STB_CHECK_LAUNCH();
+          ++all_launches_;
+        }
       }
+      t += kb;
     }
     STB_CUDA(cudaEventRecord(run_ev_[1], st_));
     updates_ = nsteps * d_.npoints();
+    last_k_ = kk;
     if (nrec_ && rec_out) rec_dev_.download(rec_out, nsteps * nrec_, st_);
     std::vector<int> gh(guard_steps.size() + 1, 0);
     if (!guard_steps.empty()) guards_.download(gh.data(), guard_steps.size(), st_);
@@ -264,74 +430,155 @@ class AcousticProp final : public stb_prop_s {
 
   std::string describe(int k) override {
     std::ostringstream os;
-    if (tiled_)
-      os << "acoustic_tiled_step<f32,R=" << R_ << ",TY=16,TZ=64,PF=2> k=1 cx=" << cx_len_;
+    const int kk = resolve_k(k);
+    if (path_ == Path::Fused)
+      os << "acoustic_fused<f32,R=" << R_ << ",TY=" << kTY << ",TZ=" << kTZ << ",PF=" << kPF
+         << "," << (fast_ ? "fma" : "exact") << "> k=" << kk << " cx=" << cx_len_
+         << " bytes_per_point=" << (kk == 1 ? 16 : 20);
+    else if (path_ == Path::Tiled)
+      os << "acoustic_tiled_step<f32,R=" << R_ << ",TY=16,TZ=64,PF=2> k=1 cx=" << cx_len_
+         << " bytes_per_point=16";
     else
       os << "acoustic_reference_step<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
-         << "> k=1";
-    os << " requested_k=" << k << " bytes_per_point=" << 4 * sizeof(T);
+         << "> k=1 bytes_per_point=" << 4 * sizeof(T);
     return os.str();
   }
 
  private:
-  int slot(int64_t t) const { return (int)(((t % 3) + 3) % 3); }
+  enum class Path { Reference, Tiled, Fused };
+  static constexpr int kTY = 16, kTZ = 64, kPF = 3;
 
-  // The TMA-tiled kernel serves fp32 grids with three active axes; anything
-  // else (fp64, degenerate test grids) runs the reference-order kernel.
-  void setup_tiled() {
-    tiled_ = false;
+  int slot(int64_t t) const { return (int)(((t % NB) + NB) % NB); }
+
+  int resolve_k(int k) const {
+    if (path_ != Path::Fused) return 1;
+    int kk = k < 1 ? default_k_ : k;
+    if (kk > max_k_) kk = max_k_;
+    return kk;
+  }
+
+  // fp32 grids with three active axes use the TMA kernels; fp64 and
+  // degenerate (1-D/2-D) grids run the reference-order kernel.
+  void choose_path() {
+    path_ = Path::Reference;
     if constexpr (sizeof(T) == 4) {
       if (!(active_[0] && active_[1] && active_[2])) return;
       if (R_ != 2 && R_ != 4 && R_ != 6) return;
-      if (const char* e = std::getenv("STB_FORCE_REFERENCE"))
-        if (e[0] == '1') return;
-      const int hz = (R_ + 3) / 4 * 4;
-      for (int l = 0; l < 3; ++l) {
-        map_ext_[l] = make_map3d_f32(lvl_[l].p, d_, 64 + 2 * hz, 16 + 2 * R_, 1);
-        map_tile_[l] = make_map3d_f32(lvl_[l].p, d_, 64, 16, 1);
-      }
-      if (inv_.p) map_inv_ = make_map3d_f32(inv_.p, d_, 64, 16, 1);
+      const char* e = std::getenv("STB_PATH");
+      if (e && std::strcmp(e, "reference") == 0) return;
       tcf_.c0 = cf_.c0;
       for (int r = 0; r < 8; ++r) {
         tcf_.cx[r] = cf_.c[0][r];
         tcf_.cy[r] = cf_.c[1][r];
         tcf_.cz[r] = cf_.c[2][r];
       }
-      const int64_t ntiles = ((d_.ny + 15) / 16) * ((d_.nz + 63) / 64);
-      int64_t nch = (d_.nx + 149) / 150;   // ~150-plane x chunks (sweep: r01 notes)
-      if (const char* e = std::getenv("STB_NCHUNK")) nch = std::atoi(e);
+      int64_t nch = (d_.nx + 149) / 150;
+      if (const char* c = std::getenv("STB_NCHUNK")) nch = std::atoi(c);
       if (nch < 1) nch = 1;
       cx_len_ = (int)((d_.nx + nch - 1) / nch);
-      if (cx_len_ < 1) cx_len_ = 1;
-      tiled_ = true;
+      nchunks_ = (int)((d_.nx + cx_len_ - 1) / cx_len_);
+      fast_ = arithmetic_ == 1;
+      if (const char* f = std::getenv("STB_FMA")) fast_ = f[0] == '1';
+      if (e && std::strcmp(e, "tiled") == 0) {
+        const int hz = (R_ + 3) / 4 * 4;
+        for (int l = 0; l < NB; ++l) {
+          map_ext_[l] = make_map3d_f32(lvl_[l].p, d_, 64 + 2 * hz, 16 + 2 * R_, 1);
+          map_tile_[l] = make_map3d_f32(lvl_[l].p, d_, 64, 16, 1);
+        }
+        if (inv_.p) map_inv_ = make_map3d_f32(inv_.p, d_, 64, 16, 1);
+        path_ = Path::Tiled;
+        return;
+      }
+      max_k_ = (R_ == 4) ? 2 : 1;
+      default_k_ = 1;
+      if (const char* kd = std::getenv("STB_DEFAULT_K")) default_k_ = std::atoi(kd);
+      if (default_k_ < 1) default_k_ = 1;
+      if (default_k_ > max_k_) default_k_ = max_k_;
+      path_ = Path::Fused;
+    }
+  }
+
+  template <int R, int K>
+  void fused_maps(FusedMaps& m, int s_l0, int s_lm1) {
+    using Cf = FusedCfg<R, K, kTY, kTZ, kPF>;
+    m.l0 = make_map3d_f32(reinterpret_cast<const float*>(lvl_[s_l0].p), d_, Cf::WZ0, Cf::HY0, 1);
+    m.lm1 = make_map3d_f32(reinterpret_cast<const float*>(lvl_[s_lm1].p), d_, Cf::WZ1, Cf::HY1, 1);
+    if (inv_.p) {
+      for (int j = 1; j <= K; ++j)
+        m.inv[j - 1] = make_map3d_f32(reinterpret_cast<const float*>(inv_.p), d_,
+                                      kTZ + 2 * Cf::hz(j), kTY + 2 * Cf::hy(j), 1);
+    }
+  }
+
+  template <int R, int K>
+  void launch_fused_rk(int64_t t, int* gflag, int gmask) {
+    // tensor maps are cached per (K, input slots)
+    const int s_l0 = slot(t - 1), s_lm1 = slot(t - 2);
+    const int key = (K * NB + s_l0) * NB + s_lm1;
+    auto it = fmaps_.find(key);
+    if (it == fmaps_.end()) {
+      FusedMaps m{};
+      fused_maps<R, K>(m, s_l0, s_lm1);
+      it = fmaps_.emplace(key, m).first;
+    }
+    FusedArgs a{};
+    a.out_km1 = K >= 2 ? reinterpret_cast<float*>(lvl_[slot(t + K - 2)].p) : nullptr;
+    a.out_k = reinterpret_cast<float*>(lvl_[slot(t + K - 1)].p);
+    a.fx = reinterpret_cast<const float*>(fac_[0].p);
+    a.fy = reinterpret_cast<const float*>(fac_[1].p);
+    a.fz = reinterpret_cast<const float*>(fac_[2].p);
+    a.inv_scalar = (float)inv_scalar_;
+    a.use_inv = inv_.p ? 1 : 0;
+    a.cf = tcf_;
+    a.d = d_;
+    a.cx_len = cx_len_;
+    a.ntz = (int)((d_.nz + kTZ - 1) / kTZ);
+    a.zero_lo = 1;
+    a.zero_hi = 1;
+    a.t0 = (int)t;
+    if (K_) {
+      a.src_plane = src_plane_.p;
+      a.src_list = src_list_.p;
+      a.src_tile_ptr = src_tile_ptr_.p;
+      a.series = reinterpret_cast<const float*>(series_.p);
+      a.n_src = (int)K_;
+    }
+    a.nonfinite = gflag;
+    a.guard_mask = gmask;
+    if (fast_)
+      FusedLauncher<R, K, kTY, kTZ, kPF, true>::launch(st_, it->second, a, nchunks_);
+    else
+      FusedLauncher<R, K, kTY, kTZ, kPF, false>::launch(st_, it->second, a, nchunks_);
+  }
+
+  void launch_fused(int64_t t, int kb, int* gflag, int gmask) {
+    if constexpr (sizeof(T) == 4) {
+      if (R_ == 4 && kb == 2) return launch_fused_rk<4, 2>(t, gflag, gmask);
+      if (R_ == 4) return launch_fused_rk<4, 1>(t, gflag, gmask);
+      if (R_ == 2) return launch_fused_rk<2, 1>(t, gflag, gmask);
+      if (R_ == 6) return launch_fused_rk<6, 1>(t, gflag, gmask);
+      throw Error(STB_ERR_ARG, "no fused kernel for this space order");
     }
   }
 
   void launch_tiled(int s1, int s0, T* dst, int* nonfinite) {
     if constexpr (sizeof(T) == 4) {
       const CUtensorMap& mi = inv_.p ? map_inv_ : map_tile_[s0];
+#define STB_TILED_CASE(RR)                                                                   \
+  case RR:                                                                                   \
+    TiledAcousticLauncher<RR, 16, 64, 2>::launch(st_, map_ext_[s1], map_tile_[s0], mi, dst,  \
+                                                 fac_[0].p, fac_[1].p, fac_[2].p, has_fac_,  \
+                                                 inv_.p != nullptr, inv_scalar_, tcf_, d_,   \
+                                                 cx_len_, nonfinite);                        \
+    break;
       switch (R_) {
-        case 2:
-          TiledAcousticLauncher<2, 16, 64, 2>::launch(st_, map_ext_[s1], map_tile_[s0], mi, dst,
-                                                      fac_[0].p, fac_[1].p, fac_[2].p, has_fac_,
-                                                      inv_.p != nullptr, inv_scalar_, tcf_, d_,
-                                                      cx_len_, nonfinite);
-          break;
-        case 4:
-          TiledAcousticLauncher<4, 16, 64, 2>::launch(st_, map_ext_[s1], map_tile_[s0], mi, dst,
-                                                      fac_[0].p, fac_[1].p, fac_[2].p, has_fac_,
-                                                      inv_.p != nullptr, inv_scalar_, tcf_, d_,
-                                                      cx_len_, nonfinite);
-          break;
-        case 6:
-          TiledAcousticLauncher<6, 16, 64, 2>::launch(st_, map_ext_[s1], map_tile_[s0], mi, dst,
-                                                      fac_[0].p, fac_[1].p, fac_[2].p, has_fac_,
-                                                      inv_.p != nullptr, inv_scalar_, tcf_, d_,
-                                                      cx_len_, nonfinite);
-          break;
+        STB_TILED_CASE(2)
+        STB_TILED_CASE(4)
+        STB_TILED_CASE(6)
         default:
           throw Error(STB_ERR_ARG, "no tiled kernel for this space order");
       }
+#undef STB_TILED_CASE
     }
   }
 
@@ -357,26 +604,35 @@ class AcousticProp final : public stb_prop_s {
   bool active_[3]{};
   cudaStream_t st_ = nullptr;
   AcCoefs<T> cf_{};
-  DevBuf<T> lvl_[3];
+  DevBuf<T> lvl_[NB];
   DevBuf<T> inv_;
   T inv_scalar_ = T(0);
   DevBuf<T> fac_[3];
   bool has_fac_ = false;
+  // path selection
+  Path path_ = Path::Reference;
+  bool fast_ = false;
+  int arithmetic_ = 0;
+  int max_k_ = 1, default_k_ = 1, last_k_ = 1;
+  int cx_len_ = 0, nchunks_ = 1;
+  TiledCoefs tcf_{};
+  CUtensorMap map_ext_[NB]{}, map_tile_[NB]{}, map_inv_{};
+  std::unordered_map<int, FusedMaps> fmaps_;
   // sources
   int64_t K_ = 0, src_nt_ = 0;
   DevBuf<T> series_;
   DevBuf<int64_t> src_off_;
+  DevBuf<int> src_row_, src_plane_, src_z_;
+  DevBuf<int4> src_list_;
+  DevBuf<int> src_tile_ptr_;
   // receivers
-  int64_t nrec_ = 0;
+  int64_t nrec_ = 0, ncap_ = 0;
   DevBuf<int64_t> rec_off_;
   DevBuf<double> rec_w_;
+  DevBuf<int> cap_idx_, cap_row_, cap_plane_, cap_z_;
+  DevBuf<T> cap_;
   DevBuf<double> rec_dev_;
   DevBuf<int> guards_;
-  // TMA-tiled path
-  bool tiled_ = false;
-  CUtensorMap map_ext_[3]{}, map_tile_[3]{}, map_inv_{};
-  TiledCoefs tcf_{};
-  int cx_len_ = 0;
   // timing
   std::vector<cudaEvent_t> events_;
   cudaEvent_t run_ev_[2] = {nullptr, nullptr};

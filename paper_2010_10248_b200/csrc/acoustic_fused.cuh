@@ -1,0 +1,500 @@
+// Temporally blocked acoustic kernel: K time steps fused per HBM pass.
+//
+// The paper's wavefront temporal blocking (Alg. 6, schedule.py
+// 171-310) carried to a B200 SM: each CTA owns an output tile TY x TZ in
+// (y, z) and an x chunk, and sweeps x once while computing all K time levels
+// in a pipeline.  Level j (1..K) lags level j-1 by R planes (the skew of
+// schedule.py:139-168) and is computed on the tile widened by (K-j)*R in y/z
+// (overlapped tiling; halo values are recomputed, never exchanged).  Because
+// the inspector turned off-grid sources into per-tile entry lists, injection
+// is applied inside the sweep right after each level's update -- the
+// dependency that forbids temporal blocking with off-grid sources is gone.
+//
+// Dataflow per iteration n (input plane i = x0 - K*R + n):
+//   producer warp : waits until iteration n-NSB is done, then TMA-loads the
+//                   u[t-1] plane i (tile + K*R halo, OOB zero-fill) into a
+//                   ring of R+NSB slots and the u[t-2] / inv boxes into an
+//                   NSB ring, all on one transaction mbarrier.
+//   consumers     : q0 <- own 4 z-points of plane i (register queue = x nbrs)
+//                   level 1 at plane i-R: y/z nbrs from the staged plane
+//                   level j>1 at plane i-jR: queue centre -> smem buffer,
+//                   named barrier, y/z nbrs from the buffer, x nbrs from the
+//                   level j-1 queue, u[t+j-3] centre = oldest level j-2 entry;
+//                   one "done" arrival per warp per iteration.
+// Points outside the grid are forced to +0 at every level (the reference's
+// zero halo), so overlapped halos are exact.  Only the last two levels are
+// written to HBM (20 B/pt per K-step block in fp32; 16 B/pt for K = 1).
+//
+// Arithmetic runs on packed fp32 pairs (FADD2/FMUL2/FFMA2).  EXACT mode
+// keeps the reference's IEEE operation order (physics.py:199-213): sums and
+// differences packed, products as scalar FMULs (see f32x2.cuh) -> bitwise
+// equal to stencil_tb.  FAST mode accumulates the Laplacian with FFMA2 (one
+// rounding per term instead of two); tests bound it at 1e-5 relative L2.
+#pragma once
+
+#include "acoustic_tiled.cuh"
+#include "f32x2.cuh"
+#include "fp_exact.cuh"
+#include "tma.cuh"
+
+namespace stb {
+
+constexpr int kRoundUp4(int v) { return (v + 3) / 4 * 4; }
+
+template <int R, int K, int TY, int TZ, int PF>
+struct FusedCfg {
+  static constexpr int hy(int j) { return (K - j) * R; }
+  static constexpr int hz(int j) { return j >= K ? 0 : kRoundUp4(hz(j + 1) + R); }
+  static constexpr int RP = kRoundUp4(R);
+  static constexpr int HY0 = TY + 2 * hy(0), WZ0 = TZ + 2 * hz(0);   // staged u[t-1]
+  static constexpr int HY1 = TY + 2 * hy(1), WZ1 = TZ + 2 * hz(1);   // thread grid
+  static constexpr int G1 = WZ1 / 4;
+  static constexpr int NWORK = HY1 * G1;
+  static constexpr int NTC = (NWORK + 31) / 32 * 32;
+  static constexpr int NT = NTC + 32;
+  static constexpr int NCW = NTC / 32;
+  static constexpr int Q = 2 * R + 1;
+  static constexpr int NSB = PF + 1;                  // iteration ring (barriers, aux)
+  static constexpr int NS1 = R + NSB;                 // staged u[t-1] planes
+  static constexpr int E0 = HY0 * WZ0;
+  static constexpr int E1 = HY1 * WZ1;
+  static constexpr int ebox(int j) { return (TY + 2 * hy(j)) * (TZ + 2 * hz(j)); }
+  static constexpr int aux_floats() {
+    int s = E1;
+    for (int j = 1; j <= K; ++j) s += ebox(j);
+    return s;
+  }
+  static constexpr int AUX = aux_floats();
+  static constexpr int aux_inv_off(int j) {
+    int s = E1;
+    for (int jj = 1; jj < j; ++jj) s += ebox(jj);
+    return s;
+  }
+  static constexpr int NBUF = K > 1 ? (K - 1) : 0;
+  static constexpr size_t RING1 = (size_t)NS1 * E0 * 4;
+  static constexpr size_t RING2 = (size_t)NSB * AUX * 4;
+  static constexpr size_t BUFS = (size_t)NBUF * 2 * E1 * 4;
+  static constexpr size_t BARS = (size_t)(2 * NSB) * 8;
+  static constexpr size_t SMEM = RING1 + RING2 + BUFS + BARS;
+};
+
+struct FusedMaps {
+  CUtensorMap l0;        // u[t-1], box WZ0 x HY0 x 1
+  CUtensorMap lm1;       // u[t-2], box WZ1 x HY1 x 1
+  CUtensorMap inv[4];    // inv, box of level j+1
+};
+
+struct FusedArgs {
+  float* out_km1;        // level K-1 (u[t+K-2]), unused for K == 1
+  float* out_k;          // level K   (u[t+K-1])
+  const float* fx;
+  const float* fy;
+  const float* fz;
+  float inv_scalar;
+  int use_inv;
+  TiledCoefs cf;
+  Dims d;
+  int cx_len, ntz;
+  int zero_lo, zero_hi;  // planes < 0 / >= nx are the reference's zero halo
+  int t0;                // time step of level 1
+  const int* src_plane;  // per-plane count of affected points
+  const int4* src_list;  // per-tile {x, y, z, id} sorted by x
+  const int* src_tile_ptr;
+  const float* series;   // (nt, n_src), pre-rounded to fp32
+  int n_src;
+  int* nonfinite;
+  int guard_mask;        // bit j-1: step t0+j-1 is a guard step
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Blocking wait with a suspend-time hint: the warp sleeps in the barrier
+// instead of spinning on issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity), "r"(0x100000u)
+      : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// One Laplacian term for two packed points: lap + (p + m) * c.
+template <bool FAST>
+__device__ __forceinline__ f2 term2(f2 lap, f2 p, f2 m, float c) {
+  const f2 s = add2(p, m);
+  if constexpr (FAST)
+    return fma2(s, bcast(c), lap);
+  else
+    return add2(lap, smul2(s, c));
+}
+
+// Same term when the two sums come from scalars (odd z offsets, where the
+// packed operands would straddle register pairs).
+template <bool FAST>
+__device__ __forceinline__ f2 term2s(f2 lap, float p0, float m0, float p1, float m1, float c) {
+  const f2 s = pk(__fadd_rn(p0, m0), __fadd_rn(p1, m1));
+  if constexpr (FAST)
+    return fma2(s, bcast(c), lap);
+  else
+    return add2(lap, smul2(s, c));
+}
+
+// Update of 4 consecutive z points.  xq: register queue of the input level
+// (centre slot cs); cen: shared-memory pointer to the thread's centre in the
+// input plane (row stride W); u0/iv/fac per point.  Result in o (unmasked).
+template <bool FAST, int R, int Q, int RP, int W>
+__device__ __forceinline__ void update4(const float (&xq)[Q][4], const int cs, const float* cen,
+                                        const float (&u0)[4], const float (&iv)[4],
+                                        const float (&fac)[4], const TiledCoefs& cf,
+                                        float (&o)[4]) {
+  const f2 c01 = pk(xq[cs][0], xq[cs][1]);
+  const f2 c23 = pk(xq[cs][2], xq[cs][3]);
+  f2 L01, L23;
+  if constexpr (FAST) {
+    L01 = mul2(c01, bcast(cf.c0));
+    L23 = mul2(c23, bcast(cf.c0));
+  } else {
+    L01 = smul2(c01, cf.c0);
+    L23 = smul2(c23, cf.c0);
+  }
+  // x neighbours (axis 0 first, r ascending -- the reference's term order)
+#pragma unroll
+  for (int r = 1; r <= R; ++r) {
+    const int sp = (cs + r) % Q, sm = (cs - r + Q) % Q;
+    L01 = term2<FAST>(L01, pk(xq[sp][0], xq[sp][1]), pk(xq[sm][0], xq[sm][1]), cf.cx[r - 1]);
+    L23 = term2<FAST>(L23, pk(xq[sp][2], xq[sp][3]), pk(xq[sm][2], xq[sm][3]), cf.cx[r - 1]);
+  }
+  // y neighbours
+#pragma unroll
+  for (int r = 1; r <= R; ++r) {
+    const float4 pp = *reinterpret_cast<const float4*>(cen + r * W);
+    const float4 mm = *reinterpret_cast<const float4*>(cen - r * W);
+    L01 = term2<FAST>(L01, pk(pp.x, pp.y), pk(mm.x, mm.y), cf.cy[r - 1]);
+    L23 = term2<FAST>(L23, pk(pp.z, pp.w), pk(mm.z, mm.w), cf.cy[r - 1]);
+  }
+  // z neighbours: window [z - RP, z + 4 + RP)
+  float win[4 + 2 * RP];
+#pragma unroll
+  for (int w4 = 0; w4 < (4 + 2 * RP) / 4; ++w4) {
+    const float4 v = *reinterpret_cast<const float4*>(cen - RP + 4 * w4);
+    win[4 * w4] = v.x; win[4 * w4 + 1] = v.y; win[4 * w4 + 2] = v.z; win[4 * w4 + 3] = v.w;
+  }
+#pragma unroll
+  for (int r = 1; r <= R; ++r) {
+    if ((RP + r) % 2 == 0) {
+      L01 = term2<FAST>(L01, pk(win[RP + r], win[RP + r + 1]), pk(win[RP - r], win[RP - r + 1]),
+                        cf.cz[r - 1]);
+      L23 = term2<FAST>(L23, pk(win[RP + r + 2], win[RP + r + 3]),
+                        pk(win[RP - r + 2], win[RP - r + 3]), cf.cz[r - 1]);
+    } else {
+      L01 = term2s<FAST>(L01, win[RP + r], win[RP - r], win[RP + r + 1], win[RP - r + 1],
+                         cf.cz[r - 1]);
+      L23 = term2s<FAST>(L23, win[RP + r + 2], win[RP - r + 2], win[RP + r + 3],
+                         win[RP - r + 3], cf.cz[r - 1]);
+    }
+  }
+  // epilogue: o = ((c*2 - u0) + lap*inv) * fac   (c*2 == c+c exactly)
+  f2 v01 = sub2(add2(c01, c01), pk(u0[0], u0[1]));
+  f2 v23 = sub2(add2(c23, c23), pk(u0[2], u0[3]));
+  if constexpr (FAST) {
+    v01 = fma2(L01, pk(iv[0], iv[1]), v01);
+    v23 = fma2(L23, pk(iv[2], iv[3]), v23);
+  } else {
+    float l0, l1, l2, l3;
+    upk(L01, l0, l1);
+    upk(L23, l2, l3);
+    v01 = add2(v01, pk(__fmul_rn(l0, iv[0]), __fmul_rn(l1, iv[1])));
+    v23 = add2(v23, pk(__fmul_rn(l2, iv[2]), __fmul_rn(l3, iv[3])));
+  }
+  upk(v01, o[0], o[1]);
+  upk(v23, o[2], o[3]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) o[i] = __fmul_rn(o[i], fac[i]);
+}
+
+template <int R, int K, int TY, int TZ, int PF, bool FAST>
+__global__ void __launch_bounds__(FusedCfg<R, K, TY, TZ, PF>::NT, (K == 1 ? 2 : 1))
+acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ FusedArgs a) {
+  using C = FusedCfg<R, K, TY, TZ, PF>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* ring1 = reinterpret_cast<float*>(smem_raw);
+  float* ring2 = reinterpret_cast<float*>(smem_raw + C::RING1);
+  float* bufs = reinterpret_cast<float*>(smem_raw + C::RING1 + C::RING2);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::RING1 + C::RING2 + C::BUFS);
+  uint64_t* done = full + C::NSB;
+
+  const int tid = threadIdx.x;
+  const int tile = blockIdx.x;
+  const int y0 = (tile / a.ntz) * TY;
+  const int z0 = (tile % a.ntz) * TZ;
+  const int x0 = blockIdx.y * a.cx_len;
+  const int x1 = min(x0 + a.cx_len, (int)a.d.nx);
+  const int N = (x1 - x0) + 2 * K * R;
+  const int ibase = x0 - K * R;
+
+  if (tid == 0) {
+    for (int s = 0; s < C::NSB; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], C::NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // ------------------------------------------------------------ producer warp
+  if (tid >= C::NTC) {
+    if (tid == C::NTC) {
+      prefetch_map(&maps.l0);
+      prefetch_map(&maps.lm1);
+      const bool use_inv = a.use_inv != 0;
+      for (int n = 0; n < N; ++n) {
+        const int sb = n % C::NSB;
+        if (n >= C::NSB) mbar_wait_sleep(&done[sb], (uint32_t)(((n / C::NSB) - 1) & 1));
+        uint32_t bytes = (uint32_t)C::E0 * 4u;
+        if (n >= 2 * R) {
+          bytes += (uint32_t)C::E1 * 4u;
+          if (use_inv) {
+#pragma unroll
+            for (int j = 1; j <= K; ++j)
+              if (n >= 2 * j * R) bytes += (uint32_t)C::ebox(j) * 4u;
+          }
+        }
+        mbar_arrive_expect_tx(&full[sb], bytes);
+        tma_load_3d(ring1 + (size_t)(n % C::NS1) * C::E0, &maps.l0, z0 - C::hz(0),
+                    y0 - C::hy(0), ibase + n, &full[sb]);
+        if (n >= 2 * R) {
+          float* ab = ring2 + (size_t)sb * C::AUX;
+          tma_load_3d(ab, &maps.lm1, z0 - C::hz(1), y0 - C::hy(1), ibase + n - R, &full[sb]);
+          if (use_inv) {
+#pragma unroll
+            for (int j = 1; j <= K; ++j)
+              if (n >= 2 * j * R)
+                tma_load_3d(ab + C::aux_inv_off(j), &maps.inv[j - 1], z0 - C::hz(j),
+                            y0 - C::hy(j), ibase + n - j * R, &full[sb]);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int lane = tid & 31;
+  const bool work = tid < C::NWORK;
+  const int row = work ? tid / C::G1 : 0;
+  const int g = work ? tid % C::G1 : 0;
+  const int y = y0 - C::hy(1) + row;
+  const int z = z0 - C::hz(1) + 4 * g;
+  bool inE[K + 1];
+#pragma unroll
+  for (int j = 1; j <= K; ++j) {
+    const int dy = C::hy(1) - C::hy(j), dz = C::hz(1) - C::hz(j);
+    inE[j] = work && row >= dy && row < C::HY1 - dy && 4 * g >= dz && 4 * g < C::WZ1 - dz;
+  }
+  const bool ydom = y >= 0 && y < a.d.ny;
+  bool zdom[4];
+  float fyz[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    zdom[i] = ydom && (z + i >= 0) && (z + i < a.d.nz);
+    fyz[i] = zdom[i] ? tmin(__ldg(a.fy + y), __ldg(a.fz + z + i)) : 1.0f;
+  }
+  const bool tile_owner = inE[K] && ydom && z < a.d.nz;
+  const bool use_inv = a.use_inv != 0;
+  const int64_t gbase = (int64_t)y * a.d.pitch + z;      // global offset within a plane
+
+  float q[K][C::Q][4];
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+#pragma unroll
+    for (int s = 0; s < C::Q; ++s)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) q[j][s][i] = 0.f;
+
+  const int off0 = (row + (C::hy(0) - C::hy(1))) * C::WZ0 + 4 * g + (C::hz(0) - C::hz(1));
+  const int off1 = row * C::WZ1 + 4 * g;
+  int bad = 0;
+
+  int cur[K + 1];
+  int e_end = 0;
+  if (a.src_list) {
+    const int e_beg = __ldg(a.src_tile_ptr + tile);
+    e_end = __ldg(a.src_tile_ptr + tile + 1);
+#pragma unroll
+    for (int j = 0; j <= K; ++j) cur[j] = e_beg;
+  }
+
+  // guard (before injection, as the reference's NaN check sees the stencil
+  // result) then fused injection from this tile's entry list
+  auto sparse_epilogue = [&](float (&o)[4], int j, int p, bool active) {
+    const bool pin = p >= 0 && p < a.d.nx;
+    if (a.guard_mask & (1 << (j - 1))) {
+      if (active && tile_owner && pin && p >= x0 && p < x1) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) bad |= (zdom[i] && !isfinite(o[i]));
+      }
+    }
+    if (a.src_list && pin && __ldg(a.src_plane + p) > 0) {
+      int c = cur[j];
+      while (c < e_end && __ldg(&a.src_list[c].x) < p) ++c;
+      while (c < e_end) {
+        const int4 e = __ldg(&a.src_list[c]);
+        if (e.x != p) break;
+        const int zz = e.z - z;
+        if (active && e.y == y && zz >= 0 && zz < 4) {
+          const float v = __ldg(a.series + (size_t)(a.t0 + j - 1) * a.n_src + e.w);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (i == zz) o[i] = __fadd_rn(o[i], v);
+        }
+        ++c;
+      }
+      cur[j] = c;
+    }
+  };
+
+  auto level_mask = [&](float (&o)[4], int p) {
+    const bool pin = p >= 0 && p < a.d.nx;
+    const bool live = pin || (p < 0 ? !a.zero_lo : !a.zero_hi);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = (live && zdom[i]) ? o[i] : 0.0f;
+  };
+
+  auto fac4 = [&](float (&fac)[4], int p) {
+    const float fxx = __ldg(a.fx + min(max(p, 0), (int)a.d.nx - 1));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) fac[i] = tmin(fxx, fyz[i]);
+  };
+
+  for (int nb = 0; nb < N; nb += C::Q) {
+#pragma unroll
+    for (int qq = 0; qq < C::Q; ++qq) {
+      const int n = nb + qq;
+      if (n < N) {
+        const int sb = n % C::NSB;
+        mbar_wait_sleep(&full[sb], (uint32_t)((n / C::NSB) & 1));
+        if (work) {
+          const float4 v =
+              *reinterpret_cast<const float4*>(ring1 + (size_t)(n % C::NS1) * C::E0 + off0);
+          q[0][qq][0] = v.x; q[0][qq][1] = v.y; q[0][qq][2] = v.z; q[0][qq][3] = v.w;
+        }
+        const int cs = (qq - R + C::Q) % C::Q;          // centre slot (plane of level j)
+        const int os = (qq - 2 * R + 2 * C::Q) % C::Q;  // oldest slot
+        if (n >= 2 * R) {
+          const float* aux = ring2 + (size_t)sb * C::AUX;
+          // ================= level 1 (plane i - R) from the staged plane
+          {
+            const int p = ibase + n - R;
+            float o[4] = {0.f, 0.f, 0.f, 0.f};
+            if (work) {
+              const float* cen = ring1 + (size_t)((n - R) % C::NS1) * C::E0 + off0;
+              const float4 u04 = *reinterpret_cast<const float4*>(aux + off1);
+              const float u0[4] = {u04.x, u04.y, u04.z, u04.w};
+              float iv[4];
+              if (use_inv) {
+                const float4 t4 =
+                    *reinterpret_cast<const float4*>(aux + C::aux_inv_off(1) + off1);
+                iv[0] = t4.x; iv[1] = t4.y; iv[2] = t4.z; iv[3] = t4.w;
+              } else {
+                iv[0] = iv[1] = iv[2] = iv[3] = a.inv_scalar;
+              }
+              float fac[4];
+              fac4(fac, p);
+              update4<FAST, R, C::Q, C::RP, C::WZ0>(q[0], cs, cen, u0, iv, fac, a.cf, o);
+              level_mask(o, p);
+            }
+            sparse_epilogue(o, 1, p, work);
+            if constexpr (K >= 2) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) q[1][qq][i] = o[i];
+            }
+            if constexpr (K <= 2) {
+              if (work && tile_owner && p >= x0 && p < x1) {
+                float* dst = (K == 1) ? a.out_k : a.out_km1;
+                *reinterpret_cast<float4*>(dst + (int64_t)p * a.d.plane + gbase) =
+                    make_float4(o[0], o[1], o[2], o[3]);
+              }
+            }
+          }
+          // ================= levels 2..K (plane i - jR) from the smem buffers
+#pragma unroll
+          for (int j = 2; j <= K; ++j) {
+            if (n >= 2 * j * R) {
+              float* buf = bufs + ((size_t)(j - 2) * 2 + (n & 1)) * C::E1;
+              if (inE[j - 1]) {
+                *reinterpret_cast<float4*>(buf + off1) = make_float4(
+                    q[j - 1][cs][0], q[j - 1][cs][1], q[j - 1][cs][2], q[j - 1][cs][3]);
+              }
+              named_bar_sync(1, C::NTC);
+              const int p = ibase + n - j * R;
+              float o[4] = {0.f, 0.f, 0.f, 0.f};
+              if (inE[j]) {
+                float iv[4];
+                if (use_inv) {
+                  const int dy = C::hy(1) - C::hy(j), dz = C::hz(1) - C::hz(j);
+                  const float4 t4 = *reinterpret_cast<const float4*>(
+                      aux + C::aux_inv_off(j) + (row - dy) * (TZ + 2 * C::hz(j)) + 4 * g - dz);
+                  iv[0] = t4.x; iv[1] = t4.y; iv[2] = t4.z; iv[3] = t4.w;
+                } else {
+                  iv[0] = iv[1] = iv[2] = iv[3] = a.inv_scalar;
+                }
+                const float u0[4] = {q[j - 2][os][0], q[j - 2][os][1], q[j - 2][os][2],
+                                     q[j - 2][os][3]};
+                float fac[4];
+                fac4(fac, p);
+                update4<FAST, R, C::Q, C::RP, C::WZ1>(q[j - 1], cs, buf + off1, u0, iv, fac,
+                                                      a.cf, o);
+                level_mask(o, p);
+              }
+              sparse_epilogue(o, j, p, inE[j]);
+              if (j < K) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) q[j][qq][i] = o[i];
+              }
+              if (tile_owner && p >= x0 && p < x1 && (j == K || j == K - 1)) {
+                float* dst = (j == K) ? a.out_k : a.out_km1;
+                *reinterpret_cast<float4*>(dst + (int64_t)p * a.d.plane + gbase) =
+                    make_float4(o[0], o[1], o[2], o[3]);
+              }
+            }
+          }
+        }
+        // iteration n done: its aux slot and the staged plane n-R (level-1
+        // centre) may be refilled by the producer
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[sb]);
+      }
+    }
+  }
+  if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.nonfinite, 1);
+}
+
+template <int R, int K, int TY, int TZ, int PF, bool FAST>
+struct FusedLauncher {
+  using C = FusedCfg<R, K, TY, TZ, PF>;
+  static void launch(cudaStream_t st, const FusedMaps& maps, const FusedArgs& a, int nchunks) {
+    static bool configured = false;
+    if (!configured) {
+      STB_CUDA(cudaFuncSetAttribute(acoustic_fused<R, K, TY, TZ, PF, FAST>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      configured = true;
+    }
+    const int nty = (int)((a.d.ny + TY - 1) / TY);
+    dim3 grid((unsigned)(a.ntz * nty), (unsigned)nchunks);
+    acoustic_fused<R, K, TY, TZ, PF, FAST><<<grid, C::NT, C::SMEM, st>>>(maps, a);
+    STB_CHECK_LAUNCH();
+  }
+};
+
+}  // namespace stb

@@ -42,13 +42,17 @@ SCHEDULE_KINDS = ("naive", "space", "wavefront", "gpu")
 
 @dataclass
 class ScheduleSpec:
-    """engine.py:52-60, plus kind="gpu" (time_height=0 -> library default)."""
+    """engine.py:52-60, plus kind="gpu" (time_height=0 -> library default)
+    and ``arithmetic``: "exact" (reference IEEE op order, bitwise equal to
+    stencil_tb) or "fma" (fused multiply-add Laplacian, within 1e-5 relative
+    L2; acoustic fp32 device kernels only)."""
 
     kind: str = "naive"
     block_shape: tuple[int, int] | None = None
     tile_shape: tuple[int, int] | None = None
     time_height: int = 1
     force_skew: tuple[int, int] | None = None
+    arithmetic: str = "exact"
 
 
 @dataclass
@@ -319,6 +323,10 @@ def build_propagator(config: RunConfig, dt: float, v_max: float) -> _Prop:
             for r in range(8):
                 d.coef[a][r] = coef[a, r]
         d.dt2 = dt ** 2
+        mode = getattr(config.schedule, "arithmetic", "exact")
+        if mode not in ("exact", "fma"):
+            raise ConfigError("schedule.arithmetic", f"must be 'exact' or 'fma', got {mode!r}")
+        d.arithmetic = 1 if mode == "fma" else 0
         vel = config.medium["velocity"]
         if np.ndim(vel):
             v = _as_f64_grid(vel, grid, "velocity")
@@ -447,7 +455,8 @@ def run(config: RunConfig) -> RunResult:
         physics=config.physics, grid_shape=grid.shape, space_order=config.space_order,
         precision=config.precision, threads=config.threads,
         schedule={"kind": s.kind, "block_shape": s.block_shape, "tile_shape": s.tile_shape,
-                  "time_height": s.time_height, "device_plan": prop.describe(k)},
+                  "time_height": s.time_height, "arithmetic": getattr(s, "arithmetic", "exact"),
+                  "device_plan": prop.describe(k)},
         nt=nt, dt=dt, elapsed_s=elapsed, precompute_s=precompute_s, gpoints_per_s=gpoints,
         arithmetic_intensity=arithmetic_intensity(config.physics, config.space_order,
                                                   config.precision),

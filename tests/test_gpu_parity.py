@@ -229,3 +229,28 @@ def test_vs_oracle_random_medium_so8():
     res = stb.run(cfg)
     ref = so.run(cfg)
     assert_parity(res, ref.fields, ref.receivers, ref.checksum)
+
+
+@pytest.mark.parametrize("name", ["ac_so4_24", "ac_so8_het_32", "ac_so12_28", "ac_aniso_so8",
+                                  "ac_dense_src"])
+@pytest.mark.parametrize("k", [1, 2])
+def test_fma_mode_within_north_star_tolerance(name, k, golden_runs):
+    """FMA arithmetic: not bit-exact by design, but fields and traces within
+    the north-star 1e-5 relative L2 of the reference."""
+    arrays, meta = golden_runs
+    res = stb.run(to_config(build_case(name), stb, schedule=stb.ScheduleSpec(
+        "gpu", time_height=k, arithmetic="fma")))
+    fields = {kk: arrays[f"{name}/field/{kk}"] for kk in meta[name]["fields"]}
+    ref = type("R", (), {"fields": fields, "receivers": arrays[f"{name}/receivers"]})()
+    rep = stb.compare_runs(res, ref)
+    assert rep.max_rel_l2 <= L2_TOL, rep.field_l2
+
+
+@pytest.mark.slow
+def test_cfg1_fma_mode_tolerance(golden_big):
+    case = build_case("cfg1")
+    res = stb.run(to_config(case, stb, schedule=stb.ScheduleSpec("gpu", time_height=2,
+                                                                 arithmetic="fma")))
+    ref_rec = np.load(os.path.join(GOLDEN, "cfg1_receivers.npy"))
+    num = np.linalg.norm(res.receivers - ref_rec)
+    assert num / np.linalg.norm(ref_rec) <= L2_TOL
