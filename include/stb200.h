@@ -139,6 +139,12 @@ typedef struct {
                                 bitwise equal to stencil_tb; 1 = FMA: the
                                 Laplacian accumulates with fused multiply-add
                                 (within 1e-5 relative L2 of the reference)   */
+  int64_t x_begin;           /* x-slab handles (multi-GPU): the handle holds
+                                global planes [x_begin, x_begin + nx_local);
+                                geom stays the GLOBAL grid (stencils, sponge
+                                tables and supports are global), velocity/m
+                                are the local slab.  nx_local == 0: whole grid */
+  int64_t nx_local;
 } stb_acoustic_desc;
 
 /* Isotropic elastic velocity-stress (ElasticModel, physics.py:216-429). */
@@ -181,6 +187,11 @@ int stb_prop_run(stb_prop_t p, int64_t t0, int64_t nsteps, int32_t time_height,
  * txz tyz) at time level t (the last two written levels are resident),
  * copied to a host (nx, ny, nz) array of the handle's dtype. */
 int stb_prop_read_field(stb_prop_t p, int32_t field, int64_t t, void* out);
+/* Device address of time level t of field `field` (x-slab halo exchange):
+ * *dev points at local plane 0; planes are contiguous blocks of
+ * *plane_elems elements (ny rows of *pitch_elems, z fastest). */
+int stb_prop_level_ptr(stb_prop_t p, int32_t field, int64_t t, void** dev,
+                       int64_t* plane_elems, int64_t* pitch_elems);
 /* Zero all time levels (reuse a handle for another shot). */
 int stb_prop_reset(stb_prop_t p);
 /* Device-side timing of the last stb_prop_run (CUDA events on the launching

@@ -29,7 +29,8 @@ EXPORTS = (
     "stb_support_compress", "stb_support_masks", "stb_support_entries",
     "stb_support_decompose", "stb_support_destroy", "stb_acoustic_create",
     "stb_elastic_create", "stb_prop_set_sources", "stb_prop_set_receivers", "stb_prop_run",
-    "stb_prop_read_field", "stb_prop_reset", "stb_prop_stats", "stb_prop_describe",
+    "stb_prop_read_field", "stb_prop_level_ptr", "stb_prop_reset", "stb_prop_stats",
+    "stb_prop_describe",
     "stb_prop_destroy",
 )
 
@@ -45,7 +46,7 @@ class AcousticDesc(C.Structure):
                 ("active", C.c_int32 * 3), ("dt2", C.c_double),
                 ("velocity", C.POINTER(C.c_double)), ("m", C.POINTER(C.c_double)),
                 ("inv_scalar", C.c_double), ("damp", C.POINTER(C.c_double) * 3),
-                ("arithmetic", C.c_int32)]
+                ("arithmetic", C.c_int32), ("x_begin", C.c_int64), ("nx_local", C.c_int64)]
 
 
 class ElasticDesc(C.Structure):
@@ -86,6 +87,7 @@ def _declare(lib):
         "stb_prop_set_receivers": ([P, pdbl, i64], C.c_int),
         "stb_prop_run": ([P, i64, i64, i32, pdbl, pi64], C.c_int),
         "stb_prop_read_field": ([P, i32, i64, P], C.c_int),
+        "stb_prop_level_ptr": ([P, i32, i64, C.POINTER(P), pi64, pi64], C.c_int),
         "stb_prop_reset": ([P], C.c_int),
         "stb_prop_stats": ([P, pi64, pdbl, pi64, pi64, pdbl], C.c_int),
         "stb_prop_describe": ([P, i32, C.c_char_p, i64], C.c_int),

@@ -239,6 +239,14 @@ STB_API int stb_prop_read_field(stb_prop_t p, int32_t field, int64_t t, void* ou
   })
 }
 
+STB_API int stb_prop_level_ptr(stb_prop_t p, int32_t field, int64_t t, void** dev,
+                               int64_t* plane_elems, int64_t* pitch_elems) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr && dev != nullptr, STB_ERR_ARG, "NULL argument");
+    p->level_ptr(field, t, dev, plane_elems, pitch_elems);
+  })
+}
+
 STB_API int stb_prop_reset(stb_prop_t p) {
   STB_GUARD({
     STB_REQUIRE(p != nullptr, STB_ERR_ARG, "NULL handle");

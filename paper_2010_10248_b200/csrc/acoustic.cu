@@ -74,19 +74,27 @@ __global__ void keys_to_offsets_kernel(const int64_t* __restrict__ keys, int64_t
   off[i] = xy * d.pitch + z;
 }
 
-__global__ void idx_to_offsets_kernel(const int64_t* __restrict__ idx, int64_t n8, Dims d,
-                                      int64_t* __restrict__ off) {
+__global__ void shift_keys_kernel(const int64_t* __restrict__ keys, int64_t n, int64_t shift,
+                                  int64_t* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n8) return;
-  off[i] = (idx[i * 3] * d.ny + idx[i * 3 + 1]) * d.pitch + idx[i * 3 + 2];
+  if (i < n) out[i] = keys[i] - shift;
 }
 
-// int32 per-column CSR + per-plane counts + z list from a support.
-__global__ void csr32_kernel(const int64_t* __restrict__ row_ptr, int64_t ncols,
-                             int* __restrict__ row32) {
+__global__ void idx_to_offsets_slab_kernel(const int64_t* __restrict__ idx, int64_t n8, Dims d,
+                                           int64_t x_begin, int64_t* __restrict__ off,
+                                           int* bad) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i <= ncols) row32[i] = (int)row_ptr[i];
+  if (i >= n8) return;
+  const int64_t x = idx[i * 3] - x_begin;
+  if (x < 0 || x >= d.nx) {
+    atomicExch(bad, 1);
+    off[i] = 0;
+    return;
+  }
+  off[i] = (x * d.ny + idx[i * 3 + 1]) * d.pitch + idx[i * 3 + 2];
 }
+
+
 
 __global__ void plane_count_kernel(const int64_t* __restrict__ row_ptr, int64_t nx, int64_t ny,
                                    int* __restrict__ plane) {
@@ -94,19 +102,7 @@ __global__ void plane_count_kernel(const int64_t* __restrict__ row_ptr, int64_t 
   if (x < nx) plane[x] = (int)(row_ptr[(x + 1) * ny] - row_ptr[x * ny]);
 }
 
-__global__ void keys_z_kernel(const int64_t* __restrict__ keys, int64_t n, int64_t nz,
-                              int* __restrict__ zz) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) zz[i] = (int)(keys[i] % nz);
-}
 
-// capture index of receiver corner e (= r*8 + c) from the sorted entries
-__global__ void corner_index_kernel(const int32_t* __restrict__ ent_entry,
-                                    const int64_t* __restrict__ ent_point, int64_t M,
-                                    int* __restrict__ cidx) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < M) cidx[ent_entry[i]] = (int)ent_point[i];
-}
 
 // Per-tile source entry lists: point k (lexicographic id) is listed for every
 // (TY x TZ) output tile whose level-1 region (tile widened by hy/hz) holds it.
@@ -166,8 +162,15 @@ class AcousticProp final : public stb_prop_s {
   explicit AcousticProp(const stb_acoustic_desc& desc) {
     R_ = desc.space_order / 2;
     arithmetic_ = desc.arithmetic;
-    d_ = make_dims(desc.geom.shape, sizeof(T));
     geom_ = desc.geom;
+    x_begin_ = desc.x_begin;
+    int64_t local_shape[3] = {desc.nx_local > 0 ? desc.nx_local : desc.geom.shape[0],
+                              desc.geom.shape[1], desc.geom.shape[2]};
+    STB_REQUIRE(x_begin_ >= 0 && x_begin_ + local_shape[0] <= desc.geom.shape[0], STB_ERR_ARG,
+                "x slab [x_begin, x_begin + nx_local) leaves the grid");
+    d_ = make_dims(local_shape, sizeof(T));
+    zero_lo_ = x_begin_ == 0;
+    zero_hi_ = x_begin_ + d_.nx == desc.geom.shape[0];
     STB_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     for (int a = 0; a < 3; ++a) active_[a] = desc.active[a] != 0;
     // coefficients, rounded once to T exactly as NumPy's weak-scalar rule
@@ -199,7 +202,8 @@ class AcousticProp final : public stb_prop_s {
     for (int a = 0; a < 3; ++a) {
       fac_[a].alloc(n3[a]);
       DevBuf<double> tmp(desc.damp[a] ? n3[a] : 0);
-      if (desc.damp[a]) tmp.upload(desc.damp[a], n3[a], st_);
+      // the x table is global: take this slab's planes
+      if (desc.damp[a]) tmp.upload(desc.damp[a] + (a == 0 ? x_begin_ : 0), n3[a], st_);
       table_kernel<T><<<g1(n3[a]), 256, 0, st_>>>(desc.damp[a] ? tmp.p : nullptr, n3[a],
                                                   fac_[a].p);
       STB_CHECK_LAUNCH();
@@ -218,41 +222,55 @@ class AcousticProp final : public stb_prop_s {
   void set_sources(Support& s, const double* wav, int64_t nt_w, const double* scale,
                    int64_t nt) override {
     check_same_geometry(s);
-    K_ = s.K;
     src_nt_ = nt;
+    K_ = 0;
+    if (s.K == 0) return;
+    // points of this slab: ids [k_lo, k_hi) of the global lexicographic list
+    const int64_t plane = geom_.shape[1] * geom_.shape[2];
+    std::vector<int64_t> rp_lohi(2);
+    STB_CUDA(cudaMemcpyAsync(&rp_lohi[0], s.row_ptr.p + x_begin_ * geom_.shape[1],
+                             sizeof(int64_t), cudaMemcpyDeviceToHost, st_));
+    STB_CUDA(cudaMemcpyAsync(&rp_lohi[1], s.row_ptr.p + (x_begin_ + d_.nx) * geom_.shape[1],
+                             sizeof(int64_t), cudaMemcpyDeviceToHost, st_));
+    STB_CUDA(cudaStreamSynchronize(st_));
+    const int64_t k_lo = rp_lohi[0], k_hi = rp_lohi[1];
+    K_ = k_hi - k_lo;
     if (K_ == 0) return;
     STB_REQUIRE(K_ < INT32_MAX, STB_ERR_ARG, "too many affected source points");
-    DevBuf<double> dwav(nt_w * s.n_points), dscale(s.n_points), dc(nt * K_);
+    DevBuf<double> dwav(nt_w * s.n_points), dscale(s.n_points), dc(nt * s.K);
     dwav.upload(wav, nt_w * s.n_points, st_);
     dscale.upload(scale, s.n_points, st_);
     support_decompose_dev(s, dwav.p, nt_w, dscale.p, nt, dc.p, st_);
+    DevBuf<double> dloc(nt * K_);
+    STB_CUDA(cudaMemcpy2DAsync(dloc.p, K_ * sizeof(double), dc.p + k_lo, s.K * sizeof(double),
+                               K_ * sizeof(double), nt, cudaMemcpyDeviceToDevice, st_));
     series_.alloc(nt * K_);
-    to_dtype_kernel<T><<<g1(nt * K_), 256, 0, st_>>>(dc.p, nt * K_, series_.p);
+    to_dtype_kernel<T><<<g1(nt * K_), 256, 0, st_>>>(dloc.p, nt * K_, series_.p);
+    // local keys (x shifted to the slab)
+    src_keys_.alloc(K_);
+    shift_keys_kernel<<<g1(K_), 256, 0, st_>>>(s.keys.p + k_lo, K_, x_begin_ * plane,
+                                               src_keys_.p);
     src_off_.alloc(K_);
-    keys_to_offsets_kernel<<<g1(K_), 256, 0, st_>>>(s.keys.p, K_, d_, src_off_.p);
+    keys_to_offsets_kernel<<<g1(K_), 256, 0, st_>>>(src_keys_.p, K_, d_, src_off_.p);
     STB_CHECK_LAUNCH();
-    // per-column CSR for the fused epilogue
-    const int64_t ncols = d_.nx * d_.ny;
-    src_row_.alloc(ncols + 1);
+    // per-plane counts for the fused epilogue (from the global CSR)
     src_plane_.alloc(d_.nx);
-    src_z_.alloc(K_);
-    csr32_kernel<<<g1(ncols + 1), 256, 0, st_>>>(s.row_ptr.p, ncols, src_row_.p);
-    plane_count_kernel<<<g1(d_.nx), 256, 0, st_>>>(s.row_ptr.p, d_.nx, d_.ny, src_plane_.p);
-    keys_z_kernel<<<g1(K_), 256, 0, st_>>>(s.keys.p, K_, d_.nz, src_z_.p);
+    plane_count_kernel<<<g1(d_.nx), 256, 0, st_>>>(s.row_ptr.p + x_begin_ * geom_.shape[1],
+                                                   d_.nx, d_.ny, src_plane_.p);
     STB_CHECK_LAUNCH();
-    if (path_ == Path::Fused) build_tile_lists(s);
+    if (path_ == Path::Fused) build_tile_lists();
     STB_CUDA(cudaStreamSynchronize(st_));
   }
 
   // Per-tile lists for the fused kernels (halo of the deepest supported K).
-  void build_tile_lists(const Support& s) {
+  void build_tile_lists() {
     const int hy = (max_k_ - 1) * R_;
     int hz = 0;
     for (int j = 1; j < max_k_; ++j) hz = (hz + R_ + 3) / 4 * 4;
     const int nty = (int)((d_.ny + kTY - 1) / kTY), ntz = (int)((d_.nz + kTZ - 1) / kTZ);
     const int ntiles = nty * ntz;
     DevBuf<int> cnt(K_), off(K_ + 1);
-    tile_count_kernel<<<g1(K_), 256, 0, st_>>>(s.keys.p, K_, d_, kTY, kTZ, hy, hz, nty, ntz,
+    tile_count_kernel<<<g1(K_), 256, 0, st_>>>(src_keys_.p, K_, d_, kTY, kTZ, hy, hz, nty, ntz,
                                                cnt.p);
     STB_CHECK_LAUNCH();
     size_t tb = 0;
@@ -267,7 +285,7 @@ class AcousticProp final : public stb_prop_s {
     DevBuf<int> tkey(n), tkey2(n);
     DevBuf<int4> ent(n);
     src_list_.alloc(n);
-    tile_fill_kernel<<<g1(K_), 256, 0, st_>>>(s.keys.p, K_, d_, kTY, kTZ, hy, hz, nty, ntz,
+    tile_fill_kernel<<<g1(K_), 256, 0, st_>>>(src_keys_.p, K_, d_, kTY, kTZ, hy, hz, nty, ntz,
                                               off.p, tkey.p, ent.p);
     STB_CHECK_LAUNCH();
     int bits = 1;
@@ -287,29 +305,23 @@ class AcousticProp final : public stb_prop_s {
   void set_receivers(const double* coords, int64_t nrec) override {
     nrec_ = nrec;
     if (nrec == 0) return;
-    // capture support: every corner of every receiver (zero weights kept, so
-    // the gather reproduces NumPy's 8-wide pairwise sum exactly)
-    Support cs;
-    support_build(cs, coords, nrec, geom_, /*keep_zero=*/true, st_);
-    ncap_ = cs.K;
-    STB_REQUIRE(ncap_ < INT32_MAX, STB_ERR_ARG, "too many receiver corners");
+    // stencils on the GLOBAL geometry (bitwise the reference's weights), then
+    // corner planes shifted into this slab
+    DevBuf<double> dc(nrec * 3);
+    dc.upload(coords, nrec * 3, st_);
+    DevBuf<int64_t> idx(nrec * 24);
     rec_w_.alloc(nrec * 8);
-    STB_CUDA(cudaMemcpyAsync(rec_w_.p, cs.w.p, nrec * 8 * sizeof(double),
-                             cudaMemcpyDeviceToDevice, st_));
+    stencils_compute(dc.p, nrec, geom_, -1, idx.p, rec_w_.p, st_);
     rec_off_.alloc(nrec * 8);
-    idx_to_offsets_kernel<<<g1(nrec * 8), 256, 0, st_>>>(cs.idx.p, nrec * 8, d_, rec_off_.p);
-    cap_idx_.alloc(nrec * 8);
-    corner_index_kernel<<<g1(cs.M), 256, 0, st_>>>(cs.ent_entry.p, cs.ent_point.p, cs.M,
-                                                   cap_idx_.p);
-    const int64_t ncols = d_.nx * d_.ny;
-    cap_row_.alloc(ncols + 1);
-    cap_plane_.alloc(d_.nx);
-    cap_z_.alloc(ncap_);
-    csr32_kernel<<<g1(ncols + 1), 256, 0, st_>>>(cs.row_ptr.p, ncols, cap_row_.p);
-    plane_count_kernel<<<g1(d_.nx), 256, 0, st_>>>(cs.row_ptr.p, d_.nx, d_.ny, cap_plane_.p);
-    keys_z_kernel<<<g1(ncap_), 256, 0, st_>>>(cs.keys.p, ncap_, d_.nz, cap_z_.p);
+    DevBuf<int> bad(1);
+    bad.zero(st_);
+    idx_to_offsets_slab_kernel<<<g1(nrec * 8), 256, 0, st_>>>(idx.p, nrec * 8, d_, x_begin_,
+                                                              rec_off_.p, bad.p);
     STB_CHECK_LAUNCH();
+    int hb = 0;
+    bad.download(&hb, 1, st_);
     STB_CUDA(cudaStreamSynchronize(st_));
+    STB_REQUIRE(hb == 0, STB_ERR_ARG, "receiver corners leave this x slab");
   }
 
   void run(int64_t t0, int64_t nsteps, int k, double* rec_out, int64_t* bad_step) override {
@@ -406,6 +418,13 @@ class AcousticProp final : public stb_prop_s {
     STB_CUDA(cudaMemcpy2DAsync(out, d_.nz * sizeof(T), src, d_.pitch * sizeof(T),
                                d_.nz * sizeof(T), d_.nx * d_.ny, cudaMemcpyDeviceToHost, st_));
     STB_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  void level_ptr(int field, int64_t t, void** dev, int64_t* plane, int64_t* pitch) override {
+    STB_REQUIRE(field == 0, STB_ERR_ARG, "acoustic handles have one field (u)");
+    *dev = lvl_[slot(t)].p;
+    if (plane) *plane = d_.plane;
+    if (pitch) *pitch = d_.pitch;
   }
 
   void reset() override {
@@ -533,8 +552,8 @@ class AcousticProp final : public stb_prop_s {
     a.d = d_;
     a.cx_len = cx_len_;
     a.ntz = (int)((d_.nz + kTZ - 1) / kTZ);
-    a.zero_lo = 1;
-    a.zero_hi = 1;
+    a.zero_lo = zero_lo_ ? 1 : 0;
+    a.zero_hi = zero_hi_ ? 1 : 0;
     a.t0 = (int)t;
     if (K_) {
       a.src_plane = src_plane_.p;
@@ -585,7 +604,7 @@ class AcousticProp final : public stb_prop_s {
   void check_same_geometry(const Support& s) {
     for (int a = 0; a < 3; ++a)
       STB_REQUIRE(s.shape[a] == geom_.shape[a], STB_ERR_ARG,
-                  "support was built for a different grid shape");
+                  "support was built for a different grid shape (supports are global)");
   }
 
   void ensure_events(int64_t n) {
@@ -600,7 +619,9 @@ class AcousticProp final : public stb_prop_s {
 
   int R_ = 1;
   Dims d_{};
-  stb_geometry geom_{};
+  stb_geometry geom_{};          // GLOBAL grid geometry
+  int64_t x_begin_ = 0;          // global plane of local plane 0 (x slabs)
+  bool zero_lo_ = true, zero_hi_ = true;
   bool active_[3]{};
   cudaStream_t st_ = nullptr;
   AcCoefs<T> cf_{};
@@ -622,15 +643,14 @@ class AcousticProp final : public stb_prop_s {
   int64_t K_ = 0, src_nt_ = 0;
   DevBuf<T> series_;
   DevBuf<int64_t> src_off_;
-  DevBuf<int> src_row_, src_plane_, src_z_;
+  DevBuf<int> src_plane_;
+  DevBuf<int64_t> src_keys_;
   DevBuf<int4> src_list_;
   DevBuf<int> src_tile_ptr_;
   // receivers
-  int64_t nrec_ = 0, ncap_ = 0;
+  int64_t nrec_ = 0;
   DevBuf<int64_t> rec_off_;
   DevBuf<double> rec_w_;
-  DevBuf<int> cap_idx_, cap_row_, cap_plane_, cap_z_;
-  DevBuf<T> cap_;
   DevBuf<double> rec_dev_;
   DevBuf<int> guards_;
   // timing

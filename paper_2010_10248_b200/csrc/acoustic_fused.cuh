@@ -223,7 +223,7 @@ __device__ __forceinline__ void update4(const float (&xq)[Q][4], const int cs, c
   for (int i = 0; i < 4; ++i) o[i] = __fmul_rn(o[i], fac[i]);
 }
 
-template <int R, int K, int TY, int TZ, int PF, bool FAST>
+template <int R, int K, int TY, int TZ, int PF, bool FAST, bool GUARD>
 __global__ void __launch_bounds__(FusedCfg<R, K, TY, TZ, PF>::NT, (K == 1 ? 2 : 1))
 acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ FusedArgs a) {
   using C = FusedCfg<R, K, TY, TZ, PF>;
@@ -312,6 +312,13 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
   }
   const bool tile_owner = inE[K] && ydom && z < a.d.nz;
   const bool use_inv = a.use_inv != 0;
+  // CTA-uniform: does any level region of this CTA leave the grid?  Interior
+  // CTAs skip all zero-halo masking.
+  const bool edge = (y0 - C::hy(1) < 0) || (y0 + TY + C::hy(1) > a.d.ny) ||
+                    (z0 - C::hz(1) < 0) || (z0 + TZ + C::hz(1) > a.d.nz) ||
+                    (x0 - (K - 1) * R < 0) || (x1 + (K - 1) * R > a.d.nx);
+  const bool has_src = a.src_list != nullptr;
+  const int nxm1 = (int)a.d.nx - 1;
   const int64_t gbase = (int64_t)y * a.d.pitch + z;      // global offset within a plane
 
   float q[K][C::Q][4];
@@ -338,14 +345,16 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
   // guard (before injection, as the reference's NaN check sees the stencil
   // result) then fused injection from this tile's entry list
   auto sparse_epilogue = [&](float (&o)[4], int j, int p, bool active) {
-    const bool pin = p >= 0 && p < a.d.nx;
-    if (a.guard_mask & (1 << (j - 1))) {
-      if (active && tile_owner && pin && p >= x0 && p < x1) {
+    if constexpr (GUARD) {
+      if (a.guard_mask & (1 << (j - 1))) {
+        const bool pin = p >= 0 && p < a.d.nx;
+        if (active && tile_owner && pin && p >= x0 && p < x1) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) bad |= (zdom[i] && !isfinite(o[i]));
+          for (int i = 0; i < 4; ++i) bad |= (zdom[i] && !isfinite(o[i]));
+        }
       }
     }
-    if (a.src_list && pin && __ldg(a.src_plane + p) > 0) {
+    if (has_src && __ldg(a.src_plane + min(max(p, 0), nxm1)) > 0 && p >= 0 && p <= nxm1) {
       int c = cur[j];
       while (c < e_end && __ldg(&a.src_list[c].x) < p) ++c;
       while (c < e_end) {
@@ -372,7 +381,7 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
   };
 
   auto fac4 = [&](float (&fac)[4], int p) {
-    const float fxx = __ldg(a.fx + min(max(p, 0), (int)a.d.nx - 1));
+    const float fxx = __ldg(a.fx + min(max(p, 0), nxm1));
 #pragma unroll
     for (int i = 0; i < 4; ++i) fac[i] = tmin(fxx, fyz[i]);
   };
@@ -382,11 +391,12 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
     for (int qq = 0; qq < C::Q; ++qq) {
       const int n = nb + qq;
       if (n < N) {
-        const int sb = n % C::NSB;
-        mbar_wait_sleep(&full[sb], (uint32_t)((n / C::NSB) & 1));
+        const unsigned un = (unsigned)n;
+        const int sb = (int)(un % C::NSB);
+        mbar_wait_sleep(&full[sb], (uint32_t)((un / C::NSB) & 1u));
         if (work) {
           const float4 v =
-              *reinterpret_cast<const float4*>(ring1 + (size_t)(n % C::NS1) * C::E0 + off0);
+              *reinterpret_cast<const float4*>(ring1 + (size_t)(un % C::NS1) * C::E0 + off0);
           q[0][qq][0] = v.x; q[0][qq][1] = v.y; q[0][qq][2] = v.z; q[0][qq][3] = v.w;
         }
         const int cs = (qq - R + C::Q) % C::Q;          // centre slot (plane of level j)
@@ -398,7 +408,7 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
             const int p = ibase + n - R;
             float o[4] = {0.f, 0.f, 0.f, 0.f};
             if (work) {
-              const float* cen = ring1 + (size_t)((n - R) % C::NS1) * C::E0 + off0;
+              const float* cen = ring1 + (size_t)((un - R) % C::NS1) * C::E0 + off0;
               const float4 u04 = *reinterpret_cast<const float4*>(aux + off1);
               const float u0[4] = {u04.x, u04.y, u04.z, u04.w};
               float iv[4];
@@ -412,7 +422,7 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
               float fac[4];
               fac4(fac, p);
               update4<FAST, R, C::Q, C::RP, C::WZ0>(q[0], cs, cen, u0, iv, fac, a.cf, o);
-              level_mask(o, p);
+              if (edge) level_mask(o, p);
             }
             sparse_epilogue(o, 1, p, work);
             if constexpr (K >= 2) {
@@ -455,14 +465,14 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
                 fac4(fac, p);
                 update4<FAST, R, C::Q, C::RP, C::WZ1>(q[j - 1], cs, buf + off1, u0, iv, fac,
                                                       a.cf, o);
-                level_mask(o, p);
+                if (edge) level_mask(o, p);
               }
               sparse_epilogue(o, j, p, inE[j]);
               if (j < K) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) q[j][qq][i] = o[i];
               }
-              if (tile_owner && p >= x0 && p < x1 && (j == K || j == K - 1)) {
+              if (tile_owner && (j == K || (j == K - 1 && p >= x0 && p < x1))) {
                 float* dst = (j == K) ? a.out_k : a.out_km1;
                 *reinterpret_cast<float4*>(dst + (int64_t)p * a.d.plane + gbase) =
                     make_float4(o[0], o[1], o[2], o[3]);
@@ -477,23 +487,32 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
       }
     }
   }
-  if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.nonfinite, 1);
+  if constexpr (GUARD) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(a.nonfinite, 1);
+  }
 }
 
 template <int R, int K, int TY, int TZ, int PF, bool FAST>
 struct FusedLauncher {
   using C = FusedCfg<R, K, TY, TZ, PF>;
-  static void launch(cudaStream_t st, const FusedMaps& maps, const FusedArgs& a, int nchunks) {
+  template <bool GUARD>
+  static void launch_g(cudaStream_t st, const FusedMaps& maps, const FusedArgs& a, int nchunks) {
     static bool configured = false;
     if (!configured) {
-      STB_CUDA(cudaFuncSetAttribute(acoustic_fused<R, K, TY, TZ, PF, FAST>,
+      STB_CUDA(cudaFuncSetAttribute(acoustic_fused<R, K, TY, TZ, PF, FAST, GUARD>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
       configured = true;
     }
     const int nty = (int)((a.d.ny + TY - 1) / TY);
     dim3 grid((unsigned)(a.ntz * nty), (unsigned)nchunks);
-    acoustic_fused<R, K, TY, TZ, PF, FAST><<<grid, C::NT, C::SMEM, st>>>(maps, a);
+    acoustic_fused<R, K, TY, TZ, PF, FAST, GUARD><<<grid, C::NT, C::SMEM, st>>>(maps, a);
     STB_CHECK_LAUNCH();
+  }
+  static void launch(cudaStream_t st, const FusedMaps& maps, const FusedArgs& a, int nchunks) {
+    if (a.guard_mask && a.nonfinite)
+      launch_g<true>(st, maps, a, nchunks);
+    else
+      launch_g<false>(st, maps, a, nchunks);
   }
 };
 

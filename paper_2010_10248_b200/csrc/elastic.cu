@@ -435,6 +435,14 @@ class ElasticProp final : public stb_prop_s {
     STB_CUDA(cudaStreamSynchronize(st_));
   }
 
+  void level_ptr(int field, int64_t t, void** dev, int64_t* plane, int64_t* pitch) override {
+    STB_REQUIRE(field >= 0 && field < NFIELDS, STB_ERR_ARG, "elastic field index in [0, 9)");
+    (void)t;
+    *dev = f_[field].p;
+    if (plane) *plane = d_.plane;
+    if (pitch) *pitch = d_.pitch;
+  }
+
   void reset() override {
     for (auto& f : f_) f.zero(st_);
     t_next_ = 0;

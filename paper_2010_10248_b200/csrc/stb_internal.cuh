@@ -152,6 +152,7 @@ struct stb_prop_s {
   virtual void set_receivers(const double* coords, int64_t nrec) = 0;
   virtual void run(int64_t t0, int64_t nsteps, int k, double* rec_out, int64_t* bad_step) = 0;
   virtual void read_field(int field, int64_t t, void* out) = 0;
+  virtual void level_ptr(int field, int64_t t, void** dev, int64_t* plane, int64_t* pitch) = 0;
   virtual void reset() = 0;
   virtual void stats(int64_t* launches, double* ms, int64_t* updates, int64_t* all_launches,
                      double* run_ms) = 0;

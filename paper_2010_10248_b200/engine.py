@@ -305,8 +305,13 @@ def _as_f64_grid(values, grid: GridSpec, what: str):
     return arr
 
 
-def build_propagator(config: RunConfig, dt: float, v_max: float) -> _Prop:
-    """Device model for a config (engine.py:235-255 + physics.py:124-278)."""
+def build_propagator(config: RunConfig, dt: float, v_max: float, x_begin: int = 0,
+                     nx_local: int = 0) -> _Prop:
+    """Device model for a config (engine.py:235-255 + physics.py:124-278).
+
+    ``x_begin``/``nx_local`` select an x slab (multi-GPU, see slabs.py): the
+    geometry, sponge tables and sparse supports stay global; the medium is
+    sliced to the slab's planes."""
     grid = config.grid
     decay = (config.damping_decay if config.damping_decay is not None
              else default_damping_decay(grid, v_max))
@@ -327,9 +332,12 @@ def build_propagator(config: RunConfig, dt: float, v_max: float) -> _Prop:
         if mode not in ("exact", "fma"):
             raise ConfigError("schedule.arithmetic", f"must be 'exact' or 'fma', got {mode!r}")
         d.arithmetic = 1 if mode == "fma" else 0
+        d.x_begin, d.nx_local = int(x_begin), int(nx_local)
         vel = config.medium["velocity"]
         if np.ndim(vel):
             v = _as_f64_grid(vel, grid, "velocity")
+            if nx_local:
+                v = np.ascontiguousarray(v[x_begin:x_begin + nx_local])
             vmax = float(np.max(np.abs(v))) if v.size else 0.0
             if not vmax * vmax < math.inf and np.any(1.0 / v ** 2 <= 0.0):
                 raise ValueError("m must be positive everywhere")   # physics.py:149-150
@@ -347,6 +355,8 @@ def build_propagator(config: RunConfig, dt: float, v_max: float) -> _Prop:
         raw = C.c_void_p()
         _lib.check(_lib.lib().stb_acoustic_create(C.byref(d), C.byref(raw)))
         return _Prop(raw, config.dtype, ACOUSTIC_FIELDS)
+    if nx_local:
+        raise NotImplementedError("x-slab handles cover the acoustic path")
     vp = np.asarray(config.medium["vp"], dtype=np.float64)
     vs = np.asarray(config.medium["vs"], dtype=np.float64)
     rho = np.asarray(config.medium["rho"], dtype=np.float64)

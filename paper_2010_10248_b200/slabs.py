@@ -1,57 +1,286 @@
-"""Device runner used by bench.py: one propagator per rank.
+"""Multi-GPU x-slab decomposition of the time loop (one process per GPU).
 
-``SlabRunner(config, rank, world)`` builds the device model, sources and
-receivers for its share of the grid and advances it.  With ``world == 1`` it
-is the whole grid; with ``world > 1`` the grid is decomposed in x-slabs (x is
-the slowest axis, so halo planes are contiguous) -- see DESIGN.md §5.
+x is the slowest axis of the (x, y, z) C-order field, so an x-slab's halo
+planes are contiguous blocks: the exchange needs no packing kernels.  Rank r
+owns global planes [a_r, b_r) and holds [a_r - G, b_r + G) clipped to the
+grid, with ghost depth G = k*R + 1 for k fused steps per block:
+
+* before a block every held plane of u[t-1] and u[t-2] is valid;
+* the device computes all held planes (each level loses R valid planes per
+  ghost side), so after the block the owned planes -- and one plane beyond
+  them (the "+1"), which receivers straddling the slab boundary read -- are
+  exact;
+* the last two written levels' ghost zones are then refreshed from the
+  neighbours over NCCL (torch.distributed point-to-point), one
+  batch_isend_irecv per block.
+
+Per-point arithmetic is unchanged, so the decomposed run is bitwise equal to
+the single-device run (tests/test_slabs_gloo.py checks the exchange and
+ownership logic against the oracle with gloo on CPU).  Sources come from the
+global inspector support restricted to the slab; receivers are owned by the
+rank holding their base plane and gathered to rank 0 in the original order.
+
+Backends: ``DeviceSlab`` (libstb200, CUDA) is the product path; tests plug
+in a CPU stand-in with the same small interface.
 """
 
 from __future__ import annotations
 
+import ctypes as C
+import math
+
 import numpy as np
 
 from . import _lib
-from .engine import (_gpu_time_height, _Handle, _wavelets, build_propagator,
+from .engine import (_gpu_time_height, _Handle, _Prop, _wavelets, build_propagator,
                      medium_velocity_bounds, resolve_steps)
-from .sparse import nearest_scales_from_velocity, validate_coords_in_extent
+from .sparse import nearest_scales_from_velocity, stencils, validate_coords_in_extent
 
 DEFAULT_TIME_HEIGHT = 1
 
 
-class SlabRunner:
-    def __init__(self, config, rank: int = 0, world: int = 1):
-        if world != 1:
-            raise NotImplementedError("multi-rank x-slab runner not built yet")
-        _lib.require_device()
+def partition(nx: int, world: int, rank: int) -> tuple[int, int]:
+    """Balanced contiguous split of nx planes over world ranks."""
+    base, extra = divmod(nx, world)
+    a = rank * base + min(rank, extra)
+    return a, a + base + (1 if rank < extra else 0)
+
+
+def ghost_depth(k: int, radius: int) -> int:
+    return k * radius + 1
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of device memory owned by libstb200."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class DeviceSlab:
+    """Local propagator of one x-slab on the current CUDA device."""
+
+    def __init__(self, config, dt, v_max, x_begin, nx_local):
         self.config = config
+        self.prop: _Prop = build_propagator(config, dt, v_max, x_begin=x_begin,
+                                            nx_local=nx_local)
+        self.item = np.dtype(config.dtype).itemsize
+        self._rec = None
+
+    def set_sources(self, coords, wav, scale, nt):
+        # the inspector runs on the GLOBAL grid; the handle keeps this
+        # slab's lexicographic id range
+        self._src = _Handle.from_coords(coords, self.config.grid)
+        self.prop.set_sources(self._src, wav, scale, nt)
+
+    def set_receivers(self, coords):
+        self.prop.set_receivers(coords)
+        self.nrec = len(coords)
+
+    def run(self, t0, n, k, rec_out=None):
+        self.prop.run(t0, n, k, rec_out)
+
+    def planes(self, t: int, i: int, j: int):
+        """torch view of local planes [i, j) of time level t (contiguous)."""
+        import torch
+        dev, plane, pitch = C.c_void_p(), C.c_int64(), C.c_int64()
+        _lib.check(_lib.lib().stb_prop_level_ptr(self.prop.raw, 0, t, C.byref(dev),
+                                                 C.byref(plane), C.byref(pitch)))
+        typestr = "<f4" if self.item == 4 else "<f8"
+        base = dev.value + i * plane.value * self.item
+        return torch.as_tensor(_DevArray(base, (j - i, plane.value), typestr), device="cuda")
+
+    def read(self, t, shape):
+        return self.prop.read("u", t, shape)
+
+    def stats(self):
+        return self.prop.stats()
+
+    def describe(self, k):
+        return self.prop.describe(k)
+
+    def synchronize(self):
+        import torch
+        torch.cuda.synchronize()
+
+
+class SlabRunner:
+    """One rank's share of a run.  world == 1 is the plain single-GPU run."""
+
+    def __init__(self, config, rank: int = 0, world: int = 1, backend_factory=None,
+                 group=None):
+        if config.physics != "acoustic":
+            raise NotImplementedError("x-slab runner covers the acoustic path")
+        self.config, self.rank, self.world, self.group = config, rank, world, group
         self.dt, self.nt = resolve_steps(config)
         k = _gpu_time_height(config)
         self.time_height = k if k > 0 else DEFAULT_TIME_HEIGHT
-        v_max = medium_velocity_bounds(config.physics, config.medium)
         grid = config.grid
-        self.prop = build_propagator(config, self.dt, v_max)
+        nx = grid.shape[0]
+        R = config.space_order // 2
+        self.R = R
+        self.a, self.b = partition(nx, world, rank)
+        G = ghost_depth(self.time_height, R) if world > 1 else 0
+        if world > 1 and self.b - self.a < G:
+            raise ValueError(f"x slab of {self.b - self.a} planes is thinner than the "
+                             f"ghost depth {G}; use fewer ranks or a smaller time_height")
+        self.G = G
+        self.lo, self.hi = max(self.a - G, 0), min(self.b + G, nx)
+        self.nl = self.hi - self.lo
+        v_max = medium_velocity_bounds(config.physics, config.medium)
+        if backend_factory is None:
+            _lib.require_device()
+            backend_factory = DeviceSlab
+        self.dev = backend_factory(config, self.dt, v_max, self.lo, self.nl)
+        # sources: the global inspector support, restricted on the device
         spec = config.sources
-        if spec is not None and spec.nsrc:
+        if spec is not None and spec.nsrc and self.nt > 0:
             validate_coords_in_extent(spec.coords, grid, what="source")
             wav = _wavelets(config, self.dt, self.nt)
             scale = nearest_scales_from_velocity(spec.coords, grid, config.medium["velocity"],
                                                  self.dt)
-            self._src = _Handle.from_coords(spec.coords, grid)
-            self.prop.set_sources(self._src, wav, scale, self.nt)
-        if config.receiver_coords is not None and len(config.receiver_coords):
-            validate_coords_in_extent(config.receiver_coords, grid,
-                                      margin_points=grid.boundary_layers, what="receiver")
-            self.prop.set_receivers(config.receiver_coords)
-        self._local_points = grid.npoints
+            self.dev.set_sources(spec.coords, wav, scale, self.nt)
+        # receivers owned by base plane
+        self.rec_index = np.zeros(0, dtype=np.int64)
+        self.nrec_total = 0
+        rc = config.receiver_coords
+        if rc is not None and len(rc):
+            validate_coords_in_extent(rc, grid, margin_points=grid.boundary_layers,
+                                      what="receiver")
+            self.nrec_total = len(rc)
+            base = self._base_planes(rc)
+            mine = np.flatnonzero((base >= self.a) & (base < self.b))
+            self.rec_index = mine
+            if len(mine):
+                self.dev.set_receivers(np.ascontiguousarray(rc[mine]))
+        self._traces = []
 
-    def run(self, t0: int, nsteps: int):
-        self.prop.run(t0, nsteps, self.time_height, None)
+    # ------------------------------------------------------------ setup helpers
+    def _base_planes(self, coords):
+        idx = getattr(self.dev, "stencil_index", None)
+        if idx is not None:
+            return idx(coords)[:, 0, 0]
+        return stencils(coords, self.config.grid)[0][:, 0, 0]
 
+    def local_points(self) -> int:
+        g = self.config.grid
+        return (self.b - self.a) * g.shape[1] * g.shape[2]
+
+    # ------------------------------------------------------------ stepping
+    def run(self, t0: int, nsteps: int, record: bool = False):
+        """Advance [t0, t0 + nsteps) in blocks of time_height with a halo
+        exchange after each block."""
+        k = self.time_height
+        self._acc = {}
+        if self.world == 1:
+            # no exchange: one device call covers every block
+            rec = (np.zeros((nsteps, len(self.rec_index)), dtype=np.float64)
+                   if record and len(self.rec_index) else None)
+            self.dev.run(t0, nsteps, k, rec)
+            self._accumulate()
+            if rec is not None:
+                self._traces.append((t0, rec))
+            return
+        t = t0
+        while t < t0 + nsteps:
+            kb = min(k, t0 + nsteps - t)
+            rec = None
+            if record and len(self.rec_index):
+                rec = np.zeros((kb, len(self.rec_index)), dtype=np.float64)
+            self.dev.run(t, kb, kb, rec)
+            self._accumulate()
+            if rec is not None:
+                self._traces.append((t, rec))
+            newest = [t + kb - 1] + ([t + kb - 2] if kb >= 2 else [])
+            self.exchange(newest)
+            t += kb
+
+    def _accumulate(self):
+        st = self.dev.stats() or {}
+        for key, val in st.items():
+            self._acc[key] = self._acc.get(key, 0) + val
+
+    def exchange(self, levels):
+        """Refresh ghost planes of the given time levels from the neighbours."""
+        import torch.distributed as dist
+        ops = []
+        g_lo, g_hi = self.a - self.lo, self.hi - self.b
+        for t in levels:
+            if self.rank > 0:
+                ops.append(dist.P2POp(dist.isend, self.dev.planes(t, g_lo, g_lo + g_lo),
+                                      self.rank - 1, group=self.group))
+                ops.append(dist.P2POp(dist.irecv, self.dev.planes(t, 0, g_lo), self.rank - 1,
+                                      group=self.group))
+            if self.rank < self.world - 1:
+                ops.append(dist.P2POp(dist.isend,
+                                      self.dev.planes(t, self.nl - g_hi - g_hi, self.nl - g_hi),
+                                      self.rank + 1, group=self.group))
+                ops.append(dist.P2POp(dist.irecv, self.dev.planes(t, self.nl - g_hi, self.nl),
+                                      self.rank + 1, group=self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        self.dev.synchronize()
+
+    # ------------------------------------------------------------ results
+    def gather_field(self, t: int):
+        """Full field at level t on rank 0 (None elsewhere)."""
+        import torch
+        import torch.distributed as dist
+        g = self.config.grid
+        local = self.dev.read(t, (self.nl, g.shape[1], g.shape[2]))
+        own = np.ascontiguousarray(local[self.a - self.lo: self.b - self.lo])
+        if self.world == 1:
+            return own
+        if self.rank == 0:
+            out = np.empty(g.shape, dtype=own.dtype)
+            out[self.a:self.b] = own
+            for r in range(1, self.world):
+                a, b = partition(g.shape[0], self.world, r)
+                buf = torch.empty((b - a,) + g.shape[1:], dtype=torch.from_numpy(own).dtype)
+                dist.recv(buf, r, group=self.group)
+                out[a:b] = buf.numpy()
+            return out
+        dist.send(torch.from_numpy(own), 0, group=self.group)
+        return None
+
+    def gather_receivers(self, nt: int):
+        """(nt, nrec) traces on rank 0 in the original receiver order."""
+        import torch
+        import torch.distributed as dist
+        mine = np.zeros((nt, len(self.rec_index)), dtype=np.float64)
+        for t, rec in self._traces:
+            mine[t:t + rec.shape[0]] = rec
+        if self.world == 1:
+            return mine
+        if self.rank == 0:
+            out = np.zeros((nt, self.nrec_total), dtype=np.float64)
+            out[:, self.rec_index] = mine
+            for r in range(1, self.world):
+                n = torch.zeros(1, dtype=torch.int64)
+                dist.recv(n, r, group=self.group)
+                if int(n.item()) == 0:
+                    continue
+                idx = torch.zeros(int(n.item()), dtype=torch.int64)
+                dist.recv(idx, r, group=self.group)
+                buf = torch.zeros((nt, int(n.item())), dtype=torch.float64)
+                dist.recv(buf, r, group=self.group)
+                out[:, idx.numpy()] = buf.numpy()
+            return out
+        dist.send(torch.tensor([len(self.rec_index)], dtype=torch.int64), 0, group=self.group)
+        if len(self.rec_index):
+            dist.send(torch.from_numpy(self.rec_index.astype(np.int64)), 0, group=self.group)
+            dist.send(torch.from_numpy(mine), 0, group=self.group)
+        return None
+
+    # ------------------------------------------------------------ reporting
     def stats(self) -> dict:
-        return self.prop.stats()
+        """Device counters summed over the device calls of the last run()."""
+        return dict(getattr(self, "_acc", {}))
 
     def describe(self) -> str:
-        return self.prop.describe(self.time_height)
+        return self.dev.describe(self.time_height)
 
     def kernel_tag(self) -> str:
         return self.describe().split(" ")[0]
@@ -64,5 +293,13 @@ class SlabRunner:
         item = np.dtype(self.config.dtype).itemsize
         return (4 if self.time_height == 1 else 5) * item
 
-    def local_points(self) -> int:
-        return self._local_points
+
+def run_distributed(config, rank: int, world: int, group=None, backend_factory=None):
+    """Whole forward run over x-slabs; rank 0 returns (fields, traces)."""
+    runner = SlabRunner(config, rank, world, backend_factory=backend_factory, group=group)
+    nt = runner.nt
+    if nt > 0:
+        runner.run(0, nt, record=True)
+    field = runner.gather_field(nt - 1 if nt > 0 else 0)
+    traces = runner.gather_receivers(nt) if runner.nrec_total else None
+    return field, traces

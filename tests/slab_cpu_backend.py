@@ -1,0 +1,86 @@
+"""CPU stand-in for slabs.DeviceSlab (TEST INFRASTRUCTURE ONLY).
+
+Implements the small backend interface SlabRunner drives (set_sources,
+set_receivers, run, planes, read, ...) with the oracle's NumPy restatement
+on a halo-padded local slab, so the x-slab decomposition, ghost depth,
+exchange order and receiver ownership can be checked with gloo on CPU.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import stencil_oracle as so
+
+
+class OracleSlab:
+    def __init__(self, config, dt, v_max, x_begin, nx_local):
+        g = config.grid
+        self.config = config
+        self.R = config.space_order // 2
+        self.x_begin, self.nl = x_begin, nx_local
+        self.dtype = np.float32 if config.precision == 32 else np.float64
+        bl = g.boundary_layers
+        decay = (config.damping_decay if config.damping_decay is not None
+                 else so.default_decay(g.shape, g.spacing, bl, v_max))
+        damp = so.damping3d(g.shape, bl, decay)[x_begin:x_begin + nx_local] if bl else None
+        vel = config.medium["velocity"]
+        if np.ndim(vel):
+            m = (1.0 / np.asarray(vel, dtype=np.float64) ** 2)[x_begin:x_begin + nx_local]
+        else:
+            m = 1.0 / float(vel) ** 2
+        shape_l = (nx_local,) + tuple(g.shape[1:])
+        self.model = so.Acoustic(shape_l, g.spacing, config.space_order, m, dt, damp, self.dtype)
+        self.pts = None
+        self.ridx = None
+
+    def stencil_index(self, coords):
+        g = self.config.grid
+        return so.interp_stencils(coords, g.shape, g.spacing, g.origin)[0]
+
+    def set_sources(self, coords, wav, scale, nt):
+        g = self.config.grid
+        idx, w = so.interp_stencils(coords, g.shape, g.spacing, g.origin)
+        pts, _, _ = so.source_entries(idx, w)
+        sup = so.build_support(pts.tolist(), g.shape)
+        dcmp = so.decompose(idx, w, scale, wav, sup, nt)
+        keep = (sup.points[:, 0] >= self.x_begin) & (sup.points[:, 0] < self.x_begin + self.nl)
+        self.pts = sup.points[keep] - np.array([self.x_begin, 0, 0])
+        self.dcmp = dcmp[:, keep]
+
+    def set_receivers(self, coords):
+        g = self.config.grid
+        idx, w = so.interp_stencils(coords, g.shape, g.spacing, g.origin)
+        idx = idx.copy()
+        idx[:, :, 0] -= self.x_begin
+        assert idx[:, :, 0].min() >= 0 and idx[:, :, 0].max() < self.nl
+        self.ridx, self.rw = idx, w
+
+    def run(self, t0, n, k, rec_out=None):
+        R = self.R
+        for t in range(t0, t0 + n):
+            self.model.step(t)
+            if self.pts is not None and len(self.pts):
+                lvl = self.model.level(t)
+                p = self.pts
+                lvl[p[:, 0] + R, p[:, 1] + R, p[:, 2] + R] += self.dcmp[t].astype(self.dtype)
+            if rec_out is not None and self.ridx is not None:
+                rec_out[t - t0] = so.record(self.model.level(t), self.ridx, self.rw, R)
+
+    def planes(self, t, i, j):
+        import torch
+        R = self.R
+        return torch.from_numpy(self.model.level(t)[R + i:R + j])
+
+    def read(self, t, shape):
+        R = self.R
+        return self.model.level(t)[R:-R, R:-R, R:-R].copy()
+
+    def synchronize(self):
+        pass
+
+    def stats(self):
+        return {}
+
+    def describe(self, k):
+        return f"oracle-slab k={k}"

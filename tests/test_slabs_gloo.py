@@ -1,0 +1,77 @@
+"""x-slab multi-rank path on CPU: world_size 2/3 with the gloo backend, each
+rank driving a CPU stand-in of the device slab (slab_cpu_backend.OracleSlab).
+The stitched fields and traces must equal the single-domain oracle run bit
+for bit, for k = 1 and k = 2 fused steps per exchange."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from cases import random_coords
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _case(k):
+    import paper_2010_10248_b200 as stb
+    rng = np.random.default_rng(5)
+    shape = (36, 20, 24)
+    grid = stb.GridSpec(shape, (10.0, 10.0, 10.0), (0.0, 0.0, 0.0), boundary_layers=4)
+    v = rng.uniform(1800.0, 2600.0, shape)
+    # sources near the slab boundaries (x = 12, 18, 24 for 2/3 ranks)
+    src = np.array([[117.5, 95.0, 101.0], [181.2, 80.3, 120.7], [241.0, 110.0, 90.0]])
+    rec = random_coords(rng, shape, grid.spacing, grid.origin, 12, margin=5)
+    rec[0] = [115.5, 100.0, 110.0]          # base plane 11, straddles x = 12
+    rec[1] = [175.0, 100.0, 110.0]          # on plane 17.5 -> base 17
+    return stb.RunConfig(physics="acoustic", grid=grid, space_order=8, nt=14,
+                         medium={"velocity": v}, sources=stb.SourceSpec(src, f0=25.0),
+                         receiver_coords=rec,
+                         schedule=stb.ScheduleSpec("gpu", time_height=k))
+
+
+def _worker(rank, world, port, k, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2010_10248_b200.slabs import run_distributed
+        from slab_cpu_backend import OracleSlab
+        field, traces = run_distributed(_case(k), rank, world, backend_factory=OracleSlab)
+        if rank == 0:
+            np.savez(out_path, field=field, traces=traces)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k", [(2, 1), (2, 2), (3, 1)])
+def test_xslab_matches_single_domain(world, k, tmp_path):
+    from oracle import stencil_oracle as so
+    out = str(tmp_path / "res.npz")
+    mp.start_processes(_worker, args=(world, _free_port(), k, out), nprocs=world,
+                       join=True, start_method="spawn")
+    got = np.load(out)
+    ref = so.run(_case(k))
+    np.testing.assert_array_equal(got["field"], ref.fields["u"])
+    np.testing.assert_array_equal(got["traces"], ref.receivers)
+
+
+def test_partition_and_ghosts():
+    from paper_2010_10248_b200.slabs import ghost_depth, partition
+    for nx in (36, 592, 1024):
+        for world in (1, 2, 3, 8):
+            spans = [partition(nx, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == nx
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+    assert ghost_depth(1, 4) == 5 and ghost_depth(2, 4) == 9
