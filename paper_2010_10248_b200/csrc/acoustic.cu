@@ -37,7 +37,7 @@ inline unsigned g1(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b);
 
 template <typename T>
 __global__ void inv_from_velocity_kernel(const double* __restrict__ v, const double* __restrict__ m,
-                                         double dt2, Dims d, T* __restrict__ inv) {
+                                         double dt2, Dims d, T* __restrict__ inv, int* bad_m) {
   const int64_t n = d.nx * d.ny * d.nz;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -48,6 +48,7 @@ __global__ void inv_from_velocity_kernel(const double* __restrict__ v, const dou
     } else {
       mm = m[i];
     }
+    if (mm <= 0.0) atomicExch(bad_m, 1);      // physics.py:149-150
     const int64_t z = i % d.nz, xy = i / d.nz;
     inv[xy * d.pitch + z] = from_f64<T>(rdiv(dt2, mm));   // physics.py:151
   }
@@ -189,11 +190,16 @@ class AcousticProp final : public stb_prop_s {
       tmp.upload(desc.velocity ? desc.velocity : desc.m, n, st_);
       inv_.alloc(d_.total());
       inv_.zero(st_);
+      DevBuf<int> bad(1);
+      bad.zero(st_);
       inv_from_velocity_kernel<T><<<1184, 256, 0, st_>>>(desc.velocity ? tmp.p : nullptr,
                                                          desc.velocity ? nullptr : tmp.p,
-                                                         desc.dt2, d_, inv_.p);
+                                                         desc.dt2, d_, inv_.p, bad.p);
       STB_CHECK_LAUNCH();
+      int hb = 0;
+      bad.download(&hb, 1, st_);
       STB_CUDA(cudaStreamSynchronize(st_));
+      STB_REQUIRE(hb == 0, STB_ERR_ARG, "m must be positive everywhere");
     } else {
       inv_scalar_ = (T)desc.inv_scalar;
     }

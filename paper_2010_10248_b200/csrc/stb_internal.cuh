@@ -39,6 +39,23 @@ void set_error(const std::string& msg);
     if (!(cond)) throw ::stb::Error(code, msg); \
   } while (0)
 
+// Device allocations come from the stream-ordered pool of the current device
+// with an unlimited release threshold: a process that runs many shots (or
+// re-creates handles) reuses freed field buffers instead of paying
+// cudaMalloc/page-mapping cost per handle.
+inline void retain_freed_memory() {
+  static thread_local int done_for = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  if (done_for == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_for = dev;
+}
+
 // Owning device buffer.
 template <typename T>
 struct DevBuf {
@@ -57,10 +74,17 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) STB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (count) {
+      retain_freed_memory();
+      STB_CUDA(cudaMallocAsync(&p, count * sizeof(T), 0));
+      STB_CUDA(cudaStreamSynchronize(0));
+    }
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaFreeAsync(p, 0);
+      cudaStreamSynchronize(0);
+    }
     p = nullptr;
     n = 0;
   }

@@ -254,3 +254,49 @@ def test_cfg1_fma_mode_tolerance(golden_big):
     ref_rec = np.load(os.path.join(GOLDEN, "cfg1_receivers.npy"))
     num = np.linalg.norm(res.receivers - ref_rec)
     assert num / np.linalg.norm(ref_rec) <= L2_TOL
+
+
+# ------------------------------------------------- x-slab device mechanics
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_xslab_handles_emulated_two_ranks(k):
+    """Two x-slab handles on one GPU, ghost planes exchanged by device
+    copies in the order slabs.SlabRunner uses (NCCL replaced by copies: two
+    NCCL ranks must not share one GPU).  Stitched owned planes and traces
+    equal the single-device run bit for bit."""
+    import torch
+    from paper_2010_10248_b200 import slabs
+    from test_slabs_gloo import _case
+    cfg = _case(k)
+    world = 2
+    ranks = []
+    for r in range(world):
+        ranks.append(slabs.SlabRunner(cfg, r, world))
+    nt = ranks[0].nt
+    t = 0
+    while t < nt:
+        kb = min(k, nt - t)
+        for rr in ranks:
+            rec = np.zeros((kb, len(rr.rec_index))) if len(rr.rec_index) else None
+            rr.dev.run(t, kb, kb, rec)
+            if rec is not None:
+                rr._traces.append((t, rec))
+        lo, hi = ranks
+        g = lo.hi - lo.b                       # ghost planes on each side
+        for lev in [t + kb - 1] + ([t + kb - 2] if kb >= 2 else []):
+            # rank 0 top ghost <- rank 1 first owned planes; and vice versa
+            lo.dev.planes(lev, lo.nl - g, lo.nl).copy_(hi.dev.planes(lev, g, 2 * g))
+            hi.dev.planes(lev, 0, g).copy_(lo.dev.planes(lev, lo.nl - 2 * g, lo.nl - g))
+        torch.cuda.synchronize()
+        t += kb
+    shape = cfg.grid.shape
+    field = np.empty(shape, dtype=np.float32)
+    traces = np.zeros((nt, len(cfg.receiver_coords)))
+    for rr in ranks:
+        loc = rr.dev.read(nt - 1, (rr.nl,) + shape[1:])
+        field[rr.a:rr.b] = loc[rr.a - rr.lo: rr.b - rr.lo]
+        for t0, rec in rr._traces:
+            traces[t0:t0 + rec.shape[0], rr.rec_index] = rec
+    ref = so.run(cfg)
+    np.testing.assert_array_equal(field, ref.fields["u"])
+    np.testing.assert_array_equal(traces, ref.receivers)

@@ -1,0 +1,13 @@
+"""Phase timing of paper_2010_10248_b200.run() on the cfg2 bench workload."""
+import cProfile, pstats, sys, time
+sys.path.insert(0, ".")
+import numpy as np
+import bench
+import paper_2010_10248_b200 as stb
+v, src, rec = bench.cfg2_inputs()
+cfg = bench.make_config(stb, v, src, rec, 64, 0)
+stb.run(cfg)  # warm (CUDA context, module load)
+pr = cProfile.Profile()
+t0 = time.perf_counter(); pr.enable(); res = stb.run(cfg); pr.disable(); t1 = time.perf_counter()
+print("wall", t1 - t0, "elapsed_s", res.report.elapsed_s, "precompute_s", res.report.precompute_s)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
