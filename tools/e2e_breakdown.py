@@ -1,6 +1,6 @@
 """Phase timing of paper_2010_10248_b200.run() on the cfg2 bench workload."""
-import cProfile, pstats, sys, time
-sys.path.insert(0, ".")
+import cProfile, os, pstats, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import bench
 import paper_2010_10248_b200 as stb

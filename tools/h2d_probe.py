@@ -1,5 +1,5 @@
-import time, sys
-sys.path.insert(0, ".")
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 v = np.random.default_rng(0).random((592, 592, 592))
 torch.cuda.init(); x = torch.empty(1, device="cuda"); torch.cuda.synchronize()
