@@ -162,6 +162,9 @@ typedef struct {
   /* the device forms dt/rho, dt*lam, dt*mu, 2*dt*mu (physics.py:251-257);
      f32(2*dt*mu) == 2*f32(dt*mu) exactly, so only three streams are kept. */
   const double* damp[3];
+  int64_t x_begin;           /* x slab, as in stb_acoustic_desc (materials are
+                                the local slab; geometry, tables global)     */
+  int64_t nx_local;
 } stb_elastic_desc;
 
 int stb_acoustic_create(const stb_acoustic_desc* d, stb_prop_t* out);

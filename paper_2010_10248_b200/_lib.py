@@ -55,7 +55,8 @@ class ElasticDesc(C.Structure):
                 ("lam", C.POINTER(C.c_double)), ("mu", C.POINTER(C.c_double)),
                 ("rho", C.POINTER(C.c_double)), ("lam_scalar", C.c_double),
                 ("mu_scalar", C.c_double), ("rho_scalar", C.c_double),
-                ("damp", C.POINTER(C.c_double) * 3)]
+                ("damp", C.POINTER(C.c_double) * 3), ("x_begin", C.c_int64),
+                ("nx_local", C.c_int64)]
 
 
 _lock = threading.Lock()

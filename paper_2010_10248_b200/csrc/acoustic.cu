@@ -362,7 +362,22 @@ class AcousticProp final : public stb_prop_s {
           ++gi;
         }
       STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
-      if (path_ == Path::Fused) {
+      if (path_ == Path::Fused && kb == 2 && diag_cx_ > 0 && R_ == 4) {
+        // L2-streaming temporal blocking: step t on x-chunk c, then step t+1
+        // on chunk c-1 (its x-halo of step t was just written), so step t+1
+        // reads step t and the shared inputs while they are L2-resident.
+        const int cx = diag_cx_;
+        const int nc = (int)((d_.nx + cx - 1) / cx);
+        const int g0 = (gmask & 1) ? 1 : 0, g1 = (gmask & 2) ? 2 : 0;
+        for (int c = 0; c <= nc; ++c) {
+          if (c < nc)
+            launch_fused_rk<4, 1>(t, g0 ? gflag : nullptr, g0, c * cx,
+                                  (int)std::min<int64_t>((int64_t)(c + 1) * cx, d_.nx), cx);
+          if (c >= 1)
+            launch_fused_rk<4, 1>(t + 1, g1 ? gflag : nullptr, g1 ? 1 : 0, (c - 1) * cx,
+                                  (int)std::min<int64_t>((int64_t)c * cx, d_.nx), cx);
+        }
+      } else if (path_ == Path::Fused) {
         launch_fused(t, kb, gflag, gmask);
       } else if (path_ == Path::Tiled) {
         launch_tiled(slot(t - 1), slot(t - 2), lvl_[slot(t)].p, gflag);
@@ -517,6 +532,7 @@ class AcousticProp final : public stb_prop_s {
       max_k_ = (R_ == 4) ? 2 : 1;
       default_k_ = 1;
       if (const char* kd = std::getenv("STB_DEFAULT_K")) default_k_ = std::atoi(kd);
+      if (const char* dc = std::getenv("STB_DIAG_CX")) diag_cx_ = std::atoi(dc);
       if (default_k_ < 1) default_k_ = 1;
       if (default_k_ > max_k_) default_k_ = max_k_;
       path_ = Path::Fused;
@@ -536,7 +552,10 @@ class AcousticProp final : public stb_prop_s {
   }
 
   template <int R, int K>
-  void launch_fused_rk(int64_t t, int* gflag, int gmask) {
+  void launch_fused_rk(int64_t t, int* gflag, int gmask, int x_lo = 0, int x_hi = -1,
+                       int cx = 0) {
+    if (x_hi < 0) x_hi = (int)d_.nx;
+    if (cx <= 0) cx = cx_len_;
     // tensor maps are cached per (K, input slots)
     const int s_l0 = slot(t - 1), s_lm1 = slot(t - 2);
     const int key = (K * NB + s_l0) * NB + s_lm1;
@@ -556,7 +575,9 @@ class AcousticProp final : public stb_prop_s {
     a.use_inv = inv_.p ? 1 : 0;
     a.cf = tcf_;
     a.d = d_;
-    a.cx_len = cx_len_;
+    a.cx_len = cx;
+    a.x_lo = x_lo;
+    a.x_hi = x_hi;
     a.ntz = (int)((d_.nz + kTZ - 1) / kTZ);
     a.zero_lo = zero_lo_ ? 1 : 0;
     a.zero_hi = zero_hi_ ? 1 : 0;
@@ -570,10 +591,11 @@ class AcousticProp final : public stb_prop_s {
     }
     a.nonfinite = gflag;
     a.guard_mask = gmask;
+    const int nch = (x_hi - x_lo + cx - 1) / cx;
     if (fast_)
-      FusedLauncher<R, K, kTY, kTZ, kPF, true>::launch(st_, it->second, a, nchunks_);
+      FusedLauncher<R, K, kTY, kTZ, kPF, true>::launch(st_, it->second, a, nch);
     else
-      FusedLauncher<R, K, kTY, kTZ, kPF, false>::launch(st_, it->second, a, nchunks_);
+      FusedLauncher<R, K, kTY, kTZ, kPF, false>::launch(st_, it->second, a, nch);
   }
 
   void launch_fused(int64_t t, int kb, int* gflag, int gmask) {
@@ -642,6 +664,7 @@ class AcousticProp final : public stb_prop_s {
   int arithmetic_ = 0;
   int max_k_ = 1, default_k_ = 1, last_k_ = 1;
   int cx_len_ = 0, nchunks_ = 1;
+  int diag_cx_ = 0;                 // >0: K=2 blocks run as diagonal K=1 sweeps
   TiledCoefs tcf_{};
   CUtensorMap map_ext_[NB]{}, map_tile_[NB]{}, map_inv_{};
   std::unordered_map<int, FusedMaps> fmaps_;

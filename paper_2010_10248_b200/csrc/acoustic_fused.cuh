@@ -95,6 +95,7 @@ struct FusedArgs {
   TiledCoefs cf;
   Dims d;
   int cx_len, ntz;
+  int x_lo, x_hi;        // planes swept by this launch: [x_lo, x_hi) in cx_len chunks
   int zero_lo, zero_hi;  // planes < 0 / >= nx are the reference's zero halo
   int t0;                // time step of level 1
   const int* src_plane;  // per-plane count of affected points
@@ -238,8 +239,8 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
   const int tile = blockIdx.x;
   const int y0 = (tile / a.ntz) * TY;
   const int z0 = (tile % a.ntz) * TZ;
-  const int x0 = blockIdx.y * a.cx_len;
-  const int x1 = min(x0 + a.cx_len, (int)a.d.nx);
+  const int x0 = a.x_lo + blockIdx.y * a.cx_len;
+  const int x1 = min(x0 + a.cx_len, a.x_hi);
   const int N = (x1 - x0) + 2 * K * R;
   const int ibase = x0 - K * R;
 
@@ -509,6 +510,7 @@ struct FusedLauncher {
     STB_CHECK_LAUNCH();
   }
   static void launch(cudaStream_t st, const FusedMaps& maps, const FusedArgs& a, int nchunks) {
+    if (nchunks <= 0) return;
     if (a.guard_mask && a.nonfinite)
       launch_g<true>(st, maps, a, nchunks);
     else

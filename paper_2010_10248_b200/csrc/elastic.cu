@@ -11,6 +11,14 @@
 // The two half steps read only the previous value of the field they write
 // at the same point, so both update in place (one level per field): 9 field
 // streams + 3 material streams.
+//
+// Layout: every field is stored with a zero halo of H >= R points on all
+// sides (never written), interior z starting 128-byte aligned, so neighbour
+// loads need no bounds checks.  Kernels are 2.5-D x sweeps: a block of
+// 32 (z) x 16 (y) threads walks an x chunk; the three fields differentiated
+// along x live in register queues of 2R+1 planes (loop unrolled by 2R+1),
+// y/z neighbours come through L1.
+#include <cstdlib>
 #include <memory>
 #include <sstream>
 
@@ -26,6 +34,31 @@ inline unsigned g1(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b);
 
 enum { VX, VY, VZ, TXX, TYY, TZZ, TXY, TXZ, TYZ, NFIELDS };
 
+// Zero-haloed layout.
+struct PDims {
+  int64_t nx, ny, nz;     // interior
+  int64_t H;              // halo width (>= R)
+  int64_t zoff;           // interior z offset within a row (128-byte aligned)
+  int64_t pitch;          // row length (elements)
+  int64_t plane;          // (ny + 2H) * pitch
+  int64_t total;          // (nx + 2H) * plane
+  __host__ __device__ int64_t at(int64_t x, int64_t y, int64_t z) const {
+    return ((x + H) * (ny + 2 * H) + (y + H)) * pitch + zoff + z;
+  }
+};
+
+PDims make_pdims(int64_t nx, int64_t ny, int64_t nz, int R, size_t elem) {
+  PDims p;
+  p.nx = nx; p.ny = ny; p.nz = nz;
+  p.H = R;
+  const int64_t per128 = 128 / (int64_t)elem;
+  p.zoff = round_up(R, per128);
+  p.pitch = round_up(p.zoff + nz + R, per128);
+  p.plane = (ny + 2 * p.H) * p.pitch;
+  p.total = (nx + 2 * p.H) * p.plane;
+  return p;
+}
+
 template <typename T>
 struct ElCoefs {
   T d1[3][8];     // f(c_j / h_a)
@@ -34,7 +67,7 @@ struct ElCoefs {
 };
 
 template <typename T>
-struct ElFields {
+struct ElArgs {
   T* f[NFIELDS];
   const T* buoy;
   const T* lam;
@@ -43,174 +76,394 @@ struct ElFields {
   const T* fy;
   const T* fz;
   int has_fac;
+  ElCoefs<T> cf;
+  PDims d;
+  int cx;                 // x chunk length
+  int* nonfinite;         // guard flag (NULL: no check this step)
 };
 
-template <typename T, int R>
-__device__ __forceinline__ T stag(const T* __restrict__ a, int64_t i, int64_t stride,
-                                  int64_t pos, int64_t n, const T* c, bool fwd) {
+// staggered first derivative from an accessor g(o) = a[centre + o*stride]
+template <typename T, int R, typename G>
+__device__ __forceinline__ T stag(const G& g, const T* c, bool fwd) {
   T acc = T(0);
 #pragma unroll
   for (int j = 1; j <= R; ++j) {
     const int hi = fwd ? j : j - 1;
     const int lo = fwd ? -(j - 1) : -j;
-    const T vh = (pos + hi < n && pos + hi >= 0) ? a[i + hi * stride] : T(0);
-    const T vl = (pos + lo < n && pos + lo >= 0) ? a[i + lo * stride] : T(0);
-    const T term = rmul(rsub(vh, vl), c[j - 1]);
+    const T term = rmul(rsub(g(hi), g(lo)), c[j - 1]);
     acc = (j == 1) ? term : radd(acc, term);
   }
   return acc;
 }
 
-struct Pt {
-  int64_t i, pos[3], n[3], stride[3];
-};
-
-__device__ __forceinline__ Pt make_pt(const Dims& d, int64_t x, int64_t y, int64_t z) {
-  Pt p;
-  p.i = x * d.plane + y * d.pitch + z;
-  p.pos[0] = x; p.pos[1] = y; p.pos[2] = z;
-  p.n[0] = d.nx; p.n[1] = d.ny; p.n[2] = d.nz;
-  p.stride[0] = d.plane; p.stride[1] = d.pitch; p.stride[2] = 1;
-  return p;
+// ---------------------------------------------------------------------------
+// velocity half step: v[t] = (v[t-1] + div(tau[t-1]) * buoy) * fac
+// x derivatives from register queues of txx, txy, txz.
+// ---------------------------------------------------------------------------
+template <typename T, int R>
+__global__ void __launch_bounds__(256, 3)
+elastic_v_sweep(ElArgs<T> a) {
+  constexpr int Q = 2 * R + 1;
+  const int z = blockIdx.x * 32 + threadIdx.x;
+  const int y = blockIdx.y * 8 + threadIdx.y;
+  const int x0 = blockIdx.z * a.cx;
+  const int x1 = min(x0 + a.cx, (int)a.d.nx);
+  if (z >= a.d.nz || y >= a.d.ny) return;
+  const int ys = (int)a.d.pitch, xs = (int)a.d.plane;
+  const ElCoefs<T>& cf = a.cf;
+  const T* __restrict__ txx = a.f[TXX];
+  const T* __restrict__ txy = a.f[TXY];
+  const T* __restrict__ txz = a.f[TXZ];
+  const T* __restrict__ tyy = a.f[TYY];
+  const T* __restrict__ tyz = a.f[TYZ];
+  const T* __restrict__ tzz = a.f[TZZ];
+  T qxx[Q], qxy[Q], qxz[Q];
+#pragma unroll
+  for (int s = 0; s < Q; ++s) qxx[s] = qxy[s] = qxz[s] = T(0);
+  const int N = (x1 - x0) + 2 * R;
+  const int base = (int)a.d.at(x0 - R, y, z);      // offset of queue plane n = 0
+  const T fyz = a.has_fac ? tmin(a.fy[y], a.fz[z]) : T(1);
+  int bad = 0;
+  for (int nb = 0; nb < N; nb += Q) {
+#pragma unroll
+    for (int qq = 0; qq < Q; ++qq) {
+      const int n = nb + qq;
+      if (n < N) {
+        const int ip = base + n * xs;
+        qxx[qq] = txx[ip];
+        qxy[qq] = txy[ip];
+        qxz[qq] = txz[ip];
+        if (n >= 2 * R) {
+          const int x = x0 - 2 * R + n;
+          const int i = ip - R * xs;   // centre of the output plane
+          const int cs = (qq - R + Q) % Q;
+          auto qx = [&](const T* q) { return [=](int o) { return q[(cs + o + Q) % Q]; }; };
+          auto gy = [&](const T* p) { return [=](int o) { return p[i + o * ys]; }; };
+          auto gz = [&](const T* p) { return [=](int o) { return p[i + o]; }; };
+          // elastic_update_v (physics.py:348-362), inactive axes skipped
+          T d[3];
+          bool h[3] = {false, false, false};
+#pragma unroll
+          for (int k = 0; k < 3; ++k) d[k] = T(0);
+          if (cf.active[0]) {
+            d[0] = stag<T, R>(qx(qxx), cf.d1[0], true);
+            d[1] = stag<T, R>(qx(qxy), cf.d1[0], false);
+            d[2] = stag<T, R>(qx(qxz), cf.d1[0], false);
+            h[0] = h[1] = h[2] = true;
+          }
+          if (cf.active[1]) {
+            const T e0 = stag<T, R>(gy(txy), cf.d1[1], false);
+            const T e1 = stag<T, R>(gy(tyy), cf.d1[1], true);
+            const T e2 = stag<T, R>(gy(tyz), cf.d1[1], false);
+            d[0] = h[0] ? radd(d[0], e0) : e0;
+            d[1] = h[1] ? radd(d[1], e1) : e1;
+            d[2] = h[2] ? radd(d[2], e2) : e2;
+            h[0] = h[1] = h[2] = true;
+          }
+          if (cf.active[2]) {
+            const T e0 = stag<T, R>(gz(txz), cf.d1[2], false);
+            const T e1 = stag<T, R>(gz(tyz), cf.d1[2], false);
+            const T e2 = stag<T, R>(gz(tzz), cf.d1[2], true);
+            d[0] = h[0] ? radd(d[0], e0) : e0;
+            d[1] = h[1] ? radd(d[1], e1) : e1;
+            d[2] = h[2] ? radd(d[2], e2) : e2;
+            h[0] = h[1] = h[2] = true;
+          }
+          const T buoy = a.buoy ? a.buoy[i] : cf.buoy;
+          const T fac = a.has_fac ? tmin(a.fx[x], fyz) : T(1);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            T* v = a.f[VX + k];
+            T o = v[i];
+            if (h[k]) o = radd(o, rmul(d[k], buoy));
+            if (a.has_fac) o = rmul(o, fac);
+            v[i] = o;
+            if (a.nonfinite) bad |= !finite(o);
+          }
+        }
+      }
+    }
+  }
+  if (a.nonfinite && bad) atomicExch(a.nonfinite, 1);
 }
 
-// Sum of the active terms in order (physics.py:314-321); has = any active.
+// ---------------------------------------------------------------------------
+// stress half step (physics.py:385-429); x derivatives from register queues
+// of vx, vy, vz.
+// ---------------------------------------------------------------------------
 template <typename T, int R>
-__device__ __forceinline__ T dsum3(const ElCoefs<T>& cf, const Pt& p, const T* a0, int ax0,
-                                   bool f0, const T* a1, int ax1, bool f1, const T* a2, int ax2,
-                                   bool f2, bool& has) {
-  const T* arr[3] = {a0, a1, a2};
-  const int ax[3] = {ax0, ax1, ax2};
-  const bool fw[3] = {f0, f1, f2};
-  T acc = T(0);
-  has = false;
+__global__ void __launch_bounds__(256, 3)
+elastic_tau_sweep(ElArgs<T> a) {
+  constexpr int Q = 2 * R + 1;
+  const int z = blockIdx.x * 32 + threadIdx.x;
+  const int y = blockIdx.y * 8 + threadIdx.y;
+  const int x0 = blockIdx.z * a.cx;
+  const int x1 = min(x0 + a.cx, (int)a.d.nx);
+  if (z >= a.d.nz || y >= a.d.ny) return;
+  const int ys = (int)a.d.pitch, xs = (int)a.d.plane;
+  const ElCoefs<T>& cf = a.cf;
+  const T* __restrict__ vx = a.f[VX];
+  const T* __restrict__ vy = a.f[VY];
+  const T* __restrict__ vz = a.f[VZ];
+  T qx_[Q], qy_[Q], qz_[Q];
+#pragma unroll
+  for (int s = 0; s < Q; ++s) qx_[s] = qy_[s] = qz_[s] = T(0);
+  const int N = (x1 - x0) + 2 * R;
+  const int base = (int)a.d.at(x0 - R, y, z);
+  const T fyz = a.has_fac ? tmin(a.fy[y], a.fz[z]) : T(1);
+  int bad = 0;
+  for (int nb = 0; nb < N; nb += Q) {
+#pragma unroll
+    for (int qq = 0; qq < Q; ++qq) {
+      const int n = nb + qq;
+      if (n < N) {
+        const int ip = base + n * xs;
+        qx_[qq] = vx[ip];
+        qy_[qq] = vy[ip];
+        qz_[qq] = vz[ip];
+        if (n >= 2 * R) {
+          const int x = x0 - 2 * R + n;
+          const int i = ip - R * xs;
+          const int cs = (qq - R + Q) % Q;
+          auto qx = [&](const T* q) { return [=](int o) { return q[(cs + o + Q) % Q]; }; };
+          auto gy = [&](const T* p) { return [=](int o) { return p[i + o * ys]; }; };
+          auto gz = [&](const T* p) { return [=](int o) { return p[i + o]; }; };
+          const T lam = a.lam ? a.lam[i] : cf.lam;
+          const T mu = a.mu ? a.mu[i] : cf.mu;
+          const T mu2 = rmul(mu, T(2));
+          const T fac = a.has_fac ? tmin(a.fx[x], fyz) : T(1);
+          T dg[3] = {T(0), T(0), T(0)};
+          if (cf.active[0]) dg[0] = stag<T, R>(qx(qx_), cf.d1[0], false);
+          if (cf.active[1]) dg[1] = stag<T, R>(gy(vy), cf.d1[1], false);
+          if (cf.active[2]) dg[2] = stag<T, R>(gz(vz), cf.d1[2], false);
+          T tr = T(0);
+          bool htr = false;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            if (!cf.active[k]) continue;
+            tr = htr ? radd(tr, dg[k]) : dg[k];
+            htr = true;
+          }
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            T inc = T(0);
+            bool hi = false;
+            if (htr) {
+              inc = rmul(tr, lam);
+              hi = true;
+            }
+            if (cf.active[k]) {
+              const T d2 = rmul(dg[k], mu2);
+              inc = hi ? radd(inc, d2) : d2;
+              hi = true;
+            }
+            T* f = a.f[TXX + k];
+            T o = f[i];
+            if (hi) o = radd(o, inc);
+            if (a.has_fac) o = rmul(o, fac);
+            f[i] = o;
+            if (a.nonfinite) bad |= !finite(o);
+          }
+          // shear: txy (d_y vx, d_x vy), txz (d_z vx, d_x vz), tyz (d_z vy, d_y vz)
+          T s[3] = {T(0), T(0), T(0)};
+          bool hs[3] = {false, false, false};
+          // first terms
+          if (cf.active[1]) { s[0] = stag<T, R>(gy(vx), cf.d1[1], true); hs[0] = true; }
+          if (cf.active[2]) { s[1] = stag<T, R>(gz(vx), cf.d1[2], true); hs[1] = true; }
+          if (cf.active[2]) { s[2] = stag<T, R>(gz(vy), cf.d1[2], true); hs[2] = true; }
+          // second terms
+          if (cf.active[0]) {
+            const T e = stag<T, R>(qx(qy_), cf.d1[0], true);
+            s[0] = hs[0] ? radd(s[0], e) : e;
+            hs[0] = true;
+            const T e2 = stag<T, R>(qx(qz_), cf.d1[0], true);
+            s[1] = hs[1] ? radd(s[1], e2) : e2;
+            hs[1] = true;
+          }
+          if (cf.active[1]) {
+            const T e = stag<T, R>(gy(vz), cf.d1[1], true);
+            s[2] = hs[2] ? radd(s[2], e) : e;
+            hs[2] = true;
+          }
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            T* f = a.f[TXY + k];
+            T o = f[i];
+            if (hs[k]) o = radd(o, rmul(s[k], mu));
+            if (a.has_fac) o = rmul(o, fac);
+            f[i] = o;
+            if (a.nonfinite) bad |= !finite(o);
+          }
+        }
+      }
+    }
+  }
+  if (a.nonfinite && bad) atomicExch(a.nonfinite, 1);
+}
+
+
+// ---------------------------------------------------------------------------
+// Thread-per-point variants (default): full occupancy hides L1/L2 latency of
+// the ~110 neighbour loads per point; the zero halo removes all bounds checks.
+// ---------------------------------------------------------------------------
+template <typename T, int R>
+__global__ void __launch_bounds__(128)
+elastic_v_point(ElArgs<T> a) {
+  const int z = blockIdx.x * 32 + threadIdx.x;
+  const int y = blockIdx.y * 4 + threadIdx.y;
+  const int x = blockIdx.z;
+  if (z >= a.d.nz || y >= a.d.ny) return;
+  const int ys = (int)a.d.pitch, xs = (int)a.d.plane;
+  const int i = (int)a.d.at(x, y, z);
+  const ElCoefs<T>& cf = a.cf;
+  const T* __restrict__ txx = a.f[TXX];
+  const T* __restrict__ txy = a.f[TXY];
+  const T* __restrict__ txz = a.f[TXZ];
+  const T* __restrict__ tyy = a.f[TYY];
+  const T* __restrict__ tyz = a.f[TYZ];
+  const T* __restrict__ tzz = a.f[TZZ];
+  auto gx = [&](const T* p) { return [=](int o) { return p[i + o * xs]; }; };
+  auto gy = [&](const T* p) { return [=](int o) { return p[i + o * ys]; }; };
+  auto gz = [&](const T* p) { return [=](int o) { return p[i + o]; }; };
+  T d[3] = {T(0), T(0), T(0)};
+  bool h[3] = {false, false, false};
+  if (cf.active[0]) {
+    d[0] = stag<T, R>(gx(txx), cf.d1[0], true);
+    d[1] = stag<T, R>(gx(txy), cf.d1[0], false);
+    d[2] = stag<T, R>(gx(txz), cf.d1[0], false);
+    h[0] = h[1] = h[2] = true;
+  }
+  if (cf.active[1]) {
+    const T e0 = stag<T, R>(gy(txy), cf.d1[1], false);
+    const T e1 = stag<T, R>(gy(tyy), cf.d1[1], true);
+    const T e2 = stag<T, R>(gy(tyz), cf.d1[1], false);
+    d[0] = h[0] ? radd(d[0], e0) : e0;
+    d[1] = h[1] ? radd(d[1], e1) : e1;
+    d[2] = h[2] ? radd(d[2], e2) : e2;
+    h[0] = h[1] = h[2] = true;
+  }
+  if (cf.active[2]) {
+    const T e0 = stag<T, R>(gz(txz), cf.d1[2], false);
+    const T e1 = stag<T, R>(gz(tyz), cf.d1[2], false);
+    const T e2 = stag<T, R>(gz(tzz), cf.d1[2], true);
+    d[0] = h[0] ? radd(d[0], e0) : e0;
+    d[1] = h[1] ? radd(d[1], e1) : e1;
+    d[2] = h[2] ? radd(d[2], e2) : e2;
+    h[0] = h[1] = h[2] = true;
+  }
+  const T buoy = a.buoy ? a.buoy[i] : cf.buoy;
+  const T fac = a.has_fac ? tmin(tmin(a.fx[x], a.fy[y]), a.fz[z]) : T(1);
+  bool bad = false;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    if (!cf.active[ax[k]]) continue;
-    const T d = stag<T, R>(arr[k], p.i, p.stride[ax[k]], p.pos[ax[k]], p.n[ax[k]],
-                           cf.d1[ax[k]], fw[k]);
-    acc = has ? radd(acc, d) : d;
-    has = true;
+    T* v = a.f[VX + k];
+    T o = v[i];
+    if (h[k]) o = radd(o, rmul(d[k], buoy));
+    if (a.has_fac) o = rmul(o, fac);
+    v[i] = o;
+    bad |= !finite(o);
   }
-  return acc;
-}
-
-template <typename T>
-__device__ __forceinline__ T fac_at(const ElFields<T>& F, int64_t x, int64_t y, int64_t z) {
-  return tmin(tmin(F.fx[x], F.fy[y]), F.fz[z]);
+  if (a.nonfinite && bad) atomicExch(a.nonfinite, 1);
 }
 
 template <typename T, int R>
 __global__ void __launch_bounds__(128)
-elastic_v_step(ElFields<T> F, ElCoefs<T> cf, Dims d) {
-  const int64_t z = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t y = blockIdx.y, x = blockIdx.z;
-  if (z >= d.nz) return;
-  const Pt p = make_pt(d, x, y, z);
-  const T buoy = F.buoy ? F.buoy[p.i] : cf.buoy;
-  bool h0, h1, h2;
-  // elastic_update_v (physics.py:348-362)
-  const T dvx = dsum3<T, R>(cf, p, F.f[TXX], 0, true, F.f[TXY], 1, false, F.f[TXZ], 2, false, h0);
-  const T dvy = dsum3<T, R>(cf, p, F.f[TXY], 0, false, F.f[TYY], 1, true, F.f[TYZ], 2, false, h1);
-  const T dvz = dsum3<T, R>(cf, p, F.f[TXZ], 0, false, F.f[TYZ], 1, false, F.f[TZZ], 2, true, h2);
-  const T fac = F.has_fac ? fac_at(F, x, y, z) : T(1);
-  const T incs[3] = {dvx, dvy, dvz};
-  const bool has[3] = {h0, h1, h2};
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    T o = F.f[VX + k][p.i];
-    if (has[k]) o = radd(o, rmul(incs[k], buoy));
-    if (F.has_fac) o = rmul(o, fac);
-    F.f[VX + k][p.i] = o;
-  }
-}
-
-template <typename T, int R>
-__global__ void __launch_bounds__(128)
-elastic_tau_step(ElFields<T> F, ElCoefs<T> cf, Dims d) {
-  const int64_t z = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t y = blockIdx.y, x = blockIdx.z;
-  if (z >= d.nz) return;
-  const Pt p = make_pt(d, x, y, z);
-  const T lam = F.lam ? F.lam[p.i] : cf.lam;
-  const T mu = F.mu ? F.mu[p.i] : cf.mu;
+elastic_tau_point(ElArgs<T> a) {
+  const int z = blockIdx.x * 32 + threadIdx.x;
+  const int y = blockIdx.y * 4 + threadIdx.y;
+  const int x = blockIdx.z;
+  if (z >= a.d.nz || y >= a.d.ny) return;
+  const int ys = (int)a.d.pitch, xs = (int)a.d.plane;
+  const int i = (int)a.d.at(x, y, z);
+  const ElCoefs<T>& cf = a.cf;
+  const T* __restrict__ vx = a.f[VX];
+  const T* __restrict__ vy = a.f[VY];
+  const T* __restrict__ vz = a.f[VZ];
+  auto gx = [&](const T* p) { return [=](int o) { return p[i + o * xs]; }; };
+  auto gy = [&](const T* p) { return [=](int o) { return p[i + o * ys]; }; };
+  auto gz = [&](const T* p) { return [=](int o) { return p[i + o]; }; };
+  const T lam = a.lam ? a.lam[i] : cf.lam;
+  const T mu = a.mu ? a.mu[i] : cf.mu;
   const T mu2 = rmul(mu, T(2));
-  const T fac = F.has_fac ? fac_at(F, x, y, z) : T(1);
-  // elastic_update_tau (physics.py:385-429)
-  T dg[3];
-  bool hd[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    hd[a] = cf.active[a] != 0;
-    dg[a] = hd[a] ? stag<T, R>(F.f[VX + a], p.i, p.stride[a], p.pos[a], p.n[a], cf.d1[a], false)
-                  : T(0);
-  }
+  const T fac = a.has_fac ? tmin(tmin(a.fx[x], a.fy[y]), a.fz[z]) : T(1);
+  T dg[3] = {T(0), T(0), T(0)};
+  if (cf.active[0]) dg[0] = stag<T, R>(gx(vx), cf.d1[0], false);
+  if (cf.active[1]) dg[1] = stag<T, R>(gy(vy), cf.d1[1], false);
+  if (cf.active[2]) dg[2] = stag<T, R>(gz(vz), cf.d1[2], false);
   T tr = T(0);
   bool htr = false;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    if (!hd[a]) continue;
-    tr = htr ? radd(tr, dg[a]) : dg[a];
+  for (int k = 0; k < 3; ++k) {
+    if (!cf.active[k]) continue;
+    tr = htr ? radd(tr, dg[k]) : dg[k];
     htr = true;
   }
+  bool bad = false;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
+  for (int k = 0; k < 3; ++k) {
     T inc = T(0);
     bool hi = false;
     if (htr) {
       inc = rmul(tr, lam);
       hi = true;
     }
-    if (hd[a]) {
-      const T d2 = rmul(dg[a], mu2);
+    if (cf.active[k]) {
+      const T d2 = rmul(dg[k], mu2);
       inc = hi ? radd(inc, d2) : d2;
       hi = true;
     }
-    T o = F.f[TXX + a][p.i];
+    T* f = a.f[TXX + k];
+    T o = f[i];
     if (hi) o = radd(o, inc);
-    if (F.has_fac) o = rmul(o, fac);
-    F.f[TXX + a][p.i] = o;
+    if (a.has_fac) o = rmul(o, fac);
+    f[i] = o;
+    bad |= !finite(o);
   }
-  // shear: (txy: d_y vx, d_x vy), (txz: d_z vx, d_x vz), (tyz: d_z vy, d_y vz)
-  const int sa1[3] = {1, 2, 2}, sf1[3] = {VX, VX, VY};
-  const int sa2[3] = {0, 0, 1}, sf2[3] = {VY, VZ, VZ};
+  T s[3] = {T(0), T(0), T(0)};
+  bool hs[3] = {false, false, false};
+  if (cf.active[1]) { s[0] = stag<T, R>(gy(vx), cf.d1[1], true); hs[0] = true; }
+  if (cf.active[2]) { s[1] = stag<T, R>(gz(vx), cf.d1[2], true); hs[1] = true; }
+  if (cf.active[2]) { s[2] = stag<T, R>(gz(vy), cf.d1[2], true); hs[2] = true; }
+  if (cf.active[0]) {
+    const T e = stag<T, R>(gx(vy), cf.d1[0], true);
+    s[0] = hs[0] ? radd(s[0], e) : e;
+    hs[0] = true;
+    const T e2 = stag<T, R>(gx(vz), cf.d1[0], true);
+    s[1] = hs[1] ? radd(s[1], e2) : e2;
+    hs[1] = true;
+  }
+  if (cf.active[1]) {
+    const T e = stag<T, R>(gy(vz), cf.d1[1], true);
+    s[2] = hs[2] ? radd(s[2], e) : e;
+    hs[2] = true;
+  }
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    T s = T(0);
-    bool hs = false;
-    if (cf.active[sa1[k]]) {
-      s = stag<T, R>(F.f[sf1[k]], p.i, p.stride[sa1[k]], p.pos[sa1[k]], p.n[sa1[k]],
-                     cf.d1[sa1[k]], true);
-      hs = true;
-    }
-    if (cf.active[sa2[k]]) {
-      const T d2 = stag<T, R>(F.f[sf2[k]], p.i, p.stride[sa2[k]], p.pos[sa2[k]], p.n[sa2[k]],
-                              cf.d1[sa2[k]], true);
-      s = hs ? radd(s, d2) : d2;
-      hs = true;
-    }
-    T o = F.f[TXY + k][p.i];
-    if (hs) o = radd(o, rmul(s, mu));
-    if (F.has_fac) o = rmul(o, fac);
-    F.f[TXY + k][p.i] = o;
+    T* f = a.f[TXY + k];
+    T o = f[i];
+    if (hs[k]) o = radd(o, rmul(s[k], mu));
+    if (a.has_fac) o = rmul(o, fac);
+    f[i] = o;
+    bad |= !finite(o);
   }
+  if (a.nonfinite && bad) atomicExch(a.nonfinite, 1);
 }
 
-// dt/rho, dt*lam, dt*mu from per-point (or scalar) Lame parameters.
+// dt/rho, dt*lam, dt*mu from per-point Lame parameters (compact host order)
 template <typename T>
 __global__ void elastic_materials_kernel(const double* __restrict__ lam,
                                          const double* __restrict__ mu,
-                                         const double* __restrict__ rho, double dt, Dims d,
+                                         const double* __restrict__ rho, double dt, PDims d,
                                          T* __restrict__ buoy, T* __restrict__ lam_dt,
                                          T* __restrict__ mu_dt) {
   const int64_t n = d.nx * d.ny * d.nz;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t z = i % d.nz, xy = i / d.nz;
-    const int64_t o = xy * d.pitch + z;
-    if (buoy) buoy[o] = from_f64<T>(rdiv(dt, rho[i]));
-    if (lam_dt) lam_dt[o] = from_f64<T>(rmul(dt, lam[i]));
-    if (mu_dt) mu_dt[o] = from_f64<T>(rmul(dt, mu[i]));
+    const int64_t o = d.at(xy / d.ny, xy % d.ny, z);
+    buoy[o] = from_f64<T>(rdiv(dt, rho[i]));
+    lam_dt[o] = from_f64<T>(rmul(dt, lam[i]));
+    mu_dt[o] = from_f64<T>(rmul(dt, mu[i]));
   }
 }
 
@@ -226,26 +479,56 @@ __global__ void to_dtype_kernel_el(const double* __restrict__ src, int64_t n, T*
   if (i < n) dst[i] = from_f64<T>(src[i]);
 }
 
-__global__ void keys_to_offsets_el(const int64_t* __restrict__ keys, int64_t n, Dims d,
+__global__ void keys_to_offsets_el(const int64_t* __restrict__ keys, int64_t n, int64_t gny,
+                                   int64_t gnz, int64_t x_begin, PDims d,
                                    int64_t* __restrict__ off) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t k = keys[i];
-  off[i] = (k / d.nz) * d.pitch + k % d.nz;
+  const int64_t z = k % gnz, xy = k / gnz;
+  off[i] = d.at(xy / gny - x_begin, xy % gny, z);
 }
 
-__global__ void idx_to_offsets_el(const int64_t* __restrict__ idx, int64_t n8, Dims d,
-                                  int64_t* __restrict__ off) {
+__global__ void idx_to_offsets_el(const int64_t* __restrict__ idx, int64_t n8, int64_t x_begin,
+                                  PDims d, int64_t* __restrict__ off, int* bad) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n8) return;
-  off[i] = (idx[i * 3] * d.ny + idx[i * 3 + 1]) * d.pitch + idx[i * 3 + 2];
+  const int64_t x = idx[i * 3] - x_begin;
+  if (x < 0 || x >= d.nx) {
+    atomicExch(bad, 1);
+    off[i] = 0;
+    return;
+  }
+  off[i] = d.at(x, idx[i * 3 + 1], idx[i * 3 + 2]);
+}
+
+template <typename T>
+__global__ void unpad_nonfinite_kernel(const T* __restrict__ u, PDims d, int* flag) {
+  const int64_t n = d.nx * d.ny * d.nz;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = i % d.nz, xy = i / d.nz;
+    if (!finite(u[d.at(xy / d.ny, xy % d.ny, z)])) {
+      atomicExch(flag, 1);
+      return;
+    }
+  }
 }
 
 template <typename T, int R>
-void launch_el(cudaStream_t st, const ElFields<T>& F, const ElCoefs<T>& cf, const Dims& d) {
-  dim3 block(128), grid((unsigned)((d.nz + 127) / 128), (unsigned)d.ny, (unsigned)d.nx);
-  elastic_v_step<T, R><<<grid, block, 0, st>>>(F, cf, d);
-  elastic_tau_step<T, R><<<grid, block, 0, st>>>(F, cf, d);
+void launch_sweeps(cudaStream_t st, const ElArgs<T>& a) {
+  if (a.cx <= 0) {
+    dim3 block(32, 4);
+    dim3 grid((unsigned)((a.d.nz + 31) / 32), (unsigned)((a.d.ny + 3) / 4), (unsigned)a.d.nx);
+    elastic_v_point<T, R><<<grid, block, 0, st>>>(a);
+    elastic_tau_point<T, R><<<grid, block, 0, st>>>(a);
+    return;
+  }
+  dim3 block(32, 8);
+  dim3 grid((unsigned)((a.d.nz + 31) / 32), (unsigned)((a.d.ny + 7) / 8),
+            (unsigned)((a.d.nx + a.cx - 1) / a.cx));
+  elastic_v_sweep<T, R><<<grid, block, 0, st>>>(a);
+  elastic_tau_sweep<T, R><<<grid, block, 0, st>>>(a);
 }
 
 }  // namespace
@@ -255,18 +538,22 @@ class ElasticProp final : public stb_prop_s {
  public:
   explicit ElasticProp(const stb_elastic_desc& desc) {
     R_ = desc.space_order / 2;
-    d_ = make_dims(desc.geom.shape, sizeof(T));
     geom_ = desc.geom;
+    x_begin_ = desc.x_begin;
+    const int64_t nxl = desc.nx_local > 0 ? desc.nx_local : desc.geom.shape[0];
+    STB_REQUIRE(x_begin_ >= 0 && x_begin_ + nxl <= desc.geom.shape[0], STB_ERR_ARG,
+                "x slab [x_begin, x_begin + nx_local) leaves the grid");
+    d_ = make_pdims(nxl, desc.geom.shape[1], desc.geom.shape[2], R_, sizeof(T));
     STB_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     for (int a = 0; a < 3; ++a) {
       cf_.active[a] = desc.active[a] ? 1 : 0;
       for (int j = 0; j < 8; ++j) cf_.d1[a][j] = (T)desc.d1[a][j];
     }
     for (auto& f : f_) {
-      f.alloc(d_.total());
+      f.alloc(d_.total);
       f.zero(st_);
     }
-    const int64_t n = d_.npoints();
+    const int64_t n = d_.nx * d_.ny * d_.nz;
     const double dt = desc.dt;
     // materials (physics.py:251-257)
     const bool any_arr = desc.lam || desc.mu || desc.rho;
@@ -284,9 +571,9 @@ class ElasticProp final : public stb_prop_s {
       fill(lam, desc.lam, desc.lam_scalar);
       fill(mu, desc.mu, desc.mu_scalar);
       fill(rho, desc.rho, desc.rho_scalar);
-      buoy_.alloc(d_.total());
-      lam_.alloc(d_.total());
-      mu_.alloc(d_.total());
+      buoy_.alloc(d_.total);
+      lam_.alloc(d_.total);
+      mu_.alloc(d_.total);
       buoy_.zero(st_);
       lam_.zero(st_);
       mu_.zero(st_);
@@ -304,16 +591,22 @@ class ElasticProp final : public stb_prop_s {
     for (int a = 0; a < 3; ++a) {
       fac_[a].alloc(n3[a]);
       DevBuf<double> tmp(desc.damp[a] ? n3[a] : 0);
-      if (desc.damp[a]) tmp.upload(desc.damp[a], n3[a], st_);
+      if (desc.damp[a]) tmp.upload(desc.damp[a] + (a == 0 ? x_begin_ : 0), n3[a], st_);
       table_kernel_el<T><<<g1(n3[a]), 256, 0, st_>>>(desc.damp[a] ? tmp.p : nullptr, n3[a],
                                                      fac_[a].p);
       STB_CHECK_LAUNCH();
       STB_CUDA(cudaStreamSynchronize(st_));
     }
+    cx_ = 0;   // thread-per-point kernels (x sweeps: STB_ELASTIC_CX > 0)
+    if (const char* e = std::getenv("STB_ELASTIC_CX")) cx_ = std::atoi(e);
+    STB_REQUIRE(d_.total < (int64_t)INT32_MAX, STB_ERR_ARG,
+                "elastic slab too large for 32-bit offsets; use more x slabs");
   }
 
   ~ElasticProp() override {
     for (auto& e : events_) cudaEventDestroy(e);
+    for (auto& e : run_ev_)
+      if (e) cudaEventDestroy(e);
     if (st_) cudaStreamDestroy(st_);
   }
 
@@ -321,18 +614,29 @@ class ElasticProp final : public stb_prop_s {
                    int64_t nt) override {
     for (int a = 0; a < 3; ++a)
       STB_REQUIRE(s.shape[a] == geom_.shape[a], STB_ERR_ARG,
-                  "support was built for a different grid shape");
-    K_ = s.K;
+                  "support was built for a different grid shape (supports are global)");
     src_nt_ = nt;
+    K_ = 0;
+    if (s.K == 0) return;
+    int64_t lohi[2];
+    STB_CUDA(cudaMemcpyAsync(&lohi[0], s.row_ptr.p + x_begin_ * geom_.shape[1], sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, st_));
+    STB_CUDA(cudaMemcpyAsync(&lohi[1], s.row_ptr.p + (x_begin_ + d_.nx) * geom_.shape[1],
+                             sizeof(int64_t), cudaMemcpyDeviceToHost, st_));
+    STB_CUDA(cudaStreamSynchronize(st_));
+    K_ = lohi[1] - lohi[0];
     if (K_ == 0) return;
-    DevBuf<double> dwav(nt_w * s.n_points), dscale(s.n_points), dc(nt * K_);
+    DevBuf<double> dwav(nt_w * s.n_points), dscale(s.n_points), dc(nt * s.K), dl(nt * K_);
     dwav.upload(wav, nt_w * s.n_points, st_);
     dscale.upload(scale, s.n_points, st_);
     support_decompose_dev(s, dwav.p, nt_w, dscale.p, nt, dc.p, st_);
+    STB_CUDA(cudaMemcpy2DAsync(dl.p, K_ * sizeof(double), dc.p + lohi[0], s.K * sizeof(double),
+                               K_ * sizeof(double), nt, cudaMemcpyDeviceToDevice, st_));
     series_.alloc(nt * K_);
-    to_dtype_kernel_el<T><<<g1(nt * K_), 256, 0, st_>>>(dc.p, nt * K_, series_.p);
+    to_dtype_kernel_el<T><<<g1(nt * K_), 256, 0, st_>>>(dl.p, nt * K_, series_.p);
     src_off_.alloc(K_);
-    keys_to_offsets_el<<<g1(K_), 256, 0, st_>>>(s.keys.p, K_, d_, src_off_.p);
+    keys_to_offsets_el<<<g1(K_), 256, 0, st_>>>(s.keys.p + lohi[0], K_, geom_.shape[1],
+                                                geom_.shape[2], x_begin_, d_, src_off_.p);
     STB_CHECK_LAUNCH();
     STB_CUDA(cudaStreamSynchronize(st_));
   }
@@ -346,76 +650,96 @@ class ElasticProp final : public stb_prop_s {
     rec_w_.alloc(nrec * 8);
     stencils_compute(dc.p, nrec, geom_, -1, idx.p, rec_w_.p, st_);
     rec_off_.alloc(nrec * 8);
-    idx_to_offsets_el<<<g1(nrec * 8), 256, 0, st_>>>(idx.p, nrec * 8, d_, rec_off_.p);
+    DevBuf<int> bad(1);
+    bad.zero(st_);
+    idx_to_offsets_el<<<g1(nrec * 8), 256, 0, st_>>>(idx.p, nrec * 8, x_begin_, d_, rec_off_.p,
+                                                     bad.p);
     STB_CHECK_LAUNCH();
+    int hb = 0;
+    bad.download(&hb, 1, st_);
     STB_CUDA(cudaStreamSynchronize(st_));
+    STB_REQUIRE(hb == 0, STB_ERR_ARG, "receiver corners leave this x slab");
   }
 
   void run(int64_t t0, int64_t nsteps, int k, double* rec_out, int64_t* bad_step) override {
     if (bad_step) *bad_step = -1;
+    launches_ = all_launches_ = 0;
+    run_ms_ = 0.0;
+    updates_ = 0;
     if (nsteps <= 0) return;
     STB_REQUIRE(K_ == 0 || t0 + nsteps <= src_nt_, STB_ERR_ARG,
                 "run extends past the decomposed source series");
     STB_REQUIRE(t0 == t_next_, STB_ERR_ARG,
                 "elastic handles update in place: steps must be run in order");
     (void)k;
-    DevBuf<double> rec(nrec_ && rec_out ? nsteps * nrec_ : 0);
+    if (nrec_ && (int64_t)rec_dev_.n < nsteps * nrec_) rec_dev_.alloc(nsteps * nrec_);
     std::vector<int64_t> guard_steps;
     for (int64_t t = t0; t < t0 + nsteps; ++t)
       if (t > 0 && t % 32 == 0) guard_steps.push_back(t);
     DevBuf<int> guards(guard_steps.size() + 1);
     guards.zero(st_);
-    ensure_events(nsteps);
-    ElFields<T> F;
-    for (int i = 0; i < NFIELDS; ++i) F.f[i] = f_[i].p;
-    F.buoy = buoy_.p;
-    F.lam = lam_.p;
-    F.mu = mu_.p;
-    F.fx = fac_[0].p;
-    F.fy = fac_[1].p;
-    F.fz = fac_[2].p;
-    F.has_fac = has_fac_ ? 1 : 0;
-    launches_ = 0;
+    ensure_events(nsteps + 1);
+    ElArgs<T> A{};
+    for (int i = 0; i < NFIELDS; ++i) A.f[i] = f_[i].p;
+    A.buoy = buoy_.p;
+    A.lam = lam_.p;
+    A.mu = mu_.p;
+    A.fx = fac_[0].p;
+    A.fy = fac_[1].p;
+    A.fz = fac_[2].p;
+    A.has_fac = has_fac_ ? 1 : 0;
+    A.cf = cf_;
+    A.d = d_;
+    A.cx = cx_;
     size_t gi = 0;
+    STB_CUDA(cudaEventRecord(run_ev_[0], st_));
     for (int64_t t = t0; t < t0 + nsteps; ++t) {
+      const bool guard_now = gi < guard_steps.size() && guard_steps[gi] == t;
+      // the reference's guard runs after the v half step of a guard step and
+      // checks every field (engine.py:373-376): the v fields are new, the
+      // stress fields still hold t-1 -- checked after the tau sweep here,
+      // which flags the same blow-ups one half step later.
+      A.nonfinite = guard_now ? guards.p + gi : nullptr;
       STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
       switch (R_) {
-        case 1: launch_el<T, 1>(st_, F, cf_, d_); break;
-        case 2: launch_el<T, 2>(st_, F, cf_, d_); break;
-        case 3: launch_el<T, 3>(st_, F, cf_, d_); break;
-        case 4: launch_el<T, 4>(st_, F, cf_, d_); break;
-        case 5: launch_el<T, 5>(st_, F, cf_, d_); break;
-        case 6: launch_el<T, 6>(st_, F, cf_, d_); break;
-        case 7: launch_el<T, 7>(st_, F, cf_, d_); break;
-        case 8: launch_el<T, 8>(st_, F, cf_, d_); break;
+        case 1: launch_sweeps<T, 1>(st_, A); break;
+        case 2: launch_sweeps<T, 2>(st_, A); break;
+        case 3: launch_sweeps<T, 3>(st_, A); break;
+        case 4: launch_sweeps<T, 4>(st_, A); break;
+        case 5: launch_sweeps<T, 5>(st_, A); break;
+        case 6: launch_sweeps<T, 6>(st_, A); break;
+        case 7: launch_sweeps<T, 7>(st_, A); break;
+        case 8: launch_sweeps<T, 8>(st_, A); break;
         default: throw Error(STB_ERR_ARG, "space_order must be even in [2, 16]");
       }
       STB_CHECK_LAUNCH();
       STB_CUDA(cudaEventRecord(events_[2 * launches_ + 1], st_));
       ++launches_;
-      if (gi < guard_steps.size() && guard_steps[gi] == t) {
-        for (int fi = 0; fi < NFIELDS; ++fi)
-          nonfinite_kernel<T><<<1184, 256, 0, st_>>>(f_[fi].p, d_, guards.p + gi);
-        STB_CHECK_LAUNCH();
-        ++gi;
-      }
+      all_launches_ += 2;
+      if (guard_now) ++gi;
       if (K_) {
         for (int fi = TXX; fi <= TZZ; ++fi)
           inject_kernel<T><<<g1(K_), 256, 0, st_>>>(f_[fi].p, src_off_.p, series_.p + t * K_, K_);
         STB_CHECK_LAUNCH();
+        all_launches_ += 3;
       }
-      if (rec.n) {
+      if (nrec_) {
         gather_kernel<T><<<g1(nrec_), 256, 0, st_>>>(f_[TXX].p, rec_off_.p, rec_w_.p, nrec_,
-                                                     rec.p + (t - t0) * nrec_);
+                                                     rec_dev_.p + (t - t0) * nrec_);
         STB_CHECK_LAUNCH();
+        ++all_launches_;
       }
     }
+    STB_CUDA(cudaEventRecord(run_ev_[1], st_));
     t_next_ = t0 + nsteps;
-    updates_ = nsteps * d_.npoints() * NFIELDS;
-    if (rec.n) rec.download(rec_out, nsteps * nrec_, st_);
+    updates_ = nsteps * d_.nx * d_.ny * d_.nz;
+    if (nrec_ && rec_out) rec_dev_.download(rec_out, nsteps * nrec_, st_);
     std::vector<int> gh(guard_steps.size() + 1, 0);
     if (!guard_steps.empty()) guards.download(gh.data(), guard_steps.size(), st_);
     STB_CUDA(cudaStreamSynchronize(st_));
+    float rm = 0.f;
+    STB_CUDA(cudaEventElapsedTime(&rm, run_ev_[0], run_ev_[1]));
+    run_ms_ = rm;
     for (size_t i = 0; i < guard_steps.size(); ++i) {
       if (gh[i]) {
         if (bad_step) *bad_step = guard_steps[i];
@@ -430,15 +754,22 @@ class ElasticProp final : public stb_prop_s {
     STB_REQUIRE(field >= 0 && field < NFIELDS, STB_ERR_ARG, "elastic field index in [0, 9)");
     STB_REQUIRE(t == t_next_ - 1 || (t_next_ == 0), STB_ERR_ARG,
                 "only the latest time level is resident for elastic handles");
-    STB_CUDA(cudaMemcpy2DAsync(out, d_.nz * sizeof(T), f_[field].p, d_.pitch * sizeof(T),
-                               d_.nz * sizeof(T), d_.nx * d_.ny, cudaMemcpyDeviceToHost, st_));
+    cudaMemcpy3DParms p{};
+    p.srcPtr = make_cudaPitchedPtr(f_[field].p, d_.pitch * sizeof(T), d_.pitch, d_.ny + 2 * d_.H);
+    p.srcPos = make_cudaPos(d_.zoff * sizeof(T), d_.H, d_.H);
+    p.dstPtr = make_cudaPitchedPtr(out, d_.nz * sizeof(T), d_.nz, d_.ny);
+    p.dstPos = make_cudaPos(0, 0, 0);
+    p.extent = make_cudaExtent(d_.nz * sizeof(T), d_.ny, d_.nx);
+    p.kind = cudaMemcpyDeviceToHost;
+    STB_CUDA(cudaMemcpy3DAsync(&p, st_));
     STB_CUDA(cudaStreamSynchronize(st_));
   }
 
+  // Planes of the padded layout: local plane p starts at (p + H) * plane.
   void level_ptr(int field, int64_t t, void** dev, int64_t* plane, int64_t* pitch) override {
     STB_REQUIRE(field >= 0 && field < NFIELDS, STB_ERR_ARG, "elastic field index in [0, 9)");
     (void)t;
-    *dev = f_[field].p;
+    *dev = f_[field].p + d_.H * d_.plane;
     if (plane) *plane = d_.plane;
     if (pitch) *pitch = d_.pitch;
   }
@@ -460,19 +791,26 @@ class ElasticProp final : public stb_prop_s {
     if (launches) *launches = launches_;
     if (ms) *ms = total;
     if (updates) *updates = updates_;
-    if (all_launches) *all_launches = launches_ * 2;
-    if (run_ms) *run_ms = total;
+    if (all_launches) *all_launches = all_launches_;
+    if (run_ms) *run_ms = run_ms_;
   }
 
   std::string describe(int k) override {
     std::ostringstream os;
-    os << "elastic_reference_step<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
-       << "> k=" << (k < 1 ? 1 : k);
+    if (cx_ > 0)
+      os << "elastic_sweeps<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
+         << "> (v + tau x-sweeps, 32x8 threads, cx=" << cx_ << ")";
+    else
+      os << "elastic_point<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
+         << "> (v + tau, thread per point, zero-haloed layout)";
+    os << " k=1 requested_k=" << k << " bytes_per_point=" << 30 * sizeof(T);
     return os.str();
   }
 
  private:
   void ensure_events(int64_t n) {
+    for (auto& e : run_ev_)
+      if (!e) STB_CUDA(cudaEventCreate(&e));
     while ((int64_t)events_.size() < 2 * n) {
       cudaEvent_t e;
       STB_CUDA(cudaEventCreate(&e));
@@ -481,23 +819,27 @@ class ElasticProp final : public stb_prop_s {
   }
 
   int R_ = 1;
-  Dims d_{};
+  PDims d_{};
   stb_geometry geom_{};
+  int64_t x_begin_ = 0;
   cudaStream_t st_ = nullptr;
   ElCoefs<T> cf_{};
   DevBuf<T> f_[NFIELDS];
   DevBuf<T> buoy_, lam_, mu_;
   DevBuf<T> fac_[3];
   bool has_fac_ = false;
+  int cx_ = 64;
   int64_t t_next_ = 0;
   int64_t K_ = 0, src_nt_ = 0;
   DevBuf<T> series_;
   DevBuf<int64_t> src_off_;
   int64_t nrec_ = 0;
   DevBuf<int64_t> rec_off_;
-  DevBuf<double> rec_w_;
+  DevBuf<double> rec_w_, rec_dev_;
   std::vector<cudaEvent_t> events_;
-  int64_t launches_ = 0, updates_ = 0;
+  cudaEvent_t run_ev_[2] = {nullptr, nullptr};
+  int64_t launches_ = 0, all_launches_ = 0, updates_ = 0;
+  double run_ms_ = 0.0;
 };
 
 }  // namespace stb
