@@ -388,8 +388,6 @@ def build_propagator(config: RunConfig, dt: float, v_max: float, x_begin: int = 
         raw = C.c_void_p()
         _lib.check(_lib.lib().stb_acoustic_create(C.byref(d), C.byref(raw)))
         return _Prop(raw, config.dtype, ACOUSTIC_FIELDS)
-    if nx_local:
-        raise NotImplementedError("x-slab handles cover the acoustic path")
     vp = np.asarray(config.medium["vp"], dtype=np.float64)
     vs = np.asarray(config.medium["vs"], dtype=np.float64)
     rho = np.asarray(config.medium["rho"], dtype=np.float64)
@@ -404,6 +402,7 @@ def build_propagator(config: RunConfig, dt: float, v_max: float, x_begin: int = 
     d = _lib.ElasticDesc()
     d.geom = _lib.geometry(grid)
     d.space_order, d.precision, d.dt = config.space_order, config.precision, dt
+    d.x_begin, d.nx_local = int(x_begin), int(nx_local)
     d1 = elastic_coefficients(grid, config.space_order)
     for a in range(3):
         d.active[a] = int(grid.shape[a] > 1)
@@ -413,7 +412,10 @@ def build_propagator(config: RunConfig, dt: float, v_max: float, x_begin: int = 
         if arr.ndim == 0:
             setattr(d, f"{name}_scalar", float(arr))
         else:
-            a3 = np.ascontiguousarray(np.broadcast_to(arr, grid.shape), dtype=np.float64)
+            a3 = np.broadcast_to(arr, grid.shape)
+            if nx_local:
+                a3 = a3[x_begin:x_begin + nx_local]
+            a3 = np.ascontiguousarray(a3, dtype=np.float64)
             keep.append(a3)
             setattr(d, name, _lib.dptr(a3.reshape(-1)))
     if tables is not None:

@@ -32,8 +32,8 @@ import math
 import numpy as np
 
 from . import _lib
-from .engine import (_gpu_time_height, _Handle, _Prop, _wavelets, build_propagator,
-                     medium_velocity_bounds, resolve_steps)
+from .engine import (ACOUSTIC_FIELDS, ELASTIC_FIELDS, _gpu_time_height, _Handle, _Prop,
+                     _wavelets, build_propagator, medium_velocity_bounds, resolve_steps)
 from .sparse import nearest_scales_from_velocity, stencils, validate_coords_in_extent
 
 DEFAULT_TIME_HEIGHT = 1
@@ -46,8 +46,12 @@ def partition(nx: int, world: int, rank: int) -> tuple[int, int]:
     return a, a + base + (1 if rank < extra else 0)
 
 
-def ghost_depth(k: int, radius: int) -> int:
-    return k * radius + 1
+def ghost_depth(k: int, radius: int, physics: str = "acoustic") -> int:
+    """Planes each side that k fused steps consume, +1 for receivers that
+    straddle the slab boundary.  Elastic: the v and tau half steps each
+    consume R planes per step (schedule.py:81-90: skew 2R)."""
+    per_step = 2 * radius if physics == "elastic" else radius
+    return k * per_step + 1
 
 
 class _DevArray:
@@ -81,18 +85,18 @@ class DeviceSlab:
     def run(self, t0, n, k, rec_out=None):
         self.prop.run(t0, n, k, rec_out)
 
-    def planes(self, t: int, i: int, j: int):
+    def planes(self, t: int, i: int, j: int, field: int = 0):
         """torch view of local planes [i, j) of time level t (contiguous)."""
         import torch
         dev, plane, pitch = C.c_void_p(), C.c_int64(), C.c_int64()
-        _lib.check(_lib.lib().stb_prop_level_ptr(self.prop.raw, 0, t, C.byref(dev),
+        _lib.check(_lib.lib().stb_prop_level_ptr(self.prop.raw, field, t, C.byref(dev),
                                                  C.byref(plane), C.byref(pitch)))
         typestr = "<f4" if self.item == 4 else "<f8"
         base = dev.value + i * plane.value * self.item
         return torch.as_tensor(_DevArray(base, (j - i, plane.value), typestr), device="cuda")
 
-    def read(self, t, shape):
-        return self.prop.read("u", t, shape)
+    def read(self, t, shape, name="u"):
+        return self.prop.read(name, t, shape)
 
     def stats(self):
         return self.prop.stats()
@@ -110,18 +114,18 @@ class SlabRunner:
 
     def __init__(self, config, rank: int = 0, world: int = 1, backend_factory=None,
                  group=None):
-        if config.physics != "acoustic":
-            raise NotImplementedError("x-slab runner covers the acoustic path")
         self.config, self.rank, self.world, self.group = config, rank, world, group
+        self.elastic = config.physics == "elastic"
+        self.field_names = ELASTIC_FIELDS if self.elastic else ACOUSTIC_FIELDS
         self.dt, self.nt = resolve_steps(config)
         k = _gpu_time_height(config)
-        self.time_height = k if k > 0 else DEFAULT_TIME_HEIGHT
+        self.time_height = 1 if self.elastic else (k if k > 0 else DEFAULT_TIME_HEIGHT)
         grid = config.grid
         nx = grid.shape[0]
         R = config.space_order // 2
         self.R = R
         self.a, self.b = partition(nx, world, rank)
-        G = ghost_depth(self.time_height, R) if world > 1 else 0
+        G = ghost_depth(self.time_height, R, config.physics) if world > 1 else 0
         if world > 1 and self.b - self.a < G:
             raise ValueError(f"x slab of {self.b - self.a} planes is thinner than the "
                              f"ghost depth {G}; use fewer ranks or a smaller time_height")
@@ -138,8 +142,11 @@ class SlabRunner:
         if spec is not None and spec.nsrc and self.nt > 0:
             validate_coords_in_extent(spec.coords, grid, what="source")
             wav = _wavelets(config, self.dt, self.nt)
-            scale = nearest_scales_from_velocity(spec.coords, grid, config.medium["velocity"],
-                                                 self.dt)
+            if self.elastic:
+                scale = np.full(spec.nsrc, self.dt)       # engine.py:277-278
+            else:
+                scale = nearest_scales_from_velocity(spec.coords, grid,
+                                                     config.medium["velocity"], self.dt)
             self.dev.set_sources(spec.coords, wav, scale, self.nt)
         # receivers owned by base plane
         self.rec_index = np.zeros(0, dtype=np.int64)
@@ -192,8 +199,10 @@ class SlabRunner:
             self._accumulate()
             if rec is not None:
                 self._traces.append((t, rec))
-            newest = [t + kb - 1] + ([t + kb - 2] if kb >= 2 else [])
-            self.exchange(newest)
+            if self.elastic:
+                self.exchange([t], fields=range(len(self.field_names)))   # in place
+            else:
+                self.exchange([t + kb - 1] + ([t + kb - 2] if kb >= 2 else []))
             t += kb
 
     def _accumulate(self):
@@ -201,35 +210,46 @@ class SlabRunner:
         for key, val in st.items():
             self._acc[key] = self._acc.get(key, 0) + val
 
-    def exchange(self, levels):
-        """Refresh ghost planes of the given time levels from the neighbours."""
+    def exchange(self, levels, fields=(0,)):
+        """Refresh ghost planes of the given time levels (and fields) from the
+        neighbours."""
         import torch.distributed as dist
         ops = []
         g_lo, g_hi = self.a - self.lo, self.hi - self.b
         for t in levels:
-            if self.rank > 0:
-                ops.append(dist.P2POp(dist.isend, self.dev.planes(t, g_lo, g_lo + g_lo),
-                                      self.rank - 1, group=self.group))
-                ops.append(dist.P2POp(dist.irecv, self.dev.planes(t, 0, g_lo), self.rank - 1,
-                                      group=self.group))
-            if self.rank < self.world - 1:
-                ops.append(dist.P2POp(dist.isend,
-                                      self.dev.planes(t, self.nl - g_hi - g_hi, self.nl - g_hi),
-                                      self.rank + 1, group=self.group))
-                ops.append(dist.P2POp(dist.irecv, self.dev.planes(t, self.nl - g_hi, self.nl),
-                                      self.rank + 1, group=self.group))
+            for f in fields:
+                pl = lambda i, j: self.dev.planes(t, i, j, f)   # noqa: E731
+                if self.rank > 0:
+                    ops.append(dist.P2POp(dist.isend, pl(g_lo, g_lo + g_lo), self.rank - 1,
+                                          group=self.group))
+                    ops.append(dist.P2POp(dist.irecv, pl(0, g_lo), self.rank - 1,
+                                          group=self.group))
+                if self.rank < self.world - 1:
+                    ops.append(dist.P2POp(dist.isend, pl(self.nl - g_hi - g_hi, self.nl - g_hi),
+                                          self.rank + 1, group=self.group))
+                    ops.append(dist.P2POp(dist.irecv, pl(self.nl - g_hi, self.nl),
+                                          self.rank + 1, group=self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
         self.dev.synchronize()
 
     # ------------------------------------------------------------ results
-    def gather_field(self, t: int):
-        """Full field at level t on rank 0 (None elsewhere)."""
+    def gather_fields(self, t: int) -> dict | None:
+        """All output fields at level t on rank 0 ({name: array}; None elsewhere)."""
+        out = {}
+        for name in self.field_names:
+            arr = self.gather_field(t, name)
+            if arr is not None:
+                out[name] = arr
+        return out if (self.rank == 0) else None
+
+    def gather_field(self, t: int, name: str = "u"):
+        """Full field `name` at level t on rank 0 (None elsewhere)."""
         import torch
         import torch.distributed as dist
         g = self.config.grid
-        local = self.dev.read(t, (self.nl, g.shape[1], g.shape[2]))
+        local = self.dev.read(t, (self.nl, g.shape[1], g.shape[2]), name)
         own = np.ascontiguousarray(local[self.a - self.lo: self.b - self.lo])
         if self.world == 1:
             return own
@@ -291,15 +311,19 @@ class SlabRunner:
         k >= 2 writes the last two levels (20 B).  The sponge uses 1-D
         tables (0 B/pt)."""
         item = np.dtype(self.config.dtype).itemsize
+        if self.elastic:
+            # separate v and tau launches: (6 tau + 3 v + buoy) reads + 3 v
+            # writes, then (3 v + 6 tau + lam + mu) reads + 6 tau writes
+            return 30 * item
         return (4 if self.time_height == 1 else 5) * item
 
 
 def run_distributed(config, rank: int, world: int, group=None, backend_factory=None):
-    """Whole forward run over x-slabs; rank 0 returns (fields, traces)."""
+    """Whole forward run over x-slabs; rank 0 returns ({name: field}, traces)."""
     runner = SlabRunner(config, rank, world, backend_factory=backend_factory, group=group)
     nt = runner.nt
     if nt > 0:
         runner.run(0, nt, record=True)
-    field = runner.gather_field(nt - 1 if nt > 0 else 0)
+    fields = runner.gather_fields(nt - 1 if nt > 0 else 0)
     traces = runner.gather_receivers(nt) if runner.nrec_total else None
-    return field, traces
+    return fields, traces

@@ -20,19 +20,42 @@ class OracleSlab:
         self.R = config.space_order // 2
         self.x_begin, self.nl = x_begin, nx_local
         self.dtype = np.float32 if config.precision == 32 else np.float64
+        self.elastic = config.physics == "elastic"
         bl = g.boundary_layers
         decay = (config.damping_decay if config.damping_decay is not None
                  else so.default_decay(g.shape, g.spacing, bl, v_max))
         damp = so.damping3d(g.shape, bl, decay)[x_begin:x_begin + nx_local] if bl else None
-        vel = config.medium["velocity"]
-        if np.ndim(vel):
-            m = (1.0 / np.asarray(vel, dtype=np.float64) ** 2)[x_begin:x_begin + nx_local]
-        else:
-            m = 1.0 / float(vel) ** 2
         shape_l = (nx_local,) + tuple(g.shape[1:])
-        self.model = so.Acoustic(shape_l, g.spacing, config.space_order, m, dt, damp, self.dtype)
+        sl = slice(x_begin, x_begin + nx_local)
+
+        def local(a):
+            return a if np.ndim(a) == 0 else np.broadcast_to(a, g.shape)[sl]
+
+        if self.elastic:
+            vp = np.asarray(config.medium["vp"], np.float64)
+            vs = np.asarray(config.medium["vs"], np.float64)
+            rho = np.asarray(config.medium["rho"], np.float64)
+            mu = rho * vs ** 2
+            lam = rho * vp ** 2 - 2.0 * mu
+            if lam.ndim == 0:
+                lam, mu, rho = float(lam), float(mu), float(rho)
+            self.model = so.Elastic(shape_l, g.spacing, config.space_order, local(lam),
+                                    local(mu), local(rho), dt, damp, self.dtype)
+            self.names = so.Elastic.V + so.Elastic.T
+        else:
+            vel = config.medium["velocity"]
+            if np.ndim(vel):
+                m = (1.0 / np.asarray(vel, dtype=np.float64) ** 2)[sl]
+            else:
+                m = 1.0 / float(vel) ** 2
+            self.model = so.Acoustic(shape_l, g.spacing, config.space_order, m, dt, damp,
+                                     self.dtype)
+            self.names = ("u",)
         self.pts = None
         self.ridx = None
+
+    def _level(self, name, t):
+        return self.model.lv(name, t) if self.elastic else self.model.level(t)
 
     def stencil_index(self, coords):
         g = self.config.grid
@@ -58,23 +81,29 @@ class OracleSlab:
 
     def run(self, t0, n, k, rec_out=None):
         R = self.R
+        targets = ("txx", "tyy", "tzz") if self.elastic else ("u",)
+        gather = "txx" if self.elastic else "u"
         for t in range(t0, t0 + n):
             self.model.step(t)
             if self.pts is not None and len(self.pts):
-                lvl = self.model.level(t)
                 p = self.pts
-                lvl[p[:, 0] + R, p[:, 1] + R, p[:, 2] + R] += self.dcmp[t].astype(self.dtype)
+                for name in targets:
+                    lvl = self._level(name, t)
+                    lvl[p[:, 0] + R, p[:, 1] + R, p[:, 2] + R] += self.dcmp[t].astype(self.dtype)
             if rec_out is not None and self.ridx is not None:
-                rec_out[t - t0] = so.record(self.model.level(t), self.ridx, self.rw, R)
+                rec_out[t - t0] = so.record(self._level(gather, t), self.ridx, self.rw, R)
+        self.t_last = t0 + n - 1
 
-    def planes(self, t, i, j):
+    def planes(self, t, i, j, field=0):
         import torch
         R = self.R
-        return torch.from_numpy(self.model.level(t)[R + i:R + j])
+        if self.elastic:        # in place: the newest level is the state
+            t = self.t_last
+        return torch.from_numpy(self._level(self.names[field], t)[R + i:R + j])
 
-    def read(self, t, shape):
+    def read(self, t, shape, name="u"):
         R = self.R
-        return self.model.level(t)[R:-R, R:-R, R:-R].copy()
+        return self._level(name, t)[R:-R, R:-R, R:-R].copy()
 
     def synchronize(self):
         pass

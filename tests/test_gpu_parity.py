@@ -258,20 +258,19 @@ def test_cfg1_fma_mode_tolerance(golden_big):
 
 # ------------------------------------------------- x-slab device mechanics
 
-@pytest.mark.parametrize("k", [1, 2])
-def test_xslab_handles_emulated_two_ranks(k):
+@pytest.mark.parametrize("kind,k", [("acoustic", 1), ("acoustic", 2), ("elastic", 1)])
+def test_xslab_handles_emulated_two_ranks(kind, k):
     """Two x-slab handles on one GPU, ghost planes exchanged by device
     copies in the order slabs.SlabRunner uses (NCCL replaced by copies: two
     NCCL ranks must not share one GPU).  Stitched owned planes and traces
     equal the single-device run bit for bit."""
     import torch
     from paper_2010_10248_b200 import slabs
-    from test_slabs_gloo import _case
-    cfg = _case(k)
+    from test_slabs_gloo import _make
+    cfg = _make(kind, k)
     world = 2
-    ranks = []
-    for r in range(world):
-        ranks.append(slabs.SlabRunner(cfg, r, world))
+    ranks = [slabs.SlabRunner(cfg, r, world) for r in range(world)]
+    nf = len(ranks[0].field_names)
     nt = ranks[0].nt
     t = 0
     while t < nt:
@@ -283,20 +282,24 @@ def test_xslab_handles_emulated_two_ranks(k):
                 rr._traces.append((t, rec))
         lo, hi = ranks
         g = lo.hi - lo.b                       # ghost planes on each side
-        for lev in [t + kb - 1] + ([t + kb - 2] if kb >= 2 else []):
-            # rank 0 top ghost <- rank 1 first owned planes; and vice versa
-            lo.dev.planes(lev, lo.nl - g, lo.nl).copy_(hi.dev.planes(lev, g, 2 * g))
-            hi.dev.planes(lev, 0, g).copy_(lo.dev.planes(lev, lo.nl - 2 * g, lo.nl - g))
+        levels = [t] if kind == "elastic" else [t + kb - 1] + ([t + kb - 2] if kb >= 2 else [])
+        for lev in levels:
+            for f in range(nf):
+                # rank 0 top ghost <- rank 1 first owned planes; and vice versa
+                lo.dev.planes(lev, lo.nl - g, lo.nl, f).copy_(hi.dev.planes(lev, g, 2 * g, f))
+                hi.dev.planes(lev, 0, g, f).copy_(lo.dev.planes(lev, lo.nl - 2 * g, lo.nl - g, f))
         torch.cuda.synchronize()
         t += kb
     shape = cfg.grid.shape
-    field = np.empty(shape, dtype=np.float32)
     traces = np.zeros((nt, len(cfg.receiver_coords)))
+    ref = so.run(cfg)
+    for name in ranks[0].field_names:
+        field = np.empty(shape, dtype=np.float32)
+        for rr in ranks:
+            loc = rr.dev.read(nt - 1, (rr.nl,) + shape[1:], name)
+            field[rr.a:rr.b] = loc[rr.a - rr.lo: rr.b - rr.lo]
+        np.testing.assert_array_equal(field, ref.fields[name], err_msg=name)
     for rr in ranks:
-        loc = rr.dev.read(nt - 1, (rr.nl,) + shape[1:])
-        field[rr.a:rr.b] = loc[rr.a - rr.lo: rr.b - rr.lo]
         for t0, rec in rr._traces:
             traces[t0:t0 + rec.shape[0], rr.rec_index] = rec
-    ref = so.run(cfg)
-    np.testing.assert_array_equal(field, ref.fields["u"])
     np.testing.assert_array_equal(traces, ref.receivers)

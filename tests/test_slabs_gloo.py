@@ -39,29 +39,50 @@ def _case(k):
                          schedule=stb.ScheduleSpec("gpu", time_height=k))
 
 
-def _worker(rank, world, port, k, out_path):
+def _elastic_case():
+    import paper_2010_10248_b200 as stb
+    rng = np.random.default_rng(6)
+    shape = (40, 16, 18)
+    grid = stb.GridSpec(shape, (10.0, 10.0, 10.0), (0.0, 0.0, 0.0), boundary_layers=3)
+    vp = rng.uniform(2000.0, 3500.0, shape)
+    src = np.array([[197.0, 75.0, 85.0], [101.3, 60.0, 90.5]])
+    rec = random_coords(rng, shape, grid.spacing, grid.origin, 8, margin=4)
+    rec[0] = [195.5, 70.0, 80.0]            # straddles x = 20 (2 ranks)
+    return stb.RunConfig(physics="elastic", grid=grid, space_order=4, nt=9, dt=0.4e-3,
+                         medium={"vp": vp, "vs": vp / 1.7, "rho": 2100.0},
+                         sources=stb.SourceSpec(src, f0=30.0), receiver_coords=rec)
+
+
+def _make(kind, k):
+    return _elastic_case() if kind == "elastic" else _case(k)
+
+
+def _worker(rank, world, port, k, out_path, kind="acoustic"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2010_10248_b200.slabs import run_distributed
         from slab_cpu_backend import OracleSlab
-        field, traces = run_distributed(_case(k), rank, world, backend_factory=OracleSlab)
+        fields, traces = run_distributed(_make(kind, k), rank, world, backend_factory=OracleSlab)
         if rank == 0:
-            np.savez(out_path, field=field, traces=traces)
+            np.savez(out_path, traces=traces, **fields)
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,k", [(2, 1), (2, 2), (3, 1)])
-def test_xslab_matches_single_domain(world, k, tmp_path):
+@pytest.mark.parametrize("kind,world,k", [("acoustic", 2, 1), ("acoustic", 2, 2),
+                                          ("acoustic", 3, 1), ("elastic", 2, 1),
+                                          ("elastic", 3, 1)])
+def test_xslab_matches_single_domain(kind, world, k, tmp_path):
     from oracle import stencil_oracle as so
     out = str(tmp_path / "res.npz")
-    mp.start_processes(_worker, args=(world, _free_port(), k, out), nprocs=world,
+    mp.start_processes(_worker, args=(world, _free_port(), k, out, kind), nprocs=world,
                        join=True, start_method="spawn")
     got = np.load(out)
-    ref = so.run(_case(k))
-    np.testing.assert_array_equal(got["field"], ref.fields["u"])
+    ref = so.run(_make(kind, k))
+    for name, arr in ref.fields.items():
+        np.testing.assert_array_equal(got[name], arr, err_msg=name)
     np.testing.assert_array_equal(got["traces"], ref.receivers)
 
 
