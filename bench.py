@@ -298,9 +298,25 @@ def main():
                "wall_s": e2e_s, "api": "paper_2010_10248_b200.run(RunConfig) (host numpy in/out)",
                "note": "includes model upload, GPU inspector, stepping, field+trace download"}
         del res
-    elif world > 1:
-        e2e = {"value": None, "unit": "GPts/s", "h2d_bytes_per_step": None,
-               "d2h_bytes_per_step": None, "note": "e2e measured at N=1 only"}
+    elif not args.no_e2e and world > 1:
+        # public multi-GPU entry: x-slab run + gather of field and traces on rank 0
+        cfg_e = make_config(stb, v, src, rec, args.steps, args.k, args.arithmetic)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        fields, traces = slabs.run_distributed(cfg_e, rank, world)
+        torch.cuda.synchronize()
+        wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+        e2e_s = float(wall.item())
+        h2d = v.nbytes + src.nbytes + rec.nbytes + 8 * sum(SHAPE) + 8 * args.steps
+        d2h = 4 * npts + 8 * args.steps * len(rec)
+        e2e = {"value": npts * args.steps / e2e_s / 1e9, "unit": "GPts/s",
+               "h2d_bytes_per_step": int(h2d / args.steps),
+               "d2h_bytes_per_step": int(d2h / args.steps), "wall_s": e2e_s,
+               "api": "paper_2010_10248_b200.slabs.run_distributed (host numpy in/out, "
+                      "gathered on rank 0)"}
+        del fields, traces
 
     # ------------------------------------------------------------ cpu baseline
     cpu = None

@@ -109,6 +109,15 @@ class DeviceSlab:
         torch.cuda.synchronize()
 
 
+def _wire(t):
+    """Tensor for a point-to-point collective: NCCL needs device tensors."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        return t.cuda()
+    return t
+
+
 class SlabRunner:
     """One rank's share of a run.  world == 1 is the plain single-GPU run."""
 
@@ -258,11 +267,12 @@ class SlabRunner:
             out[self.a:self.b] = own
             for r in range(1, self.world):
                 a, b = partition(g.shape[0], self.world, r)
-                buf = torch.empty((b - a,) + g.shape[1:], dtype=torch.from_numpy(own).dtype)
+                buf = _wire(torch.empty((b - a,) + g.shape[1:],
+                                        dtype=torch.from_numpy(own).dtype))
                 dist.recv(buf, r, group=self.group)
-                out[a:b] = buf.numpy()
+                out[a:b] = buf.cpu().numpy()
             return out
-        dist.send(torch.from_numpy(own), 0, group=self.group)
+        dist.send(_wire(torch.from_numpy(own)), 0, group=self.group)
         return None
 
     def gather_receivers(self, nt: int):
@@ -278,20 +288,23 @@ class SlabRunner:
             out = np.zeros((nt, self.nrec_total), dtype=np.float64)
             out[:, self.rec_index] = mine
             for r in range(1, self.world):
-                n = torch.zeros(1, dtype=torch.int64)
+                n = _wire(torch.zeros(1, dtype=torch.int64))
                 dist.recv(n, r, group=self.group)
-                if int(n.item()) == 0:
+                cnt = int(n.item())
+                if cnt == 0:
                     continue
-                idx = torch.zeros(int(n.item()), dtype=torch.int64)
+                idx = _wire(torch.zeros(cnt, dtype=torch.int64))
                 dist.recv(idx, r, group=self.group)
-                buf = torch.zeros((nt, int(n.item())), dtype=torch.float64)
+                buf = _wire(torch.zeros((nt, cnt), dtype=torch.float64))
                 dist.recv(buf, r, group=self.group)
-                out[:, idx.numpy()] = buf.numpy()
+                out[:, idx.cpu().numpy()] = buf.cpu().numpy()
             return out
-        dist.send(torch.tensor([len(self.rec_index)], dtype=torch.int64), 0, group=self.group)
+        dist.send(_wire(torch.tensor([len(self.rec_index)], dtype=torch.int64)), 0,
+                  group=self.group)
         if len(self.rec_index):
-            dist.send(torch.from_numpy(self.rec_index.astype(np.int64)), 0, group=self.group)
-            dist.send(torch.from_numpy(mine), 0, group=self.group)
+            dist.send(_wire(torch.from_numpy(self.rec_index.astype(np.int64))), 0,
+                      group=self.group)
+            dist.send(_wire(torch.from_numpy(mine)), 0, group=self.group)
         return None
 
     # ------------------------------------------------------------ reporting
