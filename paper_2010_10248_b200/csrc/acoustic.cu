@@ -472,7 +472,7 @@ class AcousticProp final : public stb_prop_s {
     std::ostringstream os;
     const int kk = resolve_k(k);
     if (path_ == Path::Fused)
-      os << "acoustic_fused<f32,R=" << R_ << ",TY=" << kTY << ",TZ=" << kTZ << ",PF=" << kPF
+      os << "acoustic_fused<f32,R=" << R_ << ",TY=" << kTY << ",TZ=" << kTZ << ",PF=" << pf_for(R_, resolve_k(k))
          << "," << (fast_ ? "fma" : "exact") << "> k=" << kk << " cx=" << cx_len_
          << " bytes_per_point=" << (kk == 1 ? 16 : 20);
     else if (path_ == Path::Tiled)
@@ -486,7 +486,10 @@ class AcousticProp final : public stb_prop_s {
 
  private:
   enum class Path { Reference, Tiled, Fused };
-  static constexpr int kTY = 16, kTZ = 64, kPF = 3;
+  static constexpr int kTY = 16, kTZ = 64;
+  // TMA prefetch depth: R = 6 stages 40% larger planes; PF = 2 keeps two
+  // CTAs per SM resident (smem), PF = 3 elsewhere.
+  static constexpr int pf_for(int R, int K = 1) { return (R >= 6 || (R <= 2 && K > 1)) ? 2 : 3; }
 
   int slot(int64_t t) const { return (int)(((t % NB) + NB) % NB); }
 
@@ -529,7 +532,7 @@ class AcousticProp final : public stb_prop_s {
         path_ = Path::Tiled;
         return;
       }
-      max_k_ = (R_ == 4) ? 2 : 1;
+      max_k_ = (R_ == 4 || R_ == 2) ? 2 : 1;
       default_k_ = 1;
       if (const char* kd = std::getenv("STB_DEFAULT_K")) default_k_ = std::atoi(kd);
       if (const char* dc = std::getenv("STB_DIAG_CX")) diag_cx_ = std::atoi(dc);
@@ -541,7 +544,7 @@ class AcousticProp final : public stb_prop_s {
 
   template <int R, int K>
   void fused_maps(FusedMaps& m, int s_l0, int s_lm1) {
-    using Cf = FusedCfg<R, K, kTY, kTZ, kPF>;
+    using Cf = FusedCfg<R, K, kTY, kTZ, pf_for(R, K)>;
     m.l0 = make_map3d_f32(reinterpret_cast<const float*>(lvl_[s_l0].p), d_, Cf::WZ0, Cf::HY0, 1);
     m.lm1 = make_map3d_f32(reinterpret_cast<const float*>(lvl_[s_lm1].p), d_, Cf::WZ1, Cf::HY1, 1);
     if (inv_.p) {
@@ -593,15 +596,16 @@ class AcousticProp final : public stb_prop_s {
     a.guard_mask = gmask;
     const int nch = (x_hi - x_lo + cx - 1) / cx;
     if (fast_)
-      FusedLauncher<R, K, kTY, kTZ, kPF, true>::launch(st_, it->second, a, nch);
+      FusedLauncher<R, K, kTY, kTZ, pf_for(R, K), true>::launch(st_, it->second, a, nch);
     else
-      FusedLauncher<R, K, kTY, kTZ, kPF, false>::launch(st_, it->second, a, nch);
+      FusedLauncher<R, K, kTY, kTZ, pf_for(R, K), false>::launch(st_, it->second, a, nch);
   }
 
   void launch_fused(int64_t t, int kb, int* gflag, int gmask) {
     if constexpr (sizeof(T) == 4) {
       if (R_ == 4 && kb == 2) return launch_fused_rk<4, 2>(t, gflag, gmask);
       if (R_ == 4) return launch_fused_rk<4, 1>(t, gflag, gmask);
+      if (R_ == 2 && kb == 2) return launch_fused_rk<2, 2>(t, gflag, gmask);
       if (R_ == 2) return launch_fused_rk<2, 1>(t, gflag, gmask);
       if (R_ == 6) return launch_fused_rk<6, 1>(t, gflag, gmask);
       throw Error(STB_ERR_ARG, "no fused kernel for this space order");

@@ -225,7 +225,7 @@ __device__ __forceinline__ void update4(const float (&xq)[Q][4], const int cs, c
 }
 
 template <int R, int K, int TY, int TZ, int PF, bool FAST, bool GUARD>
-__global__ void __launch_bounds__(FusedCfg<R, K, TY, TZ, PF>::NT, (K == 1 ? 2 : 1))
+__global__ void __launch_bounds__(FusedCfg<R, K, TY, TZ, PF>::NT, (K == 1 || R <= 2 ? 2 : 1))
 acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ FusedArgs a) {
   using C = FusedCfg<R, K, TY, TZ, PF>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -318,7 +318,6 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
   const bool edge = (y0 - C::hy(1) < 0) || (y0 + TY + C::hy(1) > a.d.ny) ||
                     (z0 - C::hz(1) < 0) || (z0 + TZ + C::hz(1) > a.d.nz) ||
                     (x0 - (K - 1) * R < 0) || (x1 + (K - 1) * R > a.d.nx);
-  const bool has_src = a.src_list != nullptr;
   const int nxm1 = (int)a.d.nx - 1;
   const int64_t gbase = (int64_t)y * a.d.pitch + z;      // global offset within a plane
 
@@ -334,13 +333,26 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
   const int off1 = row * C::WZ1 + 4 * g;
   int bad = 0;
 
-  int cur[K + 1];
+  // Per-level cursors into this tile's source list, with the plane of the
+  // next entry cached in a register so planes without sources cost one
+  // compare (no load on the critical path).  Uniform across the CTA.
+  int cur[K + 1], next_x[K + 1];
   int e_end = 0;
-  if (a.src_list) {
+  const bool has_src = a.src_list != nullptr;
+#pragma unroll
+  for (int j = 0; j <= K; ++j) {
+    cur[j] = 0;
+    next_x[j] = 0x7fffffff;
+  }
+  if (has_src) {
     const int e_beg = __ldg(a.src_tile_ptr + tile);
     e_end = __ldg(a.src_tile_ptr + tile + 1);
+    const int first = e_beg < e_end ? __ldg(&a.src_list[e_beg].x) : 0x7fffffff;
 #pragma unroll
-    for (int j = 0; j <= K; ++j) cur[j] = e_beg;
+    for (int j = 0; j <= K; ++j) {
+      cur[j] = e_beg;
+      next_x[j] = first;
+    }
   }
 
   // guard (before injection, as the reference's NaN check sees the stencil
@@ -355,14 +367,13 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
         }
       }
     }
-    if (has_src && __ldg(a.src_plane + min(max(p, 0), nxm1)) > 0 && p >= 0 && p <= nxm1) {
+    if (next_x[j] <= p) {              // rare: this plane (or a skipped one) has entries
       int c = cur[j];
-      while (c < e_end && __ldg(&a.src_list[c].x) < p) ++c;
       while (c < e_end) {
         const int4 e = __ldg(&a.src_list[c]);
-        if (e.x != p) break;
+        if (e.x > p) break;
         const int zz = e.z - z;
-        if (active && e.y == y && zz >= 0 && zz < 4) {
+        if (e.x == p && active && e.y == y && zz >= 0 && zz < 4) {
           const float v = __ldg(a.series + (size_t)(a.t0 + j - 1) * a.n_src + e.w);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -371,6 +382,7 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
         ++c;
       }
       cur[j] = c;
+      next_x[j] = c < e_end ? __ldg(&a.src_list[c].x) : 0x7fffffff;
     }
   };
 
