@@ -10,6 +10,14 @@ A "step" is one time step (stencil + fused injection + receiver gather) over
 the whole grid.  GPts/s counts the computational grid incl. sponge, as
 stencil_tb's RunReport does (engine.py:445-447).
 
+Second workload (--workload cfg4, BASELINE.json configs[3]): pseudo-acoustic
+TTI (coupled p, q; repo-defined operator), so=8, fp32, the
+same 592^3 computational grid (512^3 + 2x40 sponge) at 10 m, layered vp
+1.5-4.0 km/s, per-layer epsilon in [0, 0.3] and delta in [0, 0.2] (capped at
+epsilon: pseudo-acoustic TTI is unstable where delta > epsilon), smooth
+seeded theta/phi in [-45, 45] degrees, one 15 Hz Ricker source, 512
+receivers on a line at 20 m depth, dt = 0.5 ms.
+
 Arms:
   default          this repo's CUDA path; inputs resident in HBM for `value`,
                    public API `run()` with host buffers for `e2e`.
@@ -37,6 +45,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GPts/s (grid-point updates/s), 512^3 acoustic so=8; % of HBM roofline"
+METRIC_TTI = "GPts/s (grid-point updates/s), 512^3 TTI so=8; % of HBM roofline"
+DT_TTI = 0.5e-3
 PHYS = 512
 BL = 40
 SHAPE = (PHYS + 2 * BL,) * 3
@@ -73,12 +83,69 @@ def cfg2_inputs(seed: int = 2):
     return v, src, rec
 
 
-def make_config(stb, v, src, rec, nt, k, arithmetic="exact"):
+def cfg4_inputs(seed: int = 4):
+    """Seeded synthetic stand-in for BASELINE configs[3] (TTI)."""
+    rng = np.random.default_rng(seed)
+    n = SHAPE[2]
+    nlay = 8
+    edges = np.sort(rng.choice(np.arange(1, n - 1), size=nlay - 1, replace=False))
+    lay = np.searchsorted(edges, np.arange(n), side="right")
+    vp_l = np.sort(rng.uniform(1500.0, 4000.0, nlay))
+    eps_l = rng.uniform(0.0, 0.3, nlay)
+    del_l = np.minimum(rng.uniform(0.0, 0.2, nlay), eps_l)
+    prof = lambda vals: np.broadcast_to(vals[lay][None, None, :], SHAPE)  # noqa: E731
+    # smooth angle fields: sums of seeded low-wavenumber separable cosines
+    x = np.arange(n, dtype=np.float64) / n
+    q = np.pi / 4.0
+
+    def smooth():
+        f = np.zeros(SHAPE)
+        for _ in range(3):
+            k = rng.uniform(0.5, 2.0, 3)
+            ph = rng.uniform(0, 2 * np.pi, 3)
+            f += (np.cos(2 * np.pi * k[0] * x + ph[0])[:, None, None]
+                  * np.cos(2 * np.pi * k[1] * x + ph[1])[None, :, None]
+                  * np.cos(2 * np.pi * k[2] * x + ph[2])[None, None, :])
+        f *= q / max(float(np.max(np.abs(f))), 1e-30)
+        return f
+
+    medium = {"vp": prof(vp_l), "epsilon": prof(eps_l), "delta": prof(del_l),
+              "theta": smooth(), "phi": smooth()}
+    src = rng.uniform(0.0, (PHYS - 1) * H, size=(1, 3))
+    xs = np.clip(np.arange(PHYS) * H + rng.uniform(0.0, 9.99, size=PHYS), 0, (PHYS - 1) * H)
+    rec = np.stack([xs, np.full(PHYS, 0.5 * (PHYS - 1) * H), np.full(PHYS, 20.0)], axis=1)
+    return medium, src, rec
+
+
+def make_config(stb, v, src, rec, nt, k, arithmetic="exact", workload="cfg2"):
     grid = stb.GridSpec(SHAPE, (H, H, H), (-BL * H,) * 3, boundary_layers=BL)
+    if workload == "cfg4":
+        return stb.RunConfig(physics="tti", grid=grid, space_order=SO, nt=nt, dt=DT_TTI,
+                             medium=v, sources=stb.SourceSpec(src, f0=15.0),
+                             receiver_coords=rec, schedule=stb.ScheduleSpec("gpu", time_height=1))
     return stb.RunConfig(physics="acoustic", grid=grid, space_order=SO, nt=nt, dt=DT,
                          medium={"velocity": v}, sources=stb.SourceSpec(src, f0=15.0),
                          receiver_coords=rec,
                          schedule=stb.ScheduleSpec("gpu", time_height=k, arithmetic=arithmetic))
+
+
+def workload_inputs(workload):
+    return cfg4_inputs() if workload == "cfg4" else cfg2_inputs()
+
+
+def medium_nbytes(v):
+    if isinstance(v, dict):
+        return sum(np.asarray(a).nbytes if np.ndim(a) else 8 for a in v.values())
+    return v.nbytes
+
+
+WORKLOAD_TEXT = {
+    "cfg2": "cfg2 (BASELINE configs[1]): 512^3 + 2x40 sponge = 592^3 computational grid, "
+            "acoustic so=8, 1 Ricker 15 Hz, 512x512 receivers, dt=0.8 ms",
+    "cfg4": "cfg4 (BASELINE configs[3]): 512^3 + 2x40 sponge = 592^3 computational grid, "
+            "TTI so=8 (p, q), layered vp/eps/delta, smooth theta/phi, 1 Ricker 15 Hz, "
+            "512 receivers on a line, dt=0.5 ms",
+}
 
 
 class ClockSampler:
@@ -152,16 +219,18 @@ def dist_setup(n_gpus: int):
     return rank, world, local
 
 
-def cpu_baseline(steps: int, threads: int):
+def cpu_baseline(steps: int, threads: int, workload: str = "cfg2"):
     """Oracle port (NumPy, reference IEEE order) on the host cores: a bounded
-    sample of the same cfg2 workload."""
+    sample of the same workload."""
     from types import SimpleNamespace
     from oracle import stencil_oracle as so
-    v, src, rec = cfg2_inputs()
+    v, src, rec = workload_inputs(workload)
     grid = SimpleNamespace(shape=SHAPE, spacing=(H,) * 3, origin=(-BL * H,) * 3,
                            boundary_layers=BL)
-    cfg = SimpleNamespace(physics="acoustic", grid=grid, space_order=SO, medium={"velocity": v},
-                          nt=steps, time_ms=None, dt=DT, cfl_safety=0.9,
+    tti = workload == "cfg4"
+    cfg = SimpleNamespace(physics="tti" if tti else "acoustic", grid=grid, space_order=SO,
+                          medium=v if tti else {"velocity": v},
+                          nt=steps, time_ms=None, dt=DT_TTI if tti else DT, cfl_safety=0.9,
                           sources=SimpleNamespace(coords=src, f0=15.0, t0=None, amplitude=1.0,
                                                   wavelets=None),
                           receiver_coords=rec, precision=32, damping_decay=None)
@@ -180,16 +249,18 @@ def run_reference_arm(args):
     # 592^3 grid; warmup steps are run and discarded inside one oracle run
     total = args.warmup + args.steps
     from types import SimpleNamespace  # noqa: F401
-    gps, elapsed, steps = cpu_baseline(total, threads)
+    gps, elapsed, steps = cpu_baseline(total, threads, args.workload)
+    tti = args.workload == "cfg4"
     line = {
-        "impl": "reference", "metric": METRIC, "value": gps, "unit": "GPts/s",
+        "impl": "reference", "metric": METRIC_TTI if tti else METRIC, "value": gps,
+        "unit": "GPts/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * elapsed / max(steps, 1), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "cfg2 (BASELINE configs[1]) 592^3 incl. sponge, acoustic so=8",
-                   "grid": list(SHAPE)},
+        "config": {"workload": WORKLOAD_TEXT[args.workload], "grid": list(SHAPE)},
         "cpu_baseline": {"value": gps, "unit": "GPts/s", "cores": threads, "kind": "port",
-                         "sample": f"{steps} time steps of cfg2 (592^3) through the oracle "
+                         "sample": f"{steps} time steps of {args.workload} (592^3) through "
+                                   f"the oracle "
                                    f"port (NumPy, {threads} threads, x-chunked; warmup "
                                    f"included: the port has no warm-up effect)"},
         "e2e": {"value": gps, "unit": "GPts/s", "h2d_bytes_per_step": 0,
@@ -210,6 +281,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg4"],
+                    help="cfg2: acoustic headline (default); cfg4: TTI")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
@@ -225,9 +298,10 @@ def main():
     rank, world, local = dist_setup(args.gpus)
     torch.cuda.set_device(local)
     stb._lib.check(stb._lib.lib().stb_set_device(local))
-    v, src, rec = cfg2_inputs()
+    wl = args.workload
+    v, src, rec = workload_inputs(wl)
     nt_series = args.warmup + args.steps
-    cfg = make_config(stb, v, src, rec, nt_series, args.k, args.arithmetic)
+    cfg = make_config(stb, v, src, rec, nt_series, args.k, args.arithmetic, wl)
     npts = int(np.prod(SHAPE))
 
     # ------------------------------------------------------------ value
@@ -285,13 +359,13 @@ def main():
     # ------------------------------------------------------------ e2e
     e2e = None
     if not args.no_e2e and world == 1:
-        cfg_e = make_config(stb, v, src, rec, args.steps, args.k, args.arithmetic)
+        cfg_e = make_config(stb, v, src, rec, args.steps, args.k, args.arithmetic, wl)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = stb.run(cfg_e)
         e2e_s = time.perf_counter() - t0
-        h2d = v.nbytes + src.nbytes + rec.nbytes + 8 * sum(SHAPE) + 8 * args.steps
-        d2h = res.fields["u"].nbytes + res.receivers.nbytes
+        h2d = medium_nbytes(v) + src.nbytes + rec.nbytes + 8 * sum(SHAPE) + 8 * args.steps
+        d2h = sum(f.nbytes for f in res.fields.values()) + res.receivers.nbytes
         e2e = {"value": npts * args.steps / e2e_s / 1e9, "unit": "GPts/s",
                "h2d_bytes_per_step": int(h2d / args.steps),
                "d2h_bytes_per_step": int(d2h / args.steps),
@@ -300,7 +374,7 @@ def main():
         del res
     elif not args.no_e2e and world > 1:
         # public multi-GPU entry: x-slab run + gather of field and traces on rank 0
-        cfg_e = make_config(stb, v, src, rec, args.steps, args.k, args.arithmetic)
+        cfg_e = make_config(stb, v, src, rec, args.steps, args.k, args.arithmetic, wl)
         torch.cuda.synchronize()
         dist.barrier()
         t0 = time.perf_counter()
@@ -309,8 +383,8 @@ def main():
         wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         dist.all_reduce(wall, op=dist.ReduceOp.MAX)
         e2e_s = float(wall.item())
-        h2d = v.nbytes + src.nbytes + rec.nbytes + 8 * sum(SHAPE) + 8 * args.steps
-        d2h = 4 * npts + 8 * args.steps * len(rec)
+        h2d = medium_nbytes(v) + src.nbytes + rec.nbytes + 8 * sum(SHAPE) + 8 * args.steps
+        d2h = 4 * npts * len(fields or {"u": 0}) + 8 * args.steps * len(rec)
         e2e = {"value": npts * args.steps / e2e_s / 1e9, "unit": "GPts/s",
                "h2d_bytes_per_step": int(h2d / args.steps),
                "d2h_bytes_per_step": int(d2h / args.steps), "wall_s": e2e_s,
@@ -322,20 +396,18 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        gps, el, n = cpu_baseline(args.cpu_steps, threads)
+        gps, el, n = cpu_baseline(args.cpu_steps, threads, wl)
         cpu = {"value": gps, "unit": "GPts/s", "cores": threads, "kind": "port",
-               "sample": f"{n} time steps of cfg2 (592^3) through the oracle port "
+               "sample": f"{n} time steps of {wl} (592^3) through the oracle port "
                          f"(NumPy, {threads} threads), stepping only ({el:.1f} s)"}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "GPts/s", "n_gpus": world,
+            "metric": METRIC_TTI if wl == "cfg4" else METRIC, "value": value, "unit": "GPts/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "cfg2 (BASELINE configs[1]): 512^3 + 2x40 sponge = 592^3 "
-                                   "computational grid, acoustic so=8, 1 Ricker 15 Hz, "
-                                   "512x512 receivers, dt=0.8 ms",
+            "config": {"workload": WORKLOAD_TEXT[wl],
                        "grid": list(SHAPE), "time_height": k_used,
                        "arithmetic": args.arithmetic,
                        "parallelism": f"x-slab{world}",

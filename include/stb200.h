@@ -167,8 +167,38 @@ typedef struct {
   int64_t nx_local;
 } stb_elastic_desc;
 
+/* Pseudo-acoustic TTI, coupled p and q (eq. 2).  Not in
+ * the reference: the discrete operator is this repo's, defined
+ * by oracle/stencil_oracle.py:TTI (parity unpinned).  All material values are
+ * formed in f64 by the host and rounded once on the device:
+ *   inv = dt2 / (1/vp^2), e2 = 1 + 2 eps, d2 = sqrt(1 + 2 delta),
+ *   axis = (sin t cos f, sin t sin f, cos t).
+ * Fields: 0 = p, 1 = q.  Receivers record p; sources inject into p and q. */
+typedef struct {
+  stb_geometry geom;
+  int32_t space_order;       /* multiple of 4 in [4, 16]                     */
+  int32_t precision;         /* 32 or 64                                     */
+  double dt;
+  double d1[3][4];           /* centred first-derivative weights a_k / h_a,
+                                k = 1..so/4 (order so/2); 0 on inactive axes */
+  int32_t active[3];
+  double dt2;
+  const double* velocity;    /* vp per point (compact slab, f64) or NULL     */
+  double inv_scalar;         /* dt2/m of a homogeneous medium                */
+  const double* e2;          /* 1 + 2 epsilon per point, or NULL -> scalar   */
+  double e2_scalar;
+  const double* d2;          /* sqrt(1 + 2 delta) per point, or NULL         */
+  double d2_scalar;
+  const double* axis[3];     /* symmetry-axis components per point, or NULL  */
+  double axis_scalar[3];
+  const double* damp[3];     /* per-axis sponge tables, as acoustic          */
+  int64_t x_begin;           /* x slab, as in stb_acoustic_desc              */
+  int64_t nx_local;
+} stb_tti_desc;
+
 int stb_acoustic_create(const stb_acoustic_desc* d, stb_prop_t* out);
 int stb_elastic_create(const stb_elastic_desc* d, stb_prop_t* out);
+int stb_tti_create(const stb_tti_desc* d, stb_prop_t* out);
 
 /* Sources: fused injection of the decomposed series (Alg. 4/5,
  * precompute.py:209-252).  Decomposition runs on the device from the
@@ -187,7 +217,7 @@ int stb_prop_set_receivers(stb_prop_t p, const double* coords, int64_t nrec);
 int stb_prop_run(stb_prop_t p, int64_t t0, int64_t nsteps, int32_t time_height,
                  double* rec_out, int64_t* bad_step);
 /* Field `field` (acoustic: 0 = u; elastic: 0..8 = vx vy vz txx tyy tzz txy
- * txz tyz) at time level t (the last two written levels are resident),
+ * txz tyz; tti: 0 = p, 1 = q) at time level t (the last two written levels are resident),
  * copied to a host (nx, ny, nz) array of the handle's dtype. */
 int stb_prop_read_field(stb_prop_t p, int32_t field, int64_t t, void* out);
 /* Device address of time level t of field `field` (x-slab halo exchange):

@@ -97,10 +97,25 @@ def active_axes(shape):
     return tuple(a for a in range(3) if shape[a] > 1)
 
 
+def tti_first_weights(so: int) -> np.ndarray:
+    """Centred first-derivative weights a_1..a_r, r = so/4 (accuracy order
+    so/2, so two applications span the acoustic footprint R = so/2):
+    sum_k a_k * 2 k^(2m+1) = [m == 0], m = 0..r-1.  Repo-defined (TTI is
+    absent from the reference)."""
+    r = so // 4
+    rows = [[Fraction(2 * k ** (2 * m + 1)) for k in range(1, r + 1)] for m in range(r)]
+    rhs = [Fraction(1 if m == 0 else 0) for m in range(r)]
+    return np.array([float(a) for a in _gauss_jordan(rows, rhs)])
+
+
 def stable_dt(physics, shape, spacing, v_max, so, safety=0.9):
-    """engine.py:172-195."""
+    """engine.py:172-195 (TTI: repo-defined bound, see tti_stable_dt)."""
     axes = active_axes(shape) or (0,)
-    if physics in ("acoustic", "tti"):
+    if physics == "tti":
+        a = tti_first_weights(so)
+        lam = sum((2.0 * float(np.sum(np.abs(a)))) ** 2 / spacing[ax] ** 2 for ax in axes)
+        return safety * 2.0 / (v_max * math.sqrt(lam))
+    if physics == "acoustic":
         w = fd_weights(so)
         signs = np.cos(np.pi * np.arange(len(w)))
         g_max = -(w[0] + 2.0 * float(np.sum(w[1:] * signs[1:])))
@@ -505,6 +520,197 @@ class Elastic:
         return [self.lv(n, t) for n in self.V + self.T]
 
 
+def tti_axis(theta, phi):
+    """Unit symmetry axis z-bar = (sin t cos p, sin t sin p, cos t) of the
+    rotated frame of PAPER.md eq. 2 (x-bar = (cos t cos p, cos t sin p,
+    -sin t)), evaluated in f64."""
+    th = np.asarray(theta, np.float64)
+    ph = np.asarray(phi, np.float64)
+    return (np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th))
+
+
+class TTI:
+    """Pseudo-acoustic TTI (coupled p, q) -- this repo's own oracle; the
+    reference has no TTI, so parity is UNPINNED.  Operator:
+    PAPER.md:429-435 (eq. 2, G_aa = D_a^T D_a with rotated first
+    derivatives) in the Zhang-Zhang-Zhang (2011) form
+
+        m p_tt = (1+2 eps) H0 p + sqrt(1+2 delta) Hz q
+        m q_tt = sqrt(1+2 delta) H0 p + Hz q,
+        Hz u = D.(n (n.D u)),  H0 u = D.(D u - n (n.D u))   (= G_xx + G_yy)
+
+    with n the symmetry axis (tti_axis) and D the centred first derivative of
+    order so/2 (tti_first_weights; zero outside the grid, so D^T = -D).
+    Per step and point, in this exact IEEE order (f32 fields; material and
+    weights rounded once to the field dtype):
+
+      pass 1  g_a = sum_k (u[+k] - u[-k]) * c_ak          (k ascending)
+              w   = sum_{a active} g_a(p) * n_a           (axis order)
+              F_a = g_a(p) - w * n_a ;  G_a = (sum_a g_a(q) * n_a) * n_a
+      pass 2  Lxy = sum_a D_a F_a ;  Lzz = sum_a D_a G_a
+              p'  = (((p*2) - p_prev) + ((Lxy*e2) + (Lzz*d2)) * inv) * fac
+              q'  = (((q*2) - q_prev) + ((Lxy*d2) + Lzz) * inv) * fac
+
+    e2 = 1 + 2 eps, d2 = sqrt(1 + 2 delta), inv = dt^2/m, m = 1/vp^2 (f64,
+    then rounded).  Fields carry a zero halo of r = so/4 points; F and G too.
+    """
+
+    def __init__(self, shape, spacing, so, m, e2, d2, axis, dt, damp, dtype):
+        if so % 4 != 0:
+            raise ValueError("TTI needs space_order divisible by 4")
+        self.shape, self.so = tuple(shape), so
+        self.R = H = so // 4
+        self.dtype = np.dtype(dtype)
+        pshape = (3,) + tuple(n + 2 * H for n in shape)
+        self.p = np.zeros(pshape, dtype=self.dtype)
+        self.q = np.zeros(pshape, dtype=self.dtype)
+        tshape = tuple(n + 2 * H for n in shape)
+        self.F = [np.zeros(tshape, dtype=self.dtype) for _ in range(3)]
+        self.G = [np.zeros(tshape, dtype=self.dtype) for _ in range(3)]
+        self.inv = (dt ** 2 / float(m) if np.ndim(m) == 0
+                    else pad_material(dt ** 2 / np.asarray(m, np.float64), H, self.dtype))
+        self.e2 = pad_material(e2, H, self.dtype)
+        self.d2 = pad_material(d2, H, self.dtype)
+        self.n = [pad_material(c, H, self.dtype) for c in axis]
+        self.fac = damp_factor_padded(damp, H, dt, self.dtype)
+        a = tti_first_weights(so)
+        self.act = active_axes(shape)
+        self.w = {ax: [float(ak / spacing[ax]) for ak in a] for ax in self.act}
+
+    def lv(self, name, t):
+        return (self.p if name == "p" else self.q)[t % 3]
+
+    @staticmethod
+    def _s(v, sl):
+        return v[sl] if isinstance(v, np.ndarray) else v
+
+    def _d1(self, arr, box, axis):
+        H = self.R
+        acc = None
+        for k, c in enumerate(self.w[axis], start=1):
+            term = arr[_sl(box, H, axis, k)] - arr[_sl(box, H, axis, -k)]
+            term *= c
+            if acc is None:
+                acc = term
+            else:
+                acc += term
+        return acc
+
+    def _pass1(self, t, box):
+        sl = _sl(box, self.R)
+        p, q = self.lv("p", t - 1), self.lv("q", t - 1)
+        gp = {a: self._d1(p, box, a) for a in self.act}
+        gq = {a: self._d1(q, box, a) for a in self.act}
+        wp = wq = None
+        for a in self.act:
+            na = self._s(self.n[a], sl)
+            tp = gp[a] * na
+            tq = gq[a] * na
+            if wp is None:
+                wp, wq = tp, tq
+            else:
+                wp += tp
+                wq += tq
+        for a in self.act:
+            na = self._s(self.n[a], sl)
+            self.F[a][sl] = gp[a] - wp * na
+            self.G[a][sl] = wq * na
+
+    def _pass2(self, t, box):
+        sl = _sl(box, self.R)
+        lxy = lzz = None
+        for a in self.act:
+            fa = self._d1(self.F[a], box, a)
+            ga = self._d1(self.G[a], box, a)
+            if lxy is None:
+                lxy, lzz = fa, ga
+            else:
+                lxy += fa
+                lzz += ga
+        inv, e2, d2 = self._s(self.inv, sl), self._s(self.e2, sl), self._s(self.d2, sl)
+        for name in ("p", "q"):
+            cur, prev = self.lv(name, t - 1)[sl], self.lv(name, t - 2)[sl]
+            out = cur * 2.0
+            out -= prev
+            if lxy is not None:
+                if name == "p":
+                    inc = lxy * e2
+                    inc += lzz * d2
+                else:
+                    inc = lxy * d2
+                    inc += lzz
+                inc *= inv
+                out += inc
+            if self.fac is not None:
+                out *= self.fac[sl]
+            self.lv(name, t)[sl] = out
+
+    def step(self, t, pool=None, threads=1):
+        nx, ny, nz = self.shape
+        boxes = [((a, b), (0, ny), (0, nz)) for a, b in _xchunks(nx, threads)]
+        for fn in (self._pass1, self._pass2):
+            if pool is None or len(boxes) == 1:
+                for b in boxes:
+                    fn(t, b)
+            else:
+                list(pool.map(lambda b: fn(t, b), boxes))
+
+    def fields(self, t):
+        H = self.R
+        return {n: self.lv(n, t)[H:-H, H:-H, H:-H].copy() for n in ("p", "q")}
+
+    def all_levels(self, t):
+        return [self.lv("p", t), self.lv("q", t)]
+
+    def operator_h0(self, u):
+        """H0 u = D.(D u - n (n.D u)) on an unpadded f64 field (tests:
+        symmetry / definiteness of the discrete operator)."""
+        return self._apply_op(u, horizontal=True)
+
+    def operator_hz(self, u):
+        return self._apply_op(u, horizontal=False)
+
+    def _apply_op(self, u, horizontal):
+        H = self.R
+        box = tuple((0, n) for n in self.shape)
+        sl = _sl(box, H)
+        pad = np.zeros(tuple(n + 2 * H for n in self.shape), dtype=u.dtype)
+        pad[sl] = u
+        g = {a: self._d1(pad, box, a) for a in self.act}
+        w = sum(g[a] * self._s(self.n[a], sl) for a in self.act)
+        out = np.zeros(self.shape, dtype=u.dtype)
+        for a in self.act:
+            f = np.zeros_like(pad)
+            na = self._s(self.n[a], sl)
+            f[sl] = g[a] - w * na if horizontal else w * na
+            out += self._d1(f, box, a)
+        return out
+
+
+def tti_medium(medium):
+    """(m, e2, d2, axis) in f64 from a TTI medium dict (vp, epsilon, delta,
+    theta, phi; angles in radians; omitted -> 0)."""
+    vp = medium["vp"]
+    m = (1.0 / np.asarray(vp, np.float64) ** 2 if np.ndim(vp) else 1.0 / float(vp) ** 2)
+    eps = medium.get("epsilon", 0.0)
+    delta = medium.get("delta", 0.0)
+    e2 = 1.0 + 2.0 * np.asarray(eps, np.float64) if np.ndim(eps) else 1.0 + 2.0 * float(eps)
+    d2 = (np.sqrt(1.0 + 2.0 * np.asarray(delta, np.float64)) if np.ndim(delta)
+          else math.sqrt(1.0 + 2.0 * float(delta)))
+    th, ph = medium.get("theta", 0.0), medium.get("phi", 0.0)
+    axis = tti_axis(th, ph)
+    if np.ndim(th) == 0 and np.ndim(ph) == 0:
+        axis = tuple(float(c) for c in axis)
+    return m, e2, d2, axis
+
+
+def tti_vmax(medium):
+    """Fastest phase velocity bound vp * sqrt(1 + 2 eps) (dt default)."""
+    vp = np.asarray(medium["vp"], np.float64)
+    eps = np.asarray(medium.get("epsilon", 0.0), np.float64)
+    return float(np.max(vp * np.sqrt(1.0 + 2.0 * np.maximum(eps, 0.0))))
+
+
 # --------------------------------------------------------------------------
 # Forward run (engine.py:379-489, naive schedule semantics; injection via the
 # decomposed series, which is bitwise equal to direct injection -- SPEC
@@ -540,6 +746,8 @@ def resolve(cfg):
     phys = cfg.physics
     if phys == "elastic":
         v_max = float(np.max(cfg.medium["vp"]))
+    elif phys == "tti":
+        v_max = tti_vmax(cfg.medium)
     else:
         v_max = float(np.max(cfg.medium["velocity"]))
     g = cfg.grid
@@ -582,9 +790,14 @@ def run(cfg, threads: int = 1, steps: int | None = None, keep_support=False) -> 
         model = Elastic(shape, spacing, so, lam, mu, rho, dt, damp, dtype)
         inject_into = lambda t: [model.lv(n, t) for n in ("txx", "tyy", "tzz")]
         gather_from = lambda t: model.lv("txx", t)
+    elif cfg.physics == "tti":
+        m, e2, d2, axis = tti_medium(cfg.medium)
+        model = TTI(shape, spacing, so, m, e2, d2, axis, dt, damp, dtype)
+        inject_into = lambda t: [model.lv("p", t), model.lv("q", t)]
+        gather_from = lambda t: model.lv("p", t)
     else:
         raise ValueError(f"oracle has no physics {cfg.physics!r}")
-    R = so // 2
+    R = model.R
 
     # sources (engine.py:258-279)
     sup = dcmp = None
@@ -599,7 +812,7 @@ def run(cfg, threads: int = 1, steps: int | None = None, keep_support=False) -> 
         else:
             t0 = spec.t0 if spec.t0 is not None else 1.0 / spec.f0
             wav = np.repeat(ricker(spec.f0, t0, dt, nt, spec.amplitude)[:, None], nsrc, axis=1)
-        if cfg.physics == "acoustic":
+        if cfg.physics in ("acoustic", "tti"):
             scale = nearest_scales(spec.coords, shape, spacing, origin, m, dt)
         else:
             scale = np.full(nsrc, dt)

@@ -28,7 +28,7 @@ EXPORTS = (
     "stb_interp_stencils", "stb_support_create", "stb_support_from_points", "stb_support_info", "stb_support_points",
     "stb_support_compress", "stb_support_masks", "stb_support_entries",
     "stb_support_decompose", "stb_support_destroy", "stb_acoustic_create",
-    "stb_elastic_create", "stb_prop_set_sources", "stb_prop_set_receivers", "stb_prop_run",
+    "stb_elastic_create", "stb_tti_create", "stb_prop_set_sources", "stb_prop_set_receivers", "stb_prop_run",
     "stb_prop_read_field", "stb_prop_level_ptr", "stb_prop_reset", "stb_prop_stats",
     "stb_prop_describe",
     "stb_prop_destroy",
@@ -59,6 +59,17 @@ class ElasticDesc(C.Structure):
                 ("nx_local", C.c_int64)]
 
 
+class TTIDesc(C.Structure):
+    _fields_ = [("geom", Geometry), ("space_order", C.c_int32), ("precision", C.c_int32),
+                ("dt", C.c_double), ("d1", (C.c_double * 4) * 3), ("active", C.c_int32 * 3),
+                ("dt2", C.c_double), ("velocity", C.POINTER(C.c_double)),
+                ("inv_scalar", C.c_double), ("e2", C.POINTER(C.c_double)),
+                ("e2_scalar", C.c_double), ("d2", C.POINTER(C.c_double)),
+                ("d2_scalar", C.c_double), ("axis", C.POINTER(C.c_double) * 3),
+                ("axis_scalar", C.c_double * 3), ("damp", C.POINTER(C.c_double) * 3),
+                ("x_begin", C.c_int64), ("nx_local", C.c_int64)]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -84,6 +95,7 @@ def _declare(lib):
         "stb_support_destroy": ([P], C.c_int),
         "stb_acoustic_create": ([C.POINTER(AcousticDesc), C.POINTER(P)], C.c_int),
         "stb_elastic_create": ([C.POINTER(ElasticDesc), C.POINTER(P)], C.c_int),
+        "stb_tti_create": ([C.POINTER(TTIDesc), C.POINTER(P)], C.c_int),
         "stb_prop_set_sources": ([P, P, pdbl, i64, pdbl, i64], C.c_int),
         "stb_prop_set_receivers": ([P, pdbl, i64], C.c_int),
         "stb_prop_run": ([P, i64, i64, i32, pdbl, pi64], C.c_int),

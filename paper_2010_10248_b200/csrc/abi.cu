@@ -205,6 +205,17 @@ STB_API int stb_elastic_create(const stb_elastic_desc* d, stb_prop_t* out) {
   })
 }
 
+STB_API int stb_tti_create(const stb_tti_desc* d, stb_prop_t* out) {
+  STB_GUARD({
+    STB_REQUIRE(d != nullptr && out != nullptr, STB_ERR_ARG, "NULL argument");
+    check_geometry(&d->geom);
+    check_order(d->space_order);
+    check_precision(d->precision);
+    require_device();
+    *out = make_tti(*d);
+  })
+}
+
 STB_API int stb_prop_set_sources(stb_prop_t p, stb_support_t s, const double* wavelets,
                                  int64_t nt_w, const double* scale, int64_t nt) {
   STB_GUARD({

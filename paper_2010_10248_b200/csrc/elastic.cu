@@ -23,6 +23,7 @@
 #include <sstream>
 
 #include "fp_exact.cuh"
+#include "padded.cuh"
 #include "sparse_ops.cuh"
 #include "stb_internal.cuh"
 
@@ -33,31 +34,6 @@ namespace {
 inline unsigned g1(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
 
 enum { VX, VY, VZ, TXX, TYY, TZZ, TXY, TXZ, TYZ, NFIELDS };
-
-// Zero-haloed layout.
-struct PDims {
-  int64_t nx, ny, nz;     // interior
-  int64_t H;              // halo width (>= R)
-  int64_t zoff;           // interior z offset within a row (128-byte aligned)
-  int64_t pitch;          // row length (elements)
-  int64_t plane;          // (ny + 2H) * pitch
-  int64_t total;          // (nx + 2H) * plane
-  __host__ __device__ int64_t at(int64_t x, int64_t y, int64_t z) const {
-    return ((x + H) * (ny + 2 * H) + (y + H)) * pitch + zoff + z;
-  }
-};
-
-PDims make_pdims(int64_t nx, int64_t ny, int64_t nz, int R, size_t elem) {
-  PDims p;
-  p.nx = nx; p.ny = ny; p.nz = nz;
-  p.H = R;
-  const int64_t per128 = 128 / (int64_t)elem;
-  p.zoff = round_up(R, per128);
-  p.pitch = round_up(p.zoff + nz + R, per128);
-  p.plane = (ny + 2 * p.H) * p.pitch;
-  p.total = (nx + 2 * p.H) * p.plane;
-  return p;
-}
 
 template <typename T>
 struct ElCoefs {
@@ -467,54 +443,6 @@ __global__ void elastic_materials_kernel(const double* __restrict__ lam,
   }
 }
 
-template <typename T>
-__global__ void table_kernel_el(const double* __restrict__ src, int64_t n, T* __restrict__ dst) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = src ? from_f64<T>(src[i]) : T(1);
-}
-
-template <typename T>
-__global__ void to_dtype_kernel_el(const double* __restrict__ src, int64_t n, T* __restrict__ dst) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = from_f64<T>(src[i]);
-}
-
-__global__ void keys_to_offsets_el(const int64_t* __restrict__ keys, int64_t n, int64_t gny,
-                                   int64_t gnz, int64_t x_begin, PDims d,
-                                   int64_t* __restrict__ off) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t k = keys[i];
-  const int64_t z = k % gnz, xy = k / gnz;
-  off[i] = d.at(xy / gny - x_begin, xy % gny, z);
-}
-
-__global__ void idx_to_offsets_el(const int64_t* __restrict__ idx, int64_t n8, int64_t x_begin,
-                                  PDims d, int64_t* __restrict__ off, int* bad) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n8) return;
-  const int64_t x = idx[i * 3] - x_begin;
-  if (x < 0 || x >= d.nx) {
-    atomicExch(bad, 1);
-    off[i] = 0;
-    return;
-  }
-  off[i] = d.at(x, idx[i * 3 + 1], idx[i * 3 + 2]);
-}
-
-template <typename T>
-__global__ void unpad_nonfinite_kernel(const T* __restrict__ u, PDims d, int* flag) {
-  const int64_t n = d.nx * d.ny * d.nz;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t z = i % d.nz, xy = i / d.nz;
-    if (!finite(u[d.at(xy / d.ny, xy % d.ny, z)])) {
-      atomicExch(flag, 1);
-      return;
-    }
-  }
-}
-
 template <typename T, int R>
 void launch_sweeps(cudaStream_t st, const ElArgs<T>& a) {
   if (a.cx <= 0) {
@@ -592,7 +520,7 @@ class ElasticProp final : public stb_prop_s {
       fac_[a].alloc(n3[a]);
       DevBuf<double> tmp(desc.damp[a] ? n3[a] : 0);
       if (desc.damp[a]) tmp.upload(desc.damp[a] + (a == 0 ? x_begin_ : 0), n3[a], st_);
-      table_kernel_el<T><<<g1(n3[a]), 256, 0, st_>>>(desc.damp[a] ? tmp.p : nullptr, n3[a],
+      pad_table_kernel<T><<<g1(n3[a]), 256, 0, st_>>>(desc.damp[a] ? tmp.p : nullptr, n3[a],
                                                      fac_[a].p);
       STB_CHECK_LAUNCH();
       STB_CUDA(cudaStreamSynchronize(st_));
@@ -633,9 +561,9 @@ class ElasticProp final : public stb_prop_s {
     STB_CUDA(cudaMemcpy2DAsync(dl.p, K_ * sizeof(double), dc.p + lohi[0], s.K * sizeof(double),
                                K_ * sizeof(double), nt, cudaMemcpyDeviceToDevice, st_));
     series_.alloc(nt * K_);
-    to_dtype_kernel_el<T><<<g1(nt * K_), 256, 0, st_>>>(dl.p, nt * K_, series_.p);
+    pad_to_dtype_kernel<T><<<g1(nt * K_), 256, 0, st_>>>(dl.p, nt * K_, series_.p);
     src_off_.alloc(K_);
-    keys_to_offsets_el<<<g1(K_), 256, 0, st_>>>(s.keys.p + lohi[0], K_, geom_.shape[1],
+    pad_keys_to_offsets<<<g1(K_), 256, 0, st_>>>(s.keys.p + lohi[0], K_, geom_.shape[1],
                                                 geom_.shape[2], x_begin_, d_, src_off_.p);
     STB_CHECK_LAUNCH();
     STB_CUDA(cudaStreamSynchronize(st_));
@@ -652,7 +580,7 @@ class ElasticProp final : public stb_prop_s {
     rec_off_.alloc(nrec * 8);
     DevBuf<int> bad(1);
     bad.zero(st_);
-    idx_to_offsets_el<<<g1(nrec * 8), 256, 0, st_>>>(idx.p, nrec * 8, x_begin_, d_, rec_off_.p,
+    pad_idx_to_offsets<<<g1(nrec * 8), 256, 0, st_>>>(idx.p, nrec * 8, x_begin_, d_, rec_off_.p,
                                                      bad.p);
     STB_CHECK_LAUNCH();
     int hb = 0;

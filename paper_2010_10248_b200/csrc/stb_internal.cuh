@@ -189,3 +189,4 @@ struct stb_support_s {
 
 stb_prop_s* make_acoustic(const stb_acoustic_desc& d);
 stb_prop_s* make_elastic(const stb_elastic_desc& d);
+stb_prop_s* make_tti(const stb_tti_desc& d);

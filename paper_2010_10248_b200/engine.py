@@ -27,8 +27,9 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError, InvalidPlanError
-from .grid import GridSpec, fd_weights, staggered_fd_weights
-from .physics import acoustic_coefficients, damping_tables, elastic_coefficients, ricker
+from .grid import GridSpec, centered_first_weights, fd_weights, staggered_fd_weights
+from .physics import (acoustic_coefficients, damping_tables, elastic_coefficients, ricker,
+                      tti_coefficients, tti_medium)
 from .precompute import _Handle
 from .sparse import nearest_scales_from_velocity, validate_coords_in_extent
 
@@ -38,6 +39,7 @@ SNAPSHOT_HEADER = struct.Struct("<8sIiiiI")
 SNAPSHOT_HEADER_SIZE = 32
 
 SCHEDULE_KINDS = ("naive", "space", "wavefront", "gpu")
+PHYSICS = ("acoustic", "elastic", "tti")
 
 
 @dataclass
@@ -94,10 +96,14 @@ class RunConfig:
     validate: bool = False
 
     def __post_init__(self):
-        if self.physics not in ("acoustic", "elastic"):
-            raise ConfigError("physics", f"must be acoustic or elastic, got {self.physics!r}")
+        if self.physics not in PHYSICS:
+            raise ConfigError("physics", f"must be acoustic, elastic or tti, got {self.physics!r}")
         if self.space_order % 2 != 0 or not 2 <= self.space_order <= 16:
             raise ConfigError("space_order", f"must be even in [2, 16], got {self.space_order}")
+        if self.physics == "tti" and self.space_order % 4 != 0:
+            raise ConfigError("space_order",
+                              f"tti needs a multiple of 4 (first derivatives of order so/2), "
+                              f"got {self.space_order}")
         if self.precision not in (32, 64):
             raise ConfigError("precision", f"must be 32 or 64, got {self.precision}")
         if self.threads < 1:
@@ -191,6 +197,14 @@ def medium_velocity_bounds(physics: str, medium: dict) -> float:
         if "velocity" not in medium:
             raise ConfigError("medium.velocity", "acoustic runs need a velocity")
         return float(np.max(medium["velocity"]))
+    if physics == "tti":
+        # fastest phase velocity, vp * sqrt(1 + 2 eps) (TTI is repo-defined)
+        if "vp" not in medium:
+            raise ConfigError("medium.vp", "tti runs need vp (and optionally epsilon, "
+                              "delta, theta, phi)")
+        vp = np.asarray(medium["vp"], np.float64)
+        eps = np.asarray(medium.get("epsilon", 0.0), np.float64)
+        return float(np.max(vp * np.sqrt(1.0 + 2.0 * np.maximum(eps, 0.0))))
     for key in ("vp", "vs", "rho"):
         if key not in medium:
             raise ConfigError(f"medium.{key}", "elastic runs need vp, vs, rho")
@@ -203,6 +217,10 @@ def stable_dt(physics: str, grid: GridSpec, v_max: float, space_order: int,
     if v_max <= 0.0:
         raise ValueError(f"v_max must be > 0, got {v_max}")
     axes = grid.active_axes or (0,)
+    if physics == "tti":
+        a = centered_first_weights(space_order)
+        lam = sum((2.0 * float(np.sum(np.abs(a)))) ** 2 / grid.spacing[ax] ** 2 for ax in axes)
+        return safety * 2.0 / (v_max * math.sqrt(lam))
     if physics == "acoustic":
         w = fd_weights(space_order).weights
         alt = np.cos(np.pi * np.arange(len(w)))
@@ -238,6 +256,10 @@ def arithmetic_intensity(physics: str, space_order: int, precision: int) -> floa
     item = 4 if precision == 32 else 8
     if physics == "acoustic":
         return (3 * (3 * r + 1) + 8) / (5 * item)
+    if physics == "tti":
+        h = r // 2
+        flops = 9 * 2 * (3 * h - 1) + 18 + 12
+        return flops / (26 * item)
     return (18 * (3 * r - 1) + 45) / (22 * item)
 
 
@@ -261,7 +283,7 @@ def _gpu_time_height(config: RunConfig) -> int:
     if s.time_height < 1:
         raise InvalidPlanError(f"time_height must be >= 1, got {s.time_height}")
     r = config.space_order // 2
-    skew = (r, r) if config.physics == "acoustic" else (2 * r, 2 * r)
+    skew = (2 * r, 2 * r) if config.physics == "elastic" else (r, r)
     if s.force_skew is not None:
         forced = (int(s.force_skew[0]), int(s.force_skew[1]))
         if config.validate and any(
@@ -331,6 +353,8 @@ class _Prop:
 
 ACOUSTIC_FIELDS = ("u",)
 ELASTIC_FIELDS = ("vx", "vy", "vz", "txx", "tyy", "tzz", "txy", "txz", "tyz")
+TTI_FIELDS = ("p", "q")
+FIELDS = {"acoustic": ACOUSTIC_FIELDS, "elastic": ELASTIC_FIELDS, "tti": TTI_FIELDS}
 
 
 def _as_f64_grid(values, grid: GridSpec, what: str):
@@ -388,6 +412,8 @@ def build_propagator(config: RunConfig, dt: float, v_max: float, x_begin: int = 
         raw = C.c_void_p()
         _lib.check(_lib.lib().stb_acoustic_create(C.byref(d), C.byref(raw)))
         return _Prop(raw, config.dtype, ACOUSTIC_FIELDS)
+    if config.physics == "tti":
+        return _build_tti(config, dt, tables, x_begin, nx_local)
     vp = np.asarray(config.medium["vp"], dtype=np.float64)
     vs = np.asarray(config.medium["vs"], dtype=np.float64)
     rho = np.asarray(config.medium["rho"], dtype=np.float64)
@@ -427,6 +453,56 @@ def build_propagator(config: RunConfig, dt: float, v_max: float, x_begin: int = 
     return _Prop(raw, config.dtype, ELASTIC_FIELDS)
 
 
+def _build_tti(config: RunConfig, dt: float, tables, x_begin: int, nx_local: int) -> _Prop:
+    """TTI device model (csrc/tti.cu; repo-defined operator)."""
+    grid = config.grid
+    med = tti_medium(config.medium)
+    d = _lib.TTIDesc()
+    d.geom = _lib.geometry(grid)
+    d.space_order, d.precision, d.dt, d.dt2 = config.space_order, config.precision, dt, dt ** 2
+    d.x_begin, d.nx_local = int(x_begin), int(nx_local)
+    d1 = tti_coefficients(grid, config.space_order)
+    for a in range(3):
+        d.active[a] = int(grid.shape[a] > 1)
+        for k in range(4):
+            d.d1[a][k] = d1[a, k]
+    keep = []
+
+    def local(values, what):
+        a3 = np.ascontiguousarray(np.broadcast_to(np.asarray(values, np.float64), grid.shape))
+        if nx_local:
+            a3 = np.ascontiguousarray(a3[x_begin:x_begin + nx_local])
+        keep.append(a3)
+        return _lib.dptr(a3.reshape(-1))
+
+    if np.ndim(med.vp):
+        d.velocity = local(med.vp, "vp")
+    else:
+        m = 1.0 / float(med.vp) ** 2
+        if m <= 0.0:
+            raise ValueError("m must be positive")
+        d.inv_scalar = dt ** 2 / m
+    for name in ("e2", "d2"):
+        v = getattr(med, name)
+        if np.ndim(v):
+            setattr(d, name, local(v, name))
+        else:
+            setattr(d, f"{name}_scalar", float(v))
+    for a in range(3):
+        c = med.axis[a]
+        if np.ndim(c):
+            d.axis[a] = local(c, "axis")
+        else:
+            d.axis_scalar[a] = float(c)
+    if tables is not None:
+        for a in range(3):
+            keep.append(tables[a])
+            d.damp[a] = _lib.dptr(tables[a])
+    raw = C.c_void_p()
+    _lib.check(_lib.lib().stb_tti_create(C.byref(d), C.byref(raw)))
+    return _Prop(raw, config.dtype, TTI_FIELDS)
+
+
 def _wavelets(config: RunConfig, dt: float, nt: int) -> np.ndarray:
     """engine.py:258-272."""
     spec = config.sources
@@ -459,6 +535,8 @@ def run(config: RunConfig) -> RunResult:
         wav = _wavelets(config, dt, nt)
         if config.physics == "acoustic":
             scale = nearest_scales_from_velocity(spec.coords, grid, config.medium["velocity"], dt)
+        elif config.physics == "tti":
+            scale = nearest_scales_from_velocity(spec.coords, grid, config.medium["vp"], dt)
         else:
             scale = np.full(spec.nsrc, dt)
         handle = _Handle.from_coords(spec.coords, grid, keep_zero=False)
@@ -480,13 +558,13 @@ def run(config: RunConfig) -> RunResult:
         prop.run(0, nt, k, rec)
     elapsed = time.perf_counter() - t0
 
-    names = ACOUSTIC_FIELDS if config.physics == "acoustic" else ELASTIC_FIELDS
+    names = FIELDS[config.physics]
     t_final = nt - 1 if nt > 0 else 0
     if nt > 0:
         fields = {n: prop.read(n, t_final, grid.shape) for n in names}
     else:
         fields = {n: np.zeros(grid.shape, dtype=config.dtype) for n in names}
-    nf = 1 if config.physics == "acoustic" else 9
+    nf = len(names)
     gpoints = grid.npoints * nt * nf / elapsed / 1e9 if nt > 0 and elapsed > 0 else 0.0
     s = config.schedule
     report = RunReport(
@@ -499,8 +577,8 @@ def run(config: RunConfig) -> RunResult:
         arithmetic_intensity=arithmetic_intensity(config.physics, config.space_order,
                                                   config.precision),
         checksum_source=(fields, rec), nsrc=nsrc, nrec=nrec,
-        source_scale_rule=("dt^2/m at nearest grid point" if config.physics == "acoustic"
-                           else "dt"),
+        source_scale_rule=("dt" if config.physics == "elastic"
+                           else "dt^2/m at nearest grid point"),
         machine={"platform": platform.platform(),
                  "processor": platform.processor() or platform.machine(),
                  "cpus": os.cpu_count(), "device": "cuda"},

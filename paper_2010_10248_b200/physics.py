@@ -12,7 +12,9 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .grid import GridSpec, fd_weights, staggered_fd_weights
+import math
+
+from .grid import GridSpec, centered_first_weights, fd_weights, staggered_fd_weights
 
 
 @dataclass
@@ -100,3 +102,51 @@ def elastic_coefficients(grid: GridSpec, space_order: int):
         for j, cj in enumerate(c):
             d1[a, j] = float(cj / grid.spacing[a])
     return d1
+
+
+def tti_coefficients(grid: GridSpec, space_order: int):
+    """d1[a][k-1] = a_k / h_a for the TTI first derivatives (csrc/tti.cu)."""
+    a = centered_first_weights(space_order)
+    d1 = np.zeros((3, 4))
+    for ax in grid.active_axes:
+        for k, ak in enumerate(a):
+            d1[ax, k] = float(ak / grid.spacing[ax])
+    return d1
+
+
+def tti_axis(theta, phi):
+    """Symmetry axis z-bar = (sin t cos p, sin t sin p, cos t) of the rotated
+    frame of PAPER.md eq. 2 (x-bar = (cos t cos p, cos t sin p, -sin t)), f64."""
+    th = np.asarray(theta, dtype=np.float64)
+    ph = np.asarray(phi, dtype=np.float64)
+    return (np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th))
+
+
+@dataclass
+class TTIMedium:
+    """Host-side TTI material in f64: e2 = 1 + 2 eps, d2 = sqrt(1 + 2 delta),
+    axis = tti_axis(theta, phi); scalars stay Python floats."""
+
+    vp: object
+    e2: object
+    d2: object
+    axis: tuple
+
+
+def tti_medium(medium: dict) -> TTIMedium:
+    vp = medium["vp"]
+    eps = medium.get("epsilon", 0.0)
+    delta = medium.get("delta", 0.0)
+    th, ph = medium.get("theta", 0.0), medium.get("phi", 0.0)
+    if np.ndim(eps):
+        e2 = 1.0 + 2.0 * np.asarray(eps, dtype=np.float64)
+    else:
+        e2 = 1.0 + 2.0 * float(eps)
+    if np.ndim(delta):
+        d2 = np.sqrt(1.0 + 2.0 * np.asarray(delta, dtype=np.float64))
+    else:
+        d2 = math.sqrt(1.0 + 2.0 * float(delta))
+    axis = tti_axis(th, ph)
+    if np.ndim(th) == 0 and np.ndim(ph) == 0:
+        axis = tuple(float(c) for c in axis)
+    return TTIMedium(vp, e2, d2, axis)

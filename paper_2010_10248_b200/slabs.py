@@ -32,8 +32,8 @@ import math
 import numpy as np
 
 from . import _lib
-from .engine import (ACOUSTIC_FIELDS, ELASTIC_FIELDS, _gpu_time_height, _Handle, _Prop,
-                     _wavelets, build_propagator, medium_velocity_bounds, resolve_steps)
+from .engine import (FIELDS, _gpu_time_height, _Handle, _Prop, _wavelets, build_propagator,
+                     medium_velocity_bounds, resolve_steps)
 from .sparse import nearest_scales_from_velocity, stencils, validate_coords_in_extent
 
 DEFAULT_TIME_HEIGHT = 1
@@ -49,7 +49,8 @@ def partition(nx: int, world: int, rank: int) -> tuple[int, int]:
 def ghost_depth(k: int, radius: int, physics: str = "acoustic") -> int:
     """Planes each side that k fused steps consume, +1 for receivers that
     straddle the slab boundary.  Elastic: the v and tau half steps each
-    consume R planes per step (schedule.py:81-90: skew 2R)."""
+    consume R planes per step (schedule.py:81-90: skew 2R).  TTI: two
+    first derivatives of radius R/2 per step, i.e. R like acoustic."""
     per_step = 2 * radius if physics == "elastic" else radius
     return k * per_step + 1
 
@@ -125,10 +126,11 @@ class SlabRunner:
                  group=None):
         self.config, self.rank, self.world, self.group = config, rank, world, group
         self.elastic = config.physics == "elastic"
-        self.field_names = ELASTIC_FIELDS if self.elastic else ACOUSTIC_FIELDS
+        self.single_step = config.physics != "acoustic"     # elastic, tti: k = 1
+        self.field_names = FIELDS[config.physics]
         self.dt, self.nt = resolve_steps(config)
         k = _gpu_time_height(config)
-        self.time_height = 1 if self.elastic else (k if k > 0 else DEFAULT_TIME_HEIGHT)
+        self.time_height = 1 if self.single_step else (k if k > 0 else DEFAULT_TIME_HEIGHT)
         grid = config.grid
         nx = grid.shape[0]
         R = config.space_order // 2
@@ -154,8 +156,8 @@ class SlabRunner:
             if self.elastic:
                 scale = np.full(spec.nsrc, self.dt)       # engine.py:277-278
             else:
-                scale = nearest_scales_from_velocity(spec.coords, grid,
-                                                     config.medium["velocity"], self.dt)
+                vel = config.medium["vp" if config.physics == "tti" else "velocity"]
+                scale = nearest_scales_from_velocity(spec.coords, grid, vel, self.dt)
             self.dev.set_sources(spec.coords, wav, scale, self.nt)
         # receivers owned by base plane
         self.rec_index = np.zeros(0, dtype=np.int64)
@@ -210,6 +212,8 @@ class SlabRunner:
                 self._traces.append((t, rec))
             if self.elastic:
                 self.exchange([t], fields=range(len(self.field_names)))   # in place
+            elif self.single_step:                                       # tti: p, q
+                self.exchange([t], fields=range(len(self.field_names)))
             else:
                 self.exchange([t + kb - 1] + ([t + kb - 2] if kb >= 2 else []))
             t += kb
@@ -328,7 +332,24 @@ class SlabRunner:
             # separate v and tau launches: (6 tau + 3 v + buoy) reads + 3 v
             # writes, then (3 v + 6 tau + lam + mu) reads + 6 tau writes
             return 30 * item
+        if self.config.physics == "tti":
+            return tti_bytes_per_point(self.config)
         return (4 if self.time_height == 1 else 5) * item
+
+
+def tti_bytes_per_point(config) -> int:
+    """Compulsory HBM bytes per point of one TTI step (csrc/tti.cu): pass 1
+    reads p, q and the per-point axis components, writes F_a, G_a (2 per
+    active axis); pass 2 reads F, G, p, q, p_prev, q_prev and the per-point
+    inv/e2/d2, writes p, q."""
+    item = np.dtype(config.dtype).itemsize
+    na = len(config.grid.active_axes)
+    med = config.medium
+    th, ph = np.ndim(med.get("theta", 0.0)), np.ndim(med.get("phi", 0.0))
+    n_axis = 0 if (th == 0 and ph == 0) else na
+    mats = sum(1 for key in ("vp", "epsilon", "delta") if np.ndim(med.get(key, 0.0)))
+    streams = (2 + n_axis + 2 * na) + (2 * na + 4 + mats + 2)
+    return streams * item
 
 
 def run_distributed(config, rank: int, world: int, group=None, backend_factory=None):

@@ -121,9 +121,85 @@ def build_case(name: str) -> dict:
         c["src"] = dict(coords=[[640.3, 640.7, 200.5]], f0=10.0)
         c["receivers"] = np.stack([np.linspace(0.0, 1270.0, 101), np.full(101, 640.0),
                                    np.full(101, 20.0)], axis=1)
+    elif name.startswith("tti_"):
+        c.update(_tti_case(name, rng))
     else:
         raise KeyError(name)
     return c
+
+
+def tti_medium_arrays(rng, shape, vp_lo=1500.0, vp_hi=4000.0, layered=True):
+    """Seeded TTI medium with BASELINE cfg4's value ranges: layered vp,
+    epsilon in [0, 0.3], delta in [0, 0.2] capped at epsilon (pseudo-acoustic
+    TTI is unstable where delta > epsilon), smooth theta/phi in [-45, 45] deg
+    (radians here)."""
+    nx, ny, nz = shape
+    if layered:
+        nlay = 6
+        edges = np.sort(rng.integers(1, max(nz - 1, 2), size=nlay - 1))
+        lay = np.searchsorted(edges, np.arange(nz), side="right")
+        vp_l = np.sort(rng.uniform(vp_lo, vp_hi, nlay))
+        eps_l = rng.uniform(0.0, 0.3, nlay)
+        del_l = np.minimum(rng.uniform(0.0, 0.2, nlay), eps_l)
+        vp = np.broadcast_to(vp_l[lay][None, None, :], shape).copy()
+        eps = np.broadcast_to(eps_l[lay][None, None, :], shape).copy()
+        delta = np.broadcast_to(del_l[lay][None, None, :], shape).copy()
+    else:
+        vp = _smooth_field(rng, shape, vp_lo, vp_hi)
+        eps = _smooth_field(rng, shape, 0.0, 0.3)
+        delta = np.minimum(_smooth_field(rng, shape, 0.0, 0.2), eps)
+    q = np.pi / 4.0
+    theta = _smooth_field(rng, shape, -q, q)
+    phi = _smooth_field(rng, shape, -q, q)
+    return dict(vp=vp, epsilon=eps, delta=delta, theta=theta, phi=phi)
+
+
+def _tti_case(name, rng):
+    """Repo-defined TTI cases (no reference: parity is against the oracle)."""
+    if name in ("tti_so8_het_32", "tti_so8_het_32_f64"):
+        shape, h = (32, 30, 36), (10.0,) * 3
+        c = dict(physics="tti", shape=shape, spacing=h, bl=6, so=8, nt=40, dt=0.8e-3,
+                 medium=tti_medium_arrays(rng, shape, layered=False),
+                 precision=64 if name.endswith("f64") else 32)
+        c["src"] = dict(coords=random_coords(rng, shape, h, (0.0,) * 3, 3, margin=7), f0=20.0)
+        c["receivers"] = random_coords(rng, shape, h, (0.0,) * 3, 6, margin=7)
+    elif name == "tti_so4_layered":
+        shape, h = (28, 26, 30), (10.0, 12.0, 8.0)
+        c = dict(physics="tti", shape=shape, spacing=h, bl=4, so=4, nt=30, dt=0.6e-3,
+                 medium=tti_medium_arrays(rng, shape, layered=True))
+        c["src"] = dict(coords=random_coords(rng, shape, h, (0.0,) * 3, 2, margin=5), f0=22.0)
+        c["receivers"] = random_coords(rng, shape, h, (0.0,) * 3, 4, margin=5)
+    elif name in ("tti_so12_scalar", "tti_so16_scalar"):
+        shape, h = (26, 28, 30), (10.0,) * 3
+        c = dict(physics="tti", shape=shape, spacing=h, bl=5, so=int(name[6:8]), nt=24,
+                 dt=0.7e-3, medium=dict(vp=2600.0, epsilon=0.22, delta=0.08, theta=0.3,
+                                        phi=-0.4))
+        c["src"] = dict(coords=[[131.0, 137.3, 148.9]], f0=18.0)
+        c["receivers"] = random_coords(rng, shape, h, (0.0,) * 3, 3, margin=6)
+    elif name == "tti_so8_2d":
+        shape, h = (36, 1, 40), (10.0,) * 3
+        med = tti_medium_arrays(rng, shape, layered=False)
+        med["phi"] = 0.0
+        c = dict(physics="tti", shape=shape, spacing=h, bl=4, so=8, nt=30, dt=0.7e-3,
+                 medium=med)
+        c["src"] = dict(coords=[[171.0, 0.0, 190.5]], f0=20.0)
+        c["receivers"] = np.array([[100.0, 0.0, 100.0], [250.5, 0.0, 300.25]])
+    elif name == "tti_dense_src":
+        shape, h = (30, 30, 30), (10.0,) * 3
+        nt, nsrc = 18, 60
+        c = dict(physics="tti", shape=shape, spacing=h, bl=3, so=8, nt=nt, dt=0.6e-3,
+                 medium=tti_medium_arrays(rng, shape, layered=True))
+        coords = random_coords(rng, shape, h, (0.0,) * 3, nsrc, on_grid_fraction=0.2, margin=1)
+        coords[-1] = [290.0, 150.0, 290.0]
+        c["src"] = dict(coords=coords, wavelets=rng.normal(size=(nt, nsrc)))
+        c["receivers"] = random_coords(rng, shape, h, (0.0,) * 3, 20, margin=4)
+    else:
+        raise KeyError(name)
+    return c
+
+
+TTI_CASES = ["tti_so8_het_32", "tti_so8_het_32_f64", "tti_so4_layered", "tti_so12_scalar",
+             "tti_so16_scalar", "tti_so8_2d", "tti_dense_src"]
 
 
 SMALL_CASES = ["ac_so4_24", "ac_so8_het_32", "ac_so8_het_32_f64", "ac_so12_28",

@@ -21,6 +21,7 @@ class OracleSlab:
         self.x_begin, self.nl = x_begin, nx_local
         self.dtype = np.float32 if config.precision == 32 else np.float64
         self.elastic = config.physics == "elastic"
+        self.tti = config.physics == "tti"
         bl = g.boundary_layers
         decay = (config.damping_decay if config.damping_decay is not None
                  else so.default_decay(g.shape, g.spacing, bl, v_max))
@@ -42,6 +43,12 @@ class OracleSlab:
             self.model = so.Elastic(shape_l, g.spacing, config.space_order, local(lam),
                                     local(mu), local(rho), dt, damp, self.dtype)
             self.names = so.Elastic.V + so.Elastic.T
+        elif self.tti:
+            m, e2, d2, axis = so.tti_medium(config.medium)
+            self.R = config.space_order // 4
+            self.model = so.TTI(shape_l, g.spacing, config.space_order, local(m), local(e2),
+                                local(d2), tuple(local(c) for c in axis), dt, damp, self.dtype)
+            self.names = ("p", "q")
         else:
             vel = config.medium["velocity"]
             if np.ndim(vel):
@@ -55,7 +62,9 @@ class OracleSlab:
         self.ridx = None
 
     def _level(self, name, t):
-        return self.model.lv(name, t) if self.elastic else self.model.level(t)
+        if self.elastic or self.tti:
+            return self.model.lv(name, t)
+        return self.model.level(t)
 
     def stencil_index(self, coords):
         g = self.config.grid
@@ -81,8 +90,8 @@ class OracleSlab:
 
     def run(self, t0, n, k, rec_out=None):
         R = self.R
-        targets = ("txx", "tyy", "tzz") if self.elastic else ("u",)
-        gather = "txx" if self.elastic else "u"
+        targets = ("txx", "tyy", "tzz") if self.elastic else ("p", "q") if self.tti else ("u",)
+        gather = "txx" if self.elastic else "p" if self.tti else "u"
         for t in range(t0, t0 + n):
             self.model.step(t)
             if self.pts is not None and len(self.pts):

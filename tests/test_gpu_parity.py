@@ -258,7 +258,8 @@ def test_cfg1_fma_mode_tolerance(golden_big):
 
 # ------------------------------------------------- x-slab device mechanics
 
-@pytest.mark.parametrize("kind,k", [("acoustic", 1), ("acoustic", 2), ("elastic", 1)])
+@pytest.mark.parametrize("kind,k", [("acoustic", 1), ("acoustic", 2), ("elastic", 1),
+                                    ("tti", 1)])
 def test_xslab_handles_emulated_two_ranks(kind, k):
     """Two x-slab handles on one GPU, ghost planes exchanged by device
     copies in the order slabs.SlabRunner uses (NCCL replaced by copies: two
@@ -282,7 +283,8 @@ def test_xslab_handles_emulated_two_ranks(kind, k):
                 rr._traces.append((t, rec))
         lo, hi = ranks
         g = lo.hi - lo.b                       # ghost planes on each side
-        levels = [t] if kind == "elastic" else [t + kb - 1] + ([t + kb - 2] if kb >= 2 else [])
+        levels = ([t] if kind in ("elastic", "tti")
+                  else [t + kb - 1] + ([t + kb - 2] if kb >= 2 else []))
         for lev in levels:
             for f in range(nf):
                 # rank 0 top ghost <- rank 1 first owned planes; and vice versa

@@ -70,7 +70,7 @@ def test_config_errors_name_fields():
         stb.RunConfig(physics="acoustic", grid=g, space_order=3, nt=4)
     assert e.value.field == "space_order"
     with pytest.raises(stb.ConfigError) as e:
-        stb.RunConfig(physics="tti", grid=g, space_order=4, nt=4)
+        stb.RunConfig(physics="viscoelastic", grid=g, space_order=4, nt=4)
     assert e.value.field == "physics"
     with pytest.raises(stb.ConfigError) as e:
         stb.RunConfig(physics="acoustic", grid=g, space_order=4)

@@ -53,7 +53,23 @@ def _elastic_case():
                          sources=stb.SourceSpec(src, f0=30.0), receiver_coords=rec)
 
 
+def _tti_case():
+    import paper_2010_10248_b200 as stb
+    from cases import tti_medium_arrays
+    rng = np.random.default_rng(7)
+    shape = (38, 18, 20)
+    grid = stb.GridSpec(shape, (10.0, 10.0, 10.0), (0.0, 0.0, 0.0), boundary_layers=3)
+    src = np.array([[187.0, 85.0, 95.0], [121.3, 60.0, 90.5]])
+    rec = random_coords(rng, shape, grid.spacing, grid.origin, 8, margin=4)
+    rec[0] = [185.5, 70.0, 80.0]            # straddles x = 19 (2 ranks)
+    return stb.RunConfig(physics="tti", grid=grid, space_order=8, nt=12, dt=0.6e-3,
+                         medium=tti_medium_arrays(rng, shape, layered=False),
+                         sources=stb.SourceSpec(src, f0=30.0), receiver_coords=rec)
+
+
 def _make(kind, k):
+    if kind == "tti":
+        return _tti_case()
     return _elastic_case() if kind == "elastic" else _case(k)
 
 
@@ -73,7 +89,7 @@ def _worker(rank, world, port, k, out_path, kind="acoustic"):
 
 @pytest.mark.parametrize("kind,world,k", [("acoustic", 2, 1), ("acoustic", 2, 2),
                                           ("acoustic", 3, 1), ("elastic", 2, 1),
-                                          ("elastic", 3, 1)])
+                                          ("elastic", 3, 1), ("tti", 2, 1), ("tti", 3, 1)])
 def test_xslab_matches_single_domain(kind, world, k, tmp_path):
     from oracle import stencil_oracle as so
     out = str(tmp_path / "res.npz")
