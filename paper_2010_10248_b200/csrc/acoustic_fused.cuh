@@ -107,25 +107,6 @@ struct FusedArgs {
   int guard_mask;        // bit j-1: step t0+j-1 is a guard step
 };
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Blocking wait with a suspend-time hint: the warp sleeps in the barrier
-// instead of spinning on issue slots.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAITS_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAITS_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(parity), "r"(0x100000u)
-      : "memory");
-}
-
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

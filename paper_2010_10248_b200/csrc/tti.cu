@@ -33,6 +33,7 @@
 #include "padded.cuh"
 #include "sparse_ops.cuh"
 #include "stb_internal.cuh"
+#include "tma.cuh"
 
 namespace stb {
 
@@ -47,6 +48,14 @@ struct TtiCoefs {
   T inv, e2, d2;      // scalars when the material pointer is NULL
   T n[3];
 };
+
+}  // namespace
+}  // namespace stb
+
+#include "tti_fused.cuh"
+
+namespace stb {
+namespace {
 
 template <typename T>
 struct TtiArgs {
@@ -175,6 +184,16 @@ __global__ void tti_material_kernel(const double* __restrict__ src, PDims d, T* 
   }
 }
 
+template <typename T>
+__global__ void tti_fill_kernel(T* __restrict__ dst, PDims d, T v) {
+  const int64_t n = d.nx * d.ny * d.nz;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = i % d.nz, xy = i / d.nz;
+    dst[d.at(xy / d.ny, xy % d.ny, z)] = v;
+  }
+}
+
 template <typename T, int r>
 void launch_tti(cudaStream_t st, const TtiArgs<T>& a) {
   dim3 block(32, 4);
@@ -251,6 +270,31 @@ class TtiProp final : public stb_prop_s {
     material(desc.d2, desc.d2_scalar, d2_, cf_.d2);
     for (int ax = 0; ax < 3; ++ax) material(desc.axis[ax], desc.axis_scalar[ax], n_[ax], cf_.n[ax]);
     has_fac_ = desc.damp[0] || desc.damp[1] || desc.damp[2];
+    fused_ = sizeof(T) == 4 && cf_.active[0] && cf_.active[1] && cf_.active[2];
+    if (const char* e = std::getenv("STB_TTI_PATH")) fused_ = fused_ && std::string(e) != "twopass";
+    cx_ = 150;
+    if (const char* e = std::getenv("STB_TTI_CX")) cx_ = std::max(1, std::atoi(e));
+    if (fused_) {
+      // the gradient streams are never materialised on this path; scalar
+      // materials are, so the fused loop has no pointer tests
+      for (int ax = 0; ax < 3; ++ax) {
+        F_[ax].release();
+        G_[ax].release();
+      }
+      auto materialise = [&](DevBuf<T>& b, T v) {
+        if (b.p) return;
+        b.alloc(d_.total);
+        b.zero(st_);
+        tti_fill_kernel<T><<<1184, 256, 0, st_>>>(b.p, d_, v);
+        STB_CHECK_LAUNCH();
+      };
+      materialise(inv_, cf_.inv);
+      materialise(e2_, cf_.e2);
+      materialise(d2_, cf_.d2);
+      for (int ax = 0; ax < 3; ++ax) materialise(n_[ax], cf_.n[ax]);
+      STB_CUDA(cudaStreamSynchronize(st_));
+      setup_fused();
+    }
     const int64_t n3[3] = {d_.nx, d_.ny, d_.nz};
     for (int ax = 0; ax < 3; ++ax) {
       fac_[ax].alloc(n3[ax]);
@@ -365,7 +409,9 @@ class TtiProp final : public stb_prop_s {
       const bool guard_now = gi < guard_steps.size() && guard_steps[gi] == t;
       A.nonfinite = guard_now ? guards.p + gi : nullptr;
       STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
-      switch (r_) {
+      if (fused_) {
+        launch_fused(A, prev);
+      } else switch (r_) {
         case 1: launch_tti<T, 1>(st_, A); break;
         case 2: launch_tti<T, 2>(st_, A); break;
         case 3: launch_tti<T, 3>(st_, A); break;
@@ -375,7 +421,7 @@ class TtiProp final : public stb_prop_s {
       STB_CHECK_LAUNCH();
       STB_CUDA(cudaEventRecord(events_[2 * launches_ + 1], st_));
       ++launches_;
-      all_launches_ += 2;
+      all_launches_ += fused_ ? 1 : 2;
       if (guard_now) ++gi;
       if (K_) {
         for (int f = 0; f < 2; ++f)
@@ -451,15 +497,96 @@ class TtiProp final : public stb_prop_s {
     int nmat = (inv_.p ? 1 : 0) + (e2_.p ? 1 : 0) + (d2_.p ? 1 : 0);
     for (auto& b : n_) nmat += b.p ? 1 : 0;
     int na = cf_.active[0] + cf_.active[1] + cf_.active[2];
-    const int bpp = (int)sizeof(T) * (2 + 2 * na + 2 * na + 4 + 2 + nmat);
     std::ostringstream os;
-    os << "tti_pass1+pass2<" << (sizeof(T) == 4 ? "f32" : "f64") << ",r=" << r_
-       << "> (thread per point, zero-haloed layout) k=1 requested_k=" << k
-       << " bytes_per_point=" << bpp;
+    if (fused_) {
+      const int bpp = (int)sizeof(T) * (2 + 2 + 2 + nmat);
+      os << "tti_fused<f32,r=" << r_ << ",ring=" << m_for_r(r_) << "x" << (2 * r_ + 1)
+         << "> (TMA p/q plane ring, 16x32 tile, x chunk " << cx_
+         << ", F/G on chip) k=1 requested_k=" << k << " bytes_per_point=" << bpp;
+    } else {
+      const int bpp = (int)sizeof(T) * (2 + 2 * na + 2 * na + 4 + 2 + nmat);
+      os << "tti_pass1+pass2<" << (sizeof(T) == 4 ? "f32" : "f64") << ",r=" << r_
+         << "> (thread per point, zero-haloed layout) k=1 requested_k=" << k
+         << " bytes_per_point=" << bpp;
+    }
     return os.str();
   }
 
  private:
+  // ring of M (2r+1) plane slots: M = 2 leaves 2r+1 planes of TMA lead;
+  // so=16 (r = 4) only fits M = 1 in shared memory
+  static constexpr int m_for_r(int r) { return r <= 3 ? 2 : 1; }
+
+  template <int r>
+  void set_fused_attr() {
+    constexpr int M = m_for_r(r);
+    STB_CUDA(cudaFuncSetAttribute(tti_fused<r, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)TtiFusedCfg<r, M>::smem_bytes()));
+  }
+
+  void setup_fused() {
+    if constexpr (sizeof(T) == 4) {
+      const int r = r_;
+      // TMA view of the padded layout: dims (pitch, ny + 2H, nx + 2H)
+      Dims md{};
+      md.nx = d_.nx + 2 * d_.H;
+      md.ny = d_.ny + 2 * d_.H;
+      md.nz = d_.pitch;
+      md.pitch = d_.pitch;
+      md.plane = d_.plane;
+      const uint32_t pz = kTtiTZ + 2 * ((2 * r + 3) / 4 * 4), py = kTtiTY + 4 * r;
+      for (int l = 0; l < 2; ++l) {
+        maps_[l].p = make_map3d_f32(reinterpret_cast<const float*>(lv_[0][l].p), md, pz, py, 1);
+        maps_[l].q = make_map3d_f32(reinterpret_cast<const float*>(lv_[1][l].p), md, pz, py, 1);
+      }
+      switch (r) {
+        case 1: set_fused_attr<1>(); break;
+        case 2: set_fused_attr<2>(); break;
+        case 3: set_fused_attr<3>(); break;
+        case 4: set_fused_attr<4>(); break;
+        default: break;
+      }
+    }
+  }
+
+  template <int r>
+  void launch_fused_r(const TtiFusedArgs& fa, int prev) {
+    dim3 grid((unsigned)((d_.nz + kTtiTZ - 1) / kTtiTZ), (unsigned)((d_.ny + kTtiTY - 1) / kTtiTY),
+              (unsigned)((d_.nx + cx_ - 1) / cx_));
+    constexpr int M = m_for_r(r);
+    tti_fused<r, M><<<grid, kTtiThreads, TtiFusedCfg<r, M>::smem_bytes(), st_>>>(maps_[prev], fa);
+  }
+
+  void launch_fused(const TtiArgs<T>& A, int prev) {
+    if constexpr (sizeof(T) == 4) {
+      TtiFusedArgs fa{};
+      fa.p0 = A.p0;
+      fa.q0 = A.q0;
+      fa.inv = A.inv;
+      fa.e2 = A.e2;
+      fa.d2 = A.d2;
+      for (int ax = 0; ax < 3; ++ax) fa.n[ax] = A.n[ax];
+      fa.fx = A.fx;
+      fa.fy = A.fy;
+      fa.fz = A.fz;
+      fa.has_fac = A.has_fac;
+      fa.cf = A.cf;
+      fa.d = A.d;
+      fa.cx = cx_;
+      fa.nonfinite = A.nonfinite;
+      switch (r_) {
+        case 1: launch_fused_r<1>(fa, prev); break;
+        case 2: launch_fused_r<2>(fa, prev); break;
+        case 3: launch_fused_r<3>(fa, prev); break;
+        case 4: launch_fused_r<4>(fa, prev); break;
+        default: throw Error(STB_ERR_CONFIG, "space_order: TTI supports 4, 8, 12, 16");
+      }
+    } else {
+      (void)A;
+      (void)prev;
+    }
+  }
+
   void ensure_events(int64_t n) {
     for (auto& e : run_ev_)
       if (!e) STB_CUDA(cudaEventCreate(&e));
@@ -471,6 +598,9 @@ class TtiProp final : public stb_prop_s {
   }
 
   int r_ = 1;
+  bool fused_ = false;
+  int cx_ = 150;
+  TtiMaps maps_[2];           // [level buffer] p/q tensor maps (fused path)
   PDims d_{};
   stb_geometry geom_{};
   int64_t x_begin_ = 0;

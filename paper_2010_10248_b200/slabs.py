@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import re
 
 import numpy as np
 
@@ -333,7 +334,9 @@ class SlabRunner:
             # writes, then (3 v + 6 tau + lam + mu) reads + 6 tau writes
             return 30 * item
         if self.config.physics == "tti":
-            return tti_bytes_per_point(self.config)
+            # the device reports the path it chose (fused: 48 B f32)
+            m = re.search(r"bytes_per_point=(\d+)", self.describe())
+            return int(m.group(1)) if m else tti_bytes_per_point(self.config)
         return (4 if self.time_height == 1 else 5) * item
 
 
