@@ -225,6 +225,11 @@ int stb_prop_read_field(stb_prop_t p, int32_t field, int64_t t, void* out);
  * *plane_elems elements (ny rows of *pitch_elems, z fastest). */
 int stb_prop_level_ptr(stb_prop_t p, int32_t field, int64_t t, void** dev,
                        int64_t* plane_elems, int64_t* pitch_elems);
+/* Write field `field` at level t to `path` in stencil_tb's snapshot format
+ * (engine.py:553-577): a 32-byte header -- "STBSNAP\0", uint32 bits (32 or
+ * 64), int32 nx, ny, nz, uint32 t, zero padding -- then the (nx, ny, nz)
+ * C-order little-endian samples.  Device -> file without Python. */
+int stb_prop_write_snapshot(stb_prop_t p, int32_t field, int64_t t, const char* path);
 /* Zero all time levels (reuse a handle for another shot). */
 int stb_prop_reset(stb_prop_t p);
 /* Device-side timing of the last stb_prop_run (CUDA events on the launching

@@ -29,7 +29,7 @@ EXPORTS = (
     "stb_support_compress", "stb_support_masks", "stb_support_entries",
     "stb_support_decompose", "stb_support_destroy", "stb_acoustic_create",
     "stb_elastic_create", "stb_tti_create", "stb_prop_set_sources", "stb_prop_set_receivers", "stb_prop_run",
-    "stb_prop_read_field", "stb_prop_level_ptr", "stb_prop_reset", "stb_prop_stats",
+    "stb_prop_read_field", "stb_prop_level_ptr", "stb_prop_write_snapshot", "stb_prop_reset", "stb_prop_stats",
     "stb_prop_describe",
     "stb_prop_destroy",
 )
@@ -101,6 +101,7 @@ def _declare(lib):
         "stb_prop_run": ([P, i64, i64, i32, pdbl, pi64], C.c_int),
         "stb_prop_read_field": ([P, i32, i64, P], C.c_int),
         "stb_prop_level_ptr": ([P, i32, i64, C.POINTER(P), pi64, pi64], C.c_int),
+        "stb_prop_write_snapshot": ([P, i32, i64, C.c_char_p], C.c_int),
         "stb_prop_reset": ([P], C.c_int),
         "stb_prop_stats": ([P, pi64, pdbl, pi64, pi64, pdbl], C.c_int),
         "stb_prop_describe": ([P, i32, C.c_char_p, i64], C.c_int),

@@ -1,7 +1,9 @@
 // extern "C" entry points of libstb200.so (declared in include/stb200.h).
 // Every entry converts C++ exceptions / CUDA errors into a status code and a
 // thread-local message; nothing throws across the ABI.
+#include <cstdio>
 #include <cstring>
+#include <vector>
 #include <memory>
 #include <new>
 #include <string>
@@ -213,6 +215,33 @@ STB_API int stb_tti_create(const stb_tti_desc* d, stb_prop_t* out) {
     check_precision(d->precision);
     require_device();
     *out = make_tti(*d);
+  })
+}
+
+STB_API int stb_prop_write_snapshot(stb_prop_t p, int32_t field, int64_t t, const char* path) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr && path != nullptr, STB_ERR_ARG, "NULL argument");
+    STB_REQUIRE(t >= 0 && t <= (int64_t)UINT32_MAX, STB_ERR_ARG, "time index out of range");
+    int64_t shape[3];
+    int elem = 0;
+    p->field_info(shape, &elem);
+    STB_REQUIRE(shape[0] <= INT32_MAX && shape[1] <= INT32_MAX && shape[2] <= INT32_MAX,
+                STB_ERR_ARG, "field too large for the snapshot header");
+    std::vector<unsigned char> buf((size_t)(shape[0] * shape[1] * shape[2]) * elem);
+    p->read_field(field, t, buf.data());
+    unsigned char head[32] = {0};
+    std::memcpy(head, "STBSNAP\0", 8);
+    const uint32_t bits = (uint32_t)(8 * elem), tt = (uint32_t)t;
+    const int32_t dims[3] = {(int32_t)shape[0], (int32_t)shape[1], (int32_t)shape[2]};
+    std::memcpy(head + 8, &bits, 4);
+    std::memcpy(head + 12, dims, 12);
+    std::memcpy(head + 24, &tt, 4);
+    std::FILE* f = std::fopen(path, "wb");
+    STB_REQUIRE(f != nullptr, STB_ERR_ARG, std::string("cannot open ") + path);
+    const bool ok = std::fwrite(head, 1, 32, f) == 32 &&
+                    std::fwrite(buf.data(), 1, buf.size(), f) == buf.size();
+    std::fclose(f);
+    STB_REQUIRE(ok, STB_ERR_ARG, std::string("short write to ") + path);
   })
 }
 

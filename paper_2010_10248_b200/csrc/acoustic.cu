@@ -468,6 +468,13 @@ class AcousticProp final : public stb_prop_s {
     if (run_ms) *run_ms = run_ms_;
   }
 
+  void field_info(int64_t shape[3], int* elem_bytes) override {
+    shape[0] = d_.nx;
+    shape[1] = d_.ny;
+    shape[2] = d_.nz;
+    *elem_bytes = (int)sizeof(T);
+  }
+
   std::string describe(int k) override {
     std::ostringstream os;
     const int kk = resolve_k(k);

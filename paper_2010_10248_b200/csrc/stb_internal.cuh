@@ -181,6 +181,8 @@ struct stb_prop_s {
   virtual void stats(int64_t* launches, double* ms, int64_t* updates, int64_t* all_launches,
                      double* run_ms) = 0;
   virtual std::string describe(int k) = 0;
+  // local field shape (x slab) and element size, for host-side copies
+  virtual void field_info(int64_t shape[3], int* elem_bytes) = 0;
 };
 
 struct stb_support_s {

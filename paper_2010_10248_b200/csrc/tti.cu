@@ -493,6 +493,13 @@ class TtiProp final : public stb_prop_s {
     if (run_ms) *run_ms = run_ms_;
   }
 
+  void field_info(int64_t shape[3], int* elem_bytes) override {
+    shape[0] = d_.nx;
+    shape[1] = d_.ny;
+    shape[2] = d_.nz;
+    *elem_bytes = (int)sizeof(T);
+  }
+
   std::string describe(int k) override {
     int nmat = (inv_.p ? 1 : 0) + (e2_.p ? 1 : 0) + (d2_.p ? 1 : 0);
     for (auto& b : n_) nmat += b.p ? 1 : 0;

@@ -330,6 +330,12 @@ class _Prop:
                                                   out.ctypes.data_as(C.c_void_p)))
         return out
 
+    def write_snapshot(self, name, t, path):
+        """Device field -> snapshot file (stb_prop_write_snapshot; same bytes
+        as save_snapshot(path, field, t), engine.py:553-566)."""
+        _lib.check(_lib.lib().stb_prop_write_snapshot(self.raw, self.fields.index(name), t,
+                                                      os.fsencode(path)))
+
     def reset(self):
         _lib.check(_lib.lib().stb_prop_reset(self.raw))
 
@@ -503,6 +509,25 @@ def _build_tti(config: RunConfig, dt: float, tables, x_begin: int, nx_local: int
     return _Prop(raw, config.dtype, TTI_FIELDS)
 
 
+def _validate_device_plan(config: RunConfig, prop: _Prop, k: int, nt: int, handle) -> None:
+    """engine.py:416-423 for the device plan: replay its launch/CTA command
+    stream through the validator (plan.py) with the source support and the
+    receiver corners as sparse footprints; any violation -> InvalidPlanError."""
+    from . import plan
+    from .sparse import stencils
+    k_dev, tile = plan.device_geometry(prop.describe(k))
+    gpts = None
+    if config.receiver_coords is not None and len(config.receiver_coords):
+        idx, w = stencils(config.receiver_coords, config.grid)
+        gpts = idx.reshape(-1, 3)[w.ravel() > 0.0]
+    viol = plan.validate_device_plan(config, nt=nt, k=k_dev, tile=tile,
+                                     inject_points=handle.points() if handle else None,
+                                     gather_points=gpts)
+    if viol:
+        raise InvalidPlanError(f"schedule validation found {len(viol)} violation(s); "
+                               f"first: {viol[0]}")
+
+
 def _wavelets(config: RunConfig, dt: float, nt: int) -> np.ndarray:
     """engine.py:258-272."""
     spec = config.sources
@@ -552,6 +577,9 @@ def run(config: RunConfig) -> RunResult:
         nrec = rc.shape[0]
         rec = np.zeros((nt, nrec), dtype=np.float64)
     precompute_s = time.perf_counter() - t_pre0
+
+    if config.validate and nt > 0:
+        _validate_device_plan(config, prop, k, nt, handle if nsrc else None)
 
     t0 = time.perf_counter()
     if nt > 0:

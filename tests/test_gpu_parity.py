@@ -305,3 +305,39 @@ def test_xslab_handles_emulated_two_ranks(kind, k):
         for t0, rec in rr._traces:
             traces[t0:t0 + rec.shape[0], rr.rec_index] = rec
     np.testing.assert_array_equal(traces, ref.receivers)
+
+
+# ------------------------------------------------- snapshots / plan validation
+
+@pytest.mark.parametrize("name", ["ac_so8_het_32", "el_so4_24", "ac_so8_het_32_f64"])
+def test_device_snapshot_matches_host_format(name, tmp_path):
+    """stb_prop_write_snapshot writes exactly save_snapshot's bytes
+    (engine.py:553-577 format), straight from device memory."""
+    from paper_2010_10248_b200.engine import (build_propagator, load_snapshot,
+                                              medium_velocity_bounds, resolve_steps,
+                                              save_snapshot)
+    cfg = to_config(build_case(name), stb)
+    vmax = medium_velocity_bounds(cfg.physics, cfg.medium)
+    dt, nt = resolve_steps(cfg, vmax)
+    prop = build_propagator(cfg, dt, vmax)
+    prop.run(0, 5, 1)
+    for field in prop.fields[:2]:
+        arr = prop.read(field, 4, cfg.grid.shape)
+        save_snapshot(tmp_path / "host.snap", arr, 4)
+        prop.write_snapshot(field, 4, tmp_path / "dev.snap")
+        assert (tmp_path / "host.snap").read_bytes() == (tmp_path / "dev.snap").read_bytes()
+        back, t = load_snapshot(tmp_path / "dev.snap")
+        np.testing.assert_array_equal(back, arr)
+        assert t == 4
+
+
+def test_validate_flag_replays_device_plan():
+    """RunConfig.validate runs the device-plan legality check (plan.py) before
+    stepping, as engine.py:416-423 does for the CPU plans."""
+    for k in (1, 2):
+        case = build_case("ac_so4_24")
+        res = stb.run(to_config(case, stb, schedule=stb.ScheduleSpec("gpu", time_height=k)))
+        cfg = to_config(case, stb, schedule=stb.ScheduleSpec("gpu", time_height=k))
+        cfg.validate = True
+        res_v = stb.run(cfg)
+        np.testing.assert_array_equal(res.fields["u"], res_v.fields["u"])
