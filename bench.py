@@ -358,6 +358,10 @@ def main():
 
     # ------------------------------------------------------------ e2e
     e2e = None
+    describe = runner.describe()
+    kernel_tag = runner.kernel_tag()
+    del runner                        # its device buffers go back to the pool
+    torch.cuda.synchronize()
     if not args.no_e2e and world == 1:
         cfg_e = make_config(stb, v, src, rec, args.steps, args.k, args.arithmetic, wl)
         torch.cuda.synchronize()
@@ -414,7 +418,7 @@ def main():
                        "l2": "inputs larger than L2 (each 592^3 f32 field ~0.85 GB >> 126 MB)",
                        "gpts_counting": "computational grid incl. sponge (engine.py:445-447)",
                        "value_physical_512": PHYS ** 3 * args.steps / (t_ms / 1e3) / 1e9,
-                       "kernel": runner.describe()},
+                       "kernel": describe},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": st["launches"], "clocks": clocks,
         }

@@ -436,9 +436,8 @@ class AcousticProp final : public stb_prop_s {
   void read_field(int field, int64_t t, void* out) override {
     STB_REQUIRE(field == 0, STB_ERR_ARG, "acoustic handles have one field (u)");
     const T* src = lvl_[slot(t)].p;
-    STB_CUDA(cudaMemcpy2DAsync(out, d_.nz * sizeof(T), src, d_.pitch * sizeof(T),
-                               d_.nz * sizeof(T), d_.nx * d_.ny, cudaMemcpyDeviceToHost, st_));
-    STB_CUDA(cudaStreamSynchronize(st_));
+    device_to_host_3d(out, src, d_.nz * sizeof(T), d_.ny, d_.nx, d_.pitch * sizeof(T),
+                      d_.plane * sizeof(T), st_);
   }
 
   void level_ptr(int field, int64_t t, void** dev, int64_t* plane, int64_t* pitch) override {

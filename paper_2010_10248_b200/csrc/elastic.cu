@@ -682,15 +682,7 @@ class ElasticProp final : public stb_prop_s {
     STB_REQUIRE(field >= 0 && field < NFIELDS, STB_ERR_ARG, "elastic field index in [0, 9)");
     STB_REQUIRE(t == t_next_ - 1 || (t_next_ == 0), STB_ERR_ARG,
                 "only the latest time level is resident for elastic handles");
-    cudaMemcpy3DParms p{};
-    p.srcPtr = make_cudaPitchedPtr(f_[field].p, d_.pitch * sizeof(T), d_.pitch, d_.ny + 2 * d_.H);
-    p.srcPos = make_cudaPos(d_.zoff * sizeof(T), d_.H, d_.H);
-    p.dstPtr = make_cudaPitchedPtr(out, d_.nz * sizeof(T), d_.nz, d_.ny);
-    p.dstPos = make_cudaPos(0, 0, 0);
-    p.extent = make_cudaExtent(d_.nz * sizeof(T), d_.ny, d_.nx);
-    p.kind = cudaMemcpyDeviceToHost;
-    STB_CUDA(cudaMemcpy3DAsync(&p, st_));
-    STB_CUDA(cudaStreamSynchronize(st_));
+    pad_read<T>(f_[field].p, d_, out, st_);
   }
 
   // Planes of the padded layout: local plane p starts at (p + H) * plane.

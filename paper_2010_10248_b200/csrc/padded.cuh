@@ -82,18 +82,11 @@ __global__ void pad_nonfinite_kernel(const T* __restrict__ u, PDims d, int* flag
 }
 
 
-// Padded interior -> host (nx, ny, nz) array.
+// Padded interior -> host (nx, ny, nz) array (staged, hostio.cu).
 template <typename T>
 void pad_read(const T* f, const PDims& d, void* out, cudaStream_t st) {
-  cudaMemcpy3DParms p{};
-  p.srcPtr = make_cudaPitchedPtr(const_cast<T*>(f), d.pitch * sizeof(T), d.pitch, d.ny + 2 * d.H);
-  p.srcPos = make_cudaPos(d.zoff * sizeof(T), d.H, d.H);
-  p.dstPtr = make_cudaPitchedPtr(out, d.nz * sizeof(T), d.nz, d.ny);
-  p.dstPos = make_cudaPos(0, 0, 0);
-  p.extent = make_cudaExtent(d.nz * sizeof(T), d.ny, d.nx);
-  p.kind = cudaMemcpyDeviceToHost;
-  STB_CUDA(cudaMemcpy3DAsync(&p, st));
-  STB_CUDA(cudaStreamSynchronize(st));
+  device_to_host_3d(out, f + d.at(0, 0, 0), d.nz * sizeof(T), d.ny, d.nx, d.pitch * sizeof(T),
+                    d.plane * sizeof(T), st);
 }
 
 }  // namespace

@@ -57,6 +57,15 @@ inline void retain_freed_memory() {
 }
 
 // Owning device buffer.
+// Large host <-> device copies staged through pinned buffers (hostio.cu).
+// host_to_device is stream-ordered (returns once the host array may be
+// reused); the device_to_host variants return when the data is on the host.
+void host_to_device(void* dev, const void* host, size_t bytes, cudaStream_t st);
+void device_to_host(void* host, const void* dev, size_t bytes, cudaStream_t st);
+// dense (nx, ny, row bytes) host array <- rows at dev + x*plane + y*pitch bytes
+void device_to_host_3d(void* host, const void* dev, size_t row, size_t ny, size_t nx,
+                       size_t pitch, size_t plane, cudaStream_t st);
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -92,10 +101,11 @@ struct DevBuf {
     if (p) STB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
   }
   void upload(const T* h, size_t count, cudaStream_t s = 0) {
-    if (count) STB_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (count) host_to_device(p, h, count * sizeof(T), s);
   }
+  // synchronous: the data is on the host when this returns
   void download(T* h, size_t count, cudaStream_t s = 0) const {
-    if (count) STB_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+    if (count) device_to_host(h, p, count * sizeof(T), s);
   }
   T* get() const { return p; }
 };

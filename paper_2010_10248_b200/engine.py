@@ -211,6 +211,7 @@ def medium_velocity_bounds(physics: str, medium: dict) -> float:
     return float(np.max(medium["vp"]))
 
 
+
 def stable_dt(physics: str, grid: GridSpec, v_max: float, space_order: int,
               safety: float = 0.9) -> float:
     """Order-aware CFL bound (engine.py:172-195)."""

@@ -5,7 +5,8 @@ import numpy as np
 import bench
 import paper_2010_10248_b200 as stb
 v, src, rec = bench.cfg2_inputs()
-cfg = bench.make_config(stb, v, src, rec, 64, 0)
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+cfg = bench.make_config(stb, v, src, rec, steps, 0)
 stb.run(cfg)  # warm (CUDA context, module load)
 pr = cProfile.Profile()
 t0 = time.perf_counter(); pr.enable(); res = stb.run(cfg); pr.disable(); t1 = time.perf_counter()
