@@ -28,8 +28,8 @@ import numpy as np
 from . import _lib
 from .errors import ConfigError, InvalidPlanError
 from .grid import GridSpec, centered_first_weights, fd_weights, staggered_fd_weights
-from .physics import (acoustic_coefficients, damping_tables, elastic_coefficients, ricker,
-                      tti_coefficients, tti_medium)
+from .physics import (_field_op, acoustic_coefficients, damping_tables, elastic_coefficients,
+                      ricker, tti_coefficients, tti_medium)
 from .precompute import _Handle
 from .sparse import nearest_scales_from_velocity, validate_coords_in_extent
 
@@ -204,7 +204,11 @@ def medium_velocity_bounds(physics: str, medium: dict) -> float:
                               "delta, theta, phi)")
         vp = np.asarray(medium["vp"], np.float64)
         eps = np.asarray(medium.get("epsilon", 0.0), np.float64)
-        return float(np.max(vp * np.sqrt(1.0 + 2.0 * np.maximum(eps, 0.0))))
+        if vp.ndim == 0 and eps.ndim == 0:
+            return float(np.max(vp * np.sqrt(1.0 + 2.0 * np.maximum(eps, 0.0))))
+        shape = np.broadcast_shapes(vp.shape, eps.shape)
+        fast = _field_op(shape, lambda v, e: v * np.sqrt(1.0 + 2.0 * np.maximum(e, 0.0)), vp, eps)
+        return float(np.max(fast))
     for key in ("vp", "vs", "rho"):
         if key not in medium:
             raise ConfigError(f"medium.{key}", "elastic runs need vp, vs, rho")
@@ -463,7 +467,7 @@ def build_propagator(config: RunConfig, dt: float, v_max: float, x_begin: int = 
 def _build_tti(config: RunConfig, dt: float, tables, x_begin: int, nx_local: int) -> _Prop:
     """TTI device model (csrc/tti.cu; repo-defined operator)."""
     grid = config.grid
-    med = tti_medium(config.medium)
+    med = tti_medium(config.medium, grid.shape)
     d = _lib.TTIDesc()
     d.geom = _lib.geometry(grid)
     d.space_order, d.precision, d.dt, d.dt2 = config.space_order, config.precision, dt, dt ** 2
@@ -476,7 +480,9 @@ def _build_tti(config: RunConfig, dt: float, tables, x_begin: int, nx_local: int
     keep = []
 
     def local(values, what):
-        a3 = np.ascontiguousarray(np.broadcast_to(np.asarray(values, np.float64), grid.shape))
+        a3 = np.asarray(values, np.float64)
+        if a3.shape != grid.shape or not a3.flags.c_contiguous:
+            a3 = _field_op(grid.shape, lambda v: v, a3)      # threaded materialisation
         if nx_local:
             a3 = np.ascontiguousarray(a3[x_begin:x_begin + nx_local])
         keep.append(a3)

@@ -114,12 +114,43 @@ def tti_coefficients(grid: GridSpec, space_order: int):
     return d1
 
 
-def tti_axis(theta, phi):
+def _chunked(n: int, fn) -> None:
+    """fn(lo, hi) over x ranges on host threads (NumPy ufuncs release the
+    GIL; element-wise results do not depend on the chunking)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+    workers = max(1, min(16, os.cpu_count() or 1))
+    if n < 2 * workers:
+        fn(0, n)
+        return
+    edges = np.linspace(0, n, workers * 4 + 1).astype(int)
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        list(ex.map(lambda ab: fn(*ab), [(a, b) for a, b in zip(edges[:-1], edges[1:]) if b > a]))
+
+
+def _field_op(shape, fn, *inputs):
+    """out = fn(*inputs) element-wise over a grid-shaped f64 array, computed in
+    x chunks on host threads; scalar/broadcast inputs are allowed."""
+    arrs = [np.broadcast_to(np.asarray(a, dtype=np.float64), shape) for a in inputs]
+    out = np.empty(shape, dtype=np.float64)
+
+    def work(lo, hi):
+        out[lo:hi] = fn(*(a[lo:hi] for a in arrs))
+    _chunked(shape[0], work)
+    return out
+
+
+def tti_axis(theta, phi, shape=None):
     """Symmetry axis z-bar = (sin t cos p, sin t sin p, cos t) of the rotated
-    frame of PAPER.md eq. 2 (x-bar = (cos t cos p, cos t sin p, -sin t)), f64."""
+    frame of PAPER.md eq. 2 (x-bar = (cos t cos p, cos t sin p, -sin t)), f64.
+    With ``shape`` (grid shape) array inputs are evaluated on host threads."""
     th = np.asarray(theta, dtype=np.float64)
     ph = np.asarray(phi, dtype=np.float64)
-    return (np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th))
+    if shape is None or (th.ndim == 0 and ph.ndim == 0):
+        return (np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th))
+    return (_field_op(shape, lambda t, p: np.sin(t) * np.cos(p), th, ph),
+            _field_op(shape, lambda t, p: np.sin(t) * np.sin(p), th, ph),
+            _field_op(shape, lambda t: np.cos(t), th))
 
 
 @dataclass
@@ -133,20 +164,25 @@ class TTIMedium:
     axis: tuple
 
 
-def tti_medium(medium: dict) -> TTIMedium:
+def tti_medium(medium: dict, shape=None) -> TTIMedium:
+    """Host material for TTI.  With ``shape`` (grid shape), array fields are
+    evaluated in x chunks on host threads -- the same element-wise NumPy
+    operations, so the values are identical to the unchunked ones."""
     vp = medium["vp"]
     eps = medium.get("epsilon", 0.0)
     delta = medium.get("delta", 0.0)
     th, ph = medium.get("theta", 0.0), medium.get("phi", 0.0)
     if np.ndim(eps):
-        e2 = 1.0 + 2.0 * np.asarray(eps, dtype=np.float64)
+        e2 = (_field_op(shape, lambda e: 1.0 + 2.0 * e, eps) if shape is not None
+              else 1.0 + 2.0 * np.asarray(eps, dtype=np.float64))
     else:
         e2 = 1.0 + 2.0 * float(eps)
     if np.ndim(delta):
-        d2 = np.sqrt(1.0 + 2.0 * np.asarray(delta, dtype=np.float64))
+        d2 = (_field_op(shape, lambda d: np.sqrt(1.0 + 2.0 * d), delta) if shape is not None
+              else np.sqrt(1.0 + 2.0 * np.asarray(delta, dtype=np.float64)))
     else:
         d2 = math.sqrt(1.0 + 2.0 * float(delta))
-    axis = tti_axis(th, ph)
+    axis = tti_axis(th, ph, shape)
     if np.ndim(th) == 0 and np.ndim(ph) == 0:
         axis = tuple(float(c) for c in axis)
     return TTIMedium(vp, e2, d2, axis)

@@ -154,12 +154,17 @@ def test_host_helpers_match_oracle():
     rng = np.random.default_rng(1)
     shape = (6, 5, 7)
     med = _random_medium(rng, shape)
-    hm = tti_medium(med)
     m, e2, d2, axis = so.tti_medium(med)
-    np.testing.assert_array_equal(hm.e2, e2)
-    np.testing.assert_array_equal(hm.d2, d2)
-    for a in range(3):
-        np.testing.assert_array_equal(hm.axis[a], axis[a])
+    big = (40, 30, 20)                       # chunked, threaded host path
+    med_big = _random_medium(rng, big)
+    med_big["vp"] = np.broadcast_to(np.linspace(1500, 4000, 20), big)
+    for hm, ref, sh in ((tti_medium(med), (e2, d2, axis), None),
+                        (tti_medium(med_big, big), so.tti_medium(med_big)[1:], big)):
+        np.testing.assert_array_equal(hm.e2, ref[0])
+        np.testing.assert_array_equal(hm.d2, ref[1])
+        for a in range(3):
+            np.testing.assert_array_equal(hm.axis[a], ref[2][a])
+    assert medium_velocity_bounds("tti", med_big) == so.tti_vmax(med_big)
     vmax = medium_velocity_bounds("tti", med)
     assert vmax == so.tti_vmax(med)
     grid = stb.GridSpec(shape, (10.0, 12.0, 8.0), (0.0,) * 3)
