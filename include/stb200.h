@@ -230,6 +230,21 @@ int stb_prop_level_ptr(stb_prop_t p, int32_t field, int64_t t, void** dev,
  * 64), int32 nx, ny, nz, uint32 t, zero padding -- then the (nx, ny, nz)
  * C-order little-endian samples.  Device -> file without Python. */
 int stb_prop_write_snapshot(stb_prop_t p, int32_t field, int64_t t, const char* path);
+/* Asynchronous stepping for x-slab multi-GPU runs (fused acoustic path).
+ * Work is enqueued on the handle's stream (stb_prop_stream; the caller
+ * orders its halo exchange against it) with no host synchronisation:
+ *   stb_prop_async_begin(p, t0, n)           window of steps [t0, t0 + n)
+ *   stb_prop_step_async(p, t, kb, lo, hi)    kb fused steps from t over
+ *                                            local planes [lo, hi)
+ *   stb_prop_gather_async(p, t, kb)          receiver rows of levels t..t+kb-1
+ *   stb_prop_async_finish(p, rec_out, &bad)  sync, (n, nrec) traces, NaN guard
+ * Replaces the engine.py:426-434 loop when the caller interleaves the halo
+ * exchange (slabs.py); stb_prop_run is the synchronous whole-window form. */
+int stb_prop_stream(stb_prop_t p, void** stream);
+int stb_prop_async_begin(stb_prop_t p, int64_t t0, int64_t nsteps);
+int stb_prop_step_async(stb_prop_t p, int64_t t, int32_t kb, int64_t x_lo, int64_t x_hi);
+int stb_prop_gather_async(stb_prop_t p, int64_t t, int32_t kb);
+int stb_prop_async_finish(stb_prop_t p, double* rec_out, int64_t* bad_step);
 /* Zero all time levels (reuse a handle for another shot). */
 int stb_prop_reset(stb_prop_t p);
 /* Device-side timing of the last stb_prop_run (CUDA events on the launching

@@ -218,6 +218,41 @@ STB_API int stb_tti_create(const stb_tti_desc* d, stb_prop_t* out) {
   })
 }
 
+STB_API int stb_prop_stream(stb_prop_t p, void** stream) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr && stream != nullptr, STB_ERR_ARG, "NULL argument");
+    *stream = p->stream();
+  })
+}
+
+STB_API int stb_prop_async_begin(stb_prop_t p, int64_t t0, int64_t nsteps) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr, STB_ERR_ARG, "NULL handle");
+    p->async_begin(t0, nsteps);
+  })
+}
+
+STB_API int stb_prop_step_async(stb_prop_t p, int64_t t, int32_t kb, int64_t x_lo, int64_t x_hi) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr, STB_ERR_ARG, "NULL handle");
+    p->step_async(t, kb, x_lo, x_hi);
+  })
+}
+
+STB_API int stb_prop_gather_async(stb_prop_t p, int64_t t, int32_t kb) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr, STB_ERR_ARG, "NULL handle");
+    p->gather_async(t, kb);
+  })
+}
+
+STB_API int stb_prop_async_finish(stb_prop_t p, double* rec_out, int64_t* bad_step) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr, STB_ERR_ARG, "NULL handle");
+    p->async_finish(rec_out, bad_step);
+  })
+}
+
 STB_API int stb_prop_write_snapshot(stb_prop_t p, int32_t field, int64_t t, const char* path) {
   STB_GUARD({
     STB_REQUIRE(p != nullptr && path != nullptr, STB_ERR_ARG, "NULL argument");

@@ -433,6 +433,84 @@ class AcousticProp final : public stb_prop_s {
     }
   }
 
+  // ---------------------------------------------------------------- async
+  void* stream() override { return st_; }
+
+  void async_begin(int64_t t0, int64_t nsteps) override {
+    STB_REQUIRE(path_ == Path::Fused, STB_ERR_ARG, "asynchronous stepping needs the fused path");
+    STB_REQUIRE(nsteps >= 0, STB_ERR_ARG, "nsteps must be >= 0");
+    STB_REQUIRE(K_ == 0 || t0 + nsteps <= src_nt_, STB_ERR_ARG,
+                "run extends past the decomposed source series");
+    as_t0_ = t0;
+    as_n_ = nsteps;
+    as_guard_.clear();
+    for (int64_t t = t0; t < t0 + nsteps; ++t)
+      if (t > 0 && t % 32 == 0) as_guard_.push_back(t);
+    if ((int64_t)guards_.n < (int64_t)as_guard_.size() + 1) guards_.alloc(as_guard_.size() + 1);
+    guards_.zero(st_);
+    if (nrec_ && (int64_t)rec_dev_.n < nsteps * nrec_) rec_dev_.alloc(nsteps * nrec_);
+    launches_ = all_launches_ = 0;
+    updates_ = 0;
+    ensure_events(1);
+    STB_CUDA(cudaEventRecord(run_ev_[0], st_));
+    as_open_ = true;
+  }
+
+  // steps [t, t + kb) over local planes [x_lo, x_hi) (stencil + fused injection)
+  void step_async(int64_t t, int kb, int64_t x_lo, int64_t x_hi) override {
+    STB_REQUIRE(as_open_, STB_ERR_ARG, "async_begin first");
+    STB_REQUIRE(t >= as_t0_ && kb >= 1 && t + kb <= as_t0_ + as_n_, STB_ERR_ARG,
+                "steps outside the async window");
+    STB_REQUIRE(kb <= max_k_, STB_ERR_PLAN, "time_height exceeds the fused kernel's depth");
+    STB_REQUIRE(0 <= x_lo && x_lo <= x_hi && x_hi <= d_.nx, STB_ERR_ARG, "plane range");
+    if (x_hi == x_lo) return;
+    int gmask = 0;
+    int* gflag = nullptr;
+    for (size_t g = 0; g < as_guard_.size(); ++g)
+      for (int j = 0; j < kb; ++j)
+        if (as_guard_[g] == t + j) {
+          gmask |= 1 << j;
+          gflag = guards_.p + g;
+        }
+    launch_fused_range(t, kb, gflag, gmask, (int)x_lo, (int)x_hi);
+    ++launches_;
+    ++all_launches_;
+    updates_ += (int64_t)kb * (x_hi - x_lo) * d_.ny * d_.nz;
+  }
+
+  void gather_async(int64_t t, int kb) override {
+    STB_REQUIRE(as_open_, STB_ERR_ARG, "async_begin first");
+    if (!nrec_) return;
+    for (int j = 0; j < kb; ++j) {
+      double* row = rec_dev_.p + (t + j - as_t0_) * nrec_;
+      gather_kernel<T><<<g1(nrec_), 256, 0, st_>>>(lvl_[slot(t + j)].p, rec_off_.p, rec_w_.p,
+                                                   nrec_, row);
+      STB_CHECK_LAUNCH();
+      ++all_launches_;
+    }
+  }
+
+  void async_finish(double* rec_out, int64_t* bad_step) override {
+    STB_REQUIRE(as_open_, STB_ERR_ARG, "async_begin first");
+    as_open_ = false;
+    if (bad_step) *bad_step = -1;
+    STB_CUDA(cudaEventRecord(run_ev_[1], st_));
+    if (nrec_ && rec_out && as_n_) rec_dev_.download(rec_out, as_n_ * nrec_, st_);
+    std::vector<int> gh(as_guard_.size() + 1, 0);
+    if (!as_guard_.empty()) guards_.download(gh.data(), as_guard_.size(), st_);
+    STB_CUDA(cudaStreamSynchronize(st_));
+    float rm = 0.f;
+    STB_CUDA(cudaEventElapsedTime(&rm, run_ev_[0], run_ev_[1]));
+    run_ms_ = rm;
+    for (size_t i = 0; i < as_guard_.size(); ++i)
+      if (gh[i]) {
+        if (bad_step) *bad_step = as_guard_[i];
+        std::ostringstream os;
+        os << "non-finite values in field group 'u' at step " << as_guard_[i];
+        throw Error(STB_ERR_UNSTABLE, os.str());
+      }
+  }
+
   void read_field(int field, int64_t t, void* out) override {
     STB_REQUIRE(field == 0, STB_ERR_ARG, "acoustic handles have one field (u)");
     const T* src = lvl_[slot(t)].p;
@@ -607,6 +685,17 @@ class AcousticProp final : public stb_prop_s {
       FusedLauncher<R, K, kTY, kTZ, pf_for(R, K), false>::launch(st_, it->second, a, nch);
   }
 
+  void launch_fused_range(int64_t t, int kb, int* gflag, int gmask, int x_lo, int x_hi) {
+    if constexpr (sizeof(T) == 4) {
+      if (R_ == 4 && kb == 2) return launch_fused_rk<4, 2>(t, gflag, gmask, x_lo, x_hi);
+      if (R_ == 4) return launch_fused_rk<4, 1>(t, gflag, gmask, x_lo, x_hi);
+      if (R_ == 2 && kb == 2) return launch_fused_rk<2, 2>(t, gflag, gmask, x_lo, x_hi);
+      if (R_ == 2) return launch_fused_rk<2, 1>(t, gflag, gmask, x_lo, x_hi);
+      if (R_ == 6) return launch_fused_rk<6, 1>(t, gflag, gmask, x_lo, x_hi);
+      throw Error(STB_ERR_ARG, "no fused kernel for this space order");
+    }
+  }
+
   void launch_fused(int64_t t, int kb, int* gflag, int gmask) {
     if constexpr (sizeof(T) == 4) {
       if (R_ == 4 && kb == 2) return launch_fused_rk<4, 2>(t, gflag, gmask);
@@ -657,6 +746,10 @@ class AcousticProp final : public stb_prop_s {
 
   int R_ = 1;
   Dims d_{};
+  // async stepping state
+  bool as_open_ = false;
+  int64_t as_t0_ = 0, as_n_ = 0;
+  std::vector<int64_t> as_guard_;
   stb_geometry geom_{};          // GLOBAL grid geometry
   int64_t x_begin_ = 0;          // global plane of local plane 0 (x slabs)
   bool zero_lo_ = true, zero_hi_ = true;

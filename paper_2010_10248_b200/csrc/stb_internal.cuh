@@ -193,6 +193,20 @@ struct stb_prop_s {
   virtual std::string describe(int k) = 0;
   // local field shape (x slab) and element size, for host-side copies
   virtual void field_info(int64_t shape[3], int* elem_bytes) = 0;
+  // asynchronous stepping (multi-GPU x slabs): enqueue on stream() without
+  // host synchronisation; traces and guard flags stay on the device until
+  // async_finish.  Default: unsupported.
+  virtual void* stream() { return nullptr; }
+  virtual void async_begin(int64_t, int64_t) { throw_unsupported(); }
+  virtual void step_async(int64_t, int, int64_t, int64_t) { throw_unsupported(); }
+  virtual void gather_async(int64_t, int) { throw_unsupported(); }
+  virtual void async_finish(double*, int64_t*) { throw_unsupported(); }
+
+ protected:
+  [[noreturn]] static void throw_unsupported() {
+    throw stb::Error(STB_ERR_ARG, "asynchronous stepping is implemented for the fused "
+                                  "acoustic path only");
+  }
 };
 
 struct stb_support_s {

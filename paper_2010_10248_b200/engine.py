@@ -335,6 +335,27 @@ class _Prop:
                                                   out.ctypes.data_as(C.c_void_p)))
         return out
 
+    # asynchronous stepping (slabs.py; stb_prop_async_begin ... _finish)
+    def stream_ptr(self) -> int:
+        st = C.c_void_p()
+        _lib.check(_lib.lib().stb_prop_stream(self.raw, C.byref(st)))
+        return st.value or 0
+
+    def async_begin(self, t0, nsteps):
+        _lib.check(_lib.lib().stb_prop_async_begin(self.raw, t0, nsteps))
+
+    def step_async(self, t, kb, x_lo, x_hi):
+        _lib.check(_lib.lib().stb_prop_step_async(self.raw, t, kb, x_lo, x_hi))
+
+    def gather_async(self, t, kb):
+        _lib.check(_lib.lib().stb_prop_gather_async(self.raw, t, kb))
+
+    def async_finish(self, rec_out=None):
+        bad = C.c_int64(-1)
+        _lib.check(_lib.lib().stb_prop_async_finish(
+            self.raw, _lib.dptr(rec_out.reshape(-1)) if rec_out is not None else _lib.dptr(None),
+            C.byref(bad)))
+
     def write_snapshot(self, name, t, path):
         """Device field -> snapshot file (stb_prop_write_snapshot; same bytes
         as save_snapshot(path, field, t), engine.py:553-566)."""

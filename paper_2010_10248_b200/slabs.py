@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import re
 
 import numpy as np
@@ -86,6 +87,26 @@ class DeviceSlab:
 
     def run(self, t0, n, k, rec_out=None):
         self.prop.run(t0, n, k, rec_out)
+
+    # asynchronous stepping (fused acoustic path): see SlabRunner._run_async
+    def supports_async(self) -> bool:
+        return self.config.physics == "acoustic" and self.prop.describe(1).startswith(
+            "acoustic_fused")
+
+    def stream_ptr(self) -> int:
+        return self.prop.stream_ptr()
+
+    def async_begin(self, t0, n):
+        self.prop.async_begin(t0, n)
+
+    def step_async(self, t, kb, x_lo, x_hi):
+        self.prop.step_async(t, kb, x_lo, x_hi)
+
+    def gather_async(self, t, kb):
+        self.prop.gather_async(t, kb)
+
+    def async_finish(self, rec_out=None):
+        self.prop.async_finish(rec_out)
 
     def planes(self, t: int, i: int, j: int, field: int = 0):
         """torch view of local planes [i, j) of time level t (contiguous)."""
@@ -192,6 +213,9 @@ class SlabRunner:
         exchange after each block."""
         k = self.time_height
         self._acc = {}
+        if (self.world > 1 and os.environ.get("STB_SLAB_ASYNC", "1") != "0"
+                and getattr(self.dev, "supports_async", lambda: False)()):
+            return self._run_async(t0, nsteps, record)
         if self.world == 1:
             # no exchange: one device call covers every block
             rec = (np.zeros((nsteps, len(self.rec_index)), dtype=np.float64)
@@ -219,14 +243,62 @@ class SlabRunner:
                 self.exchange([t + kb - 1] + ([t + kb - 2] if kb >= 2 else []))
             t += kb
 
+    def _run_async(self, t0: int, nsteps: int, record: bool):
+        """Device-ordered stepping: nothing waits on the host inside the loop.
+
+        k = 1 (default): per step, the owned boundary planes (G each side) are
+        computed first; the NCCL exchange of their newest level runs on a side
+        stream as soon as they are done, while the interior planes compute on
+        the library's stream; the receiver gather waits for both.  Ghost
+        planes are not computed (they are overwritten by the exchange).
+        k >= 2: every held plane is computed (the fused levels consume the
+        ghost zones), then the last two levels are exchanged."""
+        import torch
+        k = self.time_height
+        main = torch.cuda.ExternalStream(self.dev.stream_ptr())
+        if not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream()
+        side = self._side
+        a_loc, b_loc, G = self.a - self.lo, self.b - self.lo, self.G
+        overlap = (k == 1 and b_loc - a_loc > 2 * G
+                   and os.environ.get("STB_SLAB_OVERLAP", "1") != "0")
+        self.dev.async_begin(t0, nsteps)
+        t = t0
+        while t < t0 + nsteps:
+            kb = min(k, t0 + nsteps - t)
+            if overlap:
+                self.dev.step_async(t, 1, a_loc, a_loc + G)
+                self.dev.step_async(t, 1, b_loc - G, b_loc)
+                ev = torch.cuda.Event()
+                ev.record(main)
+                side.wait_event(ev)
+                with torch.cuda.stream(side):
+                    self.exchange([t], sync=False)
+                self.dev.step_async(t, 1, a_loc + G, b_loc - G)
+                main.wait_stream(side)
+            else:
+                lo_c, hi_c = (a_loc, b_loc) if kb == 1 else (0, self.nl)
+                self.dev.step_async(t, kb, lo_c, hi_c)
+                with torch.cuda.stream(main):
+                    self.exchange([t + kb - 1] + ([t + kb - 2] if kb >= 2 else []), sync=False)
+            self.dev.gather_async(t, kb)
+            t += kb
+        rec = (np.zeros((nsteps, len(self.rec_index)), dtype=np.float64)
+               if record and len(self.rec_index) else None)
+        self.dev.async_finish(rec)
+        if rec is not None:
+            self._traces.append((t0, rec))
+        self._accumulate()
+
     def _accumulate(self):
         st = self.dev.stats() or {}
         for key, val in st.items():
             self._acc[key] = self._acc.get(key, 0) + val
 
-    def exchange(self, levels, fields=(0,)):
+    def exchange(self, levels, fields=(0,), sync=True):
         """Refresh ghost planes of the given time levels (and fields) from the
-        neighbours."""
+        neighbours.  sync=False: the transfers are ordered on the current CUDA
+        stream (NCCL work.wait() is a stream wait) and the host does not block."""
         import torch.distributed as dist
         ops = []
         g_lo, g_hi = self.a - self.lo, self.hi - self.b
@@ -246,7 +318,8 @@ class SlabRunner:
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
-        self.dev.synchronize()
+        if sync:
+            self.dev.synchronize()
 
     # ------------------------------------------------------------ results
     def gather_fields(self, t: int) -> dict | None:

@@ -341,3 +341,76 @@ def test_validate_flag_replays_device_plan():
         cfg.validate = True
         res_v = stb.run(cfg)
         np.testing.assert_array_equal(res.fields["u"], res_v.fields["u"])
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_xslab_async_api_emulated_two_ranks(overlap):
+    """The asynchronous slab API (stb_prop_async_begin / step_async /
+    gather_async / async_finish) in SlabRunner._run_async's order -- owned
+    boundary planes, ghost exchange, interior planes, gather -- with two slab
+    handles on one GPU and device copies in place of NCCL (two NCCL ranks must
+    not share a GPU).  Owned planes and traces equal the oracle bit for bit."""
+    import torch
+    from paper_2010_10248_b200 import slabs
+    from test_slabs_gloo import _make
+    cfg = _make("acoustic", 1)
+    ranks = [slabs.SlabRunner(cfg, r, 2) for r in range(2)]
+    assert all(rr.dev.supports_async() for rr in ranks)
+    nt = ranks[0].nt
+    lo, hi = ranks
+    g = lo.hi - lo.b
+    for rr in ranks:
+        rr.dev.async_begin(0, nt)
+    for t in range(nt):
+        for rr in ranks:
+            a_loc, b_loc = rr.a - rr.lo, rr.b - rr.lo
+            if overlap:
+                rr.dev.step_async(t, 1, a_loc, a_loc + rr.G)
+                rr.dev.step_async(t, 1, b_loc - rr.G, b_loc)
+            else:
+                rr.dev.step_async(t, 1, a_loc, b_loc)
+        torch.cuda.synchronize()
+        lo.dev.planes(t, lo.nl - g, lo.nl).copy_(hi.dev.planes(t, g, 2 * g))
+        hi.dev.planes(t, 0, g).copy_(lo.dev.planes(t, lo.nl - 2 * g, lo.nl - g))
+        torch.cuda.synchronize()
+        if overlap:
+            for rr in ranks:
+                rr.dev.step_async(t, 1, rr.a - rr.lo + rr.G, rr.b - rr.lo - rr.G)
+        for rr in ranks:
+            rr.dev.gather_async(t, 1)
+        torch.cuda.synchronize()
+    ref = so.run(cfg)
+    shape = cfg.grid.shape
+    traces = np.zeros((nt, len(cfg.receiver_coords)))
+    field = np.empty(shape, dtype=np.float32)
+    for rr in ranks:
+        rec = np.zeros((nt, len(rr.rec_index))) if len(rr.rec_index) else None
+        rr.dev.async_finish(rec)
+        if rec is not None:
+            traces[:, rr.rec_index] = rec
+        loc = rr.dev.read(nt - 1, (rr.nl,) + shape[1:], "u")
+        field[rr.a:rr.b] = loc[rr.a - rr.lo: rr.b - rr.lo]
+    np.testing.assert_array_equal(field, ref.fields["u"])
+    np.testing.assert_array_equal(traces, ref.receivers)
+
+
+def test_async_api_errors():
+    from paper_2010_10248_b200.engine import build_propagator, medium_velocity_bounds, \
+        resolve_steps
+    cfg = to_config(build_case("ac_so8_het_32"), stb)
+    vmax = medium_velocity_bounds(cfg.physics, cfg.medium)
+    dt, nt = resolve_steps(cfg, vmax)
+    prop = build_propagator(cfg, dt, vmax)
+    with pytest.raises(ValueError):
+        prop.step_async(0, 1, 0, 4)                 # no async_begin
+    prop.async_begin(0, 4)
+    with pytest.raises(ValueError):
+        prop.step_async(3, 2, 0, 4)                 # outside the window
+    with pytest.raises(ValueError):
+        prop.step_async(0, 1, 0, 10 ** 6)           # plane range
+    prop.async_finish()
+    el = to_config(build_case("el_so4_24"), stb)
+    vmax = medium_velocity_bounds(el.physics, el.medium)
+    dt, _ = resolve_steps(el, vmax)
+    with pytest.raises(ValueError):
+        build_propagator(el, dt, vmax).async_begin(0, 2)

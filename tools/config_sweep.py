@@ -33,7 +33,9 @@ def measure(so, nsrc, nrec, steps=100, k=0, arith="exact"):
           f"stencil share {st['stencil_ms']/st['run_ms']:.2f}  {r.describe()}", flush=True)
 
 import sys as _s
-if len(_s.argv) > 1 and _s.argv[1] == "k2":
+if __name__ != "__main__":
+    pass
+elif len(_s.argv) > 1 and _s.argv[1] == "k2":
     for so in (4, 8):
         for k in (1, 2):
             for ar in ("exact", "fma"):
