@@ -26,6 +26,7 @@
 #include "padded.cuh"
 #include "sparse_ops.cuh"
 #include "stb_internal.cuh"
+#include "tma.cuh"
 
 namespace stb {
 
@@ -443,6 +444,24 @@ __global__ void elastic_materials_kernel(const double* __restrict__ lam,
   }
 }
 
+}  // namespace
+}  // namespace stb
+
+#include "elastic_tiled.cuh"
+
+namespace stb {
+namespace {
+
+template <typename T>
+__global__ void el_fill_kernel(T* __restrict__ dst, PDims d, T v) {
+  const int64_t n = d.nx * d.ny * d.nz;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = i % d.nz, xy = i / d.nz;
+    dst[d.at(xy / d.ny, xy % d.ny, z)] = v;
+  }
+}
+
 template <typename T, int R>
 void launch_sweeps(cudaStream_t st, const ElArgs<T>& a) {
   if (a.cx <= 0) {
@@ -527,6 +546,11 @@ class ElasticProp final : public stb_prop_s {
     }
     cx_ = 0;   // thread-per-point kernels (x sweeps: STB_ELASTIC_CX > 0)
     if (const char* e = std::getenv("STB_ELASTIC_CX")) cx_ = std::atoi(e);
+    // TMA-tiled sweeps (elastic_tiled.cuh): f32, 3-D, R <= 4
+    tiled_ = sizeof(T) == 4 && cf_.active[0] && cf_.active[1] && cf_.active[2] && R_ <= 4 &&
+             cx_ == 0;
+    if (const char* e = std::getenv("STB_ELASTIC_PATH")) tiled_ = tiled_ && std::string(e) != "point";
+    if (tiled_) setup_tiled();
     STB_REQUIRE(d_.total < (int64_t)INT32_MAX, STB_ERR_ARG,
                 "elastic slab too large for 32-bit offsets; use more x slabs");
   }
@@ -536,6 +560,93 @@ class ElasticProp final : public stb_prop_s {
     for (auto& e : run_ev_)
       if (e) cudaEventDestroy(e);
     if (st_) cudaStreamDestroy(st_);
+  }
+
+  void setup_tiled() {
+    if constexpr (sizeof(T) == 4) {
+      auto materialise = [&](DevBuf<T>& b, T v) {
+        if (b.p) return;
+        b.alloc(d_.total);
+        b.zero(st_);
+        el_fill_kernel<T><<<1184, 256, 0, st_>>>(b.p, d_, v);
+        STB_CHECK_LAUNCH();
+      };
+      materialise(buoy_, cf_.buoy);
+      materialise(lam_, cf_.lam);
+      materialise(mu_, cf_.mu);
+      STB_CUDA(cudaStreamSynchronize(st_));
+      Dims md{};
+      md.nx = d_.nx + 2 * d_.H;
+      md.ny = d_.ny + 2 * d_.H;
+      md.nz = d_.pitch;
+      md.pitch = d_.pitch;
+      md.plane = d_.plane;
+      const uint32_t py = kElTY + 2 * R_, pz = kElTZ + 2 * ((R_ + 3) / 4 * 4);
+      for (int f = 0; f < NFIELDS; ++f)
+        fmap_[f] = make_map3d_f32(reinterpret_cast<const float*>(f_[f].p), md, pz, py, 1);
+      switch (R_) {
+        case 1: set_tiled_attr<1>(); break;
+        case 2: set_tiled_attr<2>(); break;
+        case 3: set_tiled_attr<3>(); break;
+        case 4: set_tiled_attr<4>(); break;
+        default: break;
+      }
+    }
+  }
+
+  template <int R>
+  void set_tiled_attr() {
+    STB_CUDA(cudaFuncSetAttribute(elastic_tiled<R, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ElTiledCfg<R, 6>::smem_bytes()));
+    STB_CUDA(cudaFuncSetAttribute(elastic_tiled<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)ElTiledCfg<R, 3>::smem_bytes()));
+  }
+
+  template <int R>
+  void launch_tiled_r(int* nonfinite) {
+    const int cx = 150;
+    dim3 grid((unsigned)((d_.nz + kElTZ - 1) / kElTZ), (unsigned)((d_.ny + kElTY - 1) / kElTY),
+              (unsigned)((d_.nx + cx - 1) / cx));
+    ElTiledArgs a{};
+    a.fx = reinterpret_cast<const float*>(fac_[0].p);
+    a.fy = reinterpret_cast<const float*>(fac_[1].p);
+    a.fz = reinterpret_cast<const float*>(fac_[2].p);
+    a.has_fac = has_fac_ ? 1 : 0;
+    for (int ax = 0; ax < 3; ++ax)
+      for (int j = 0; j < 8; ++j) a.cf.d1[ax][j] = (float)cf_.d1[ax][j];
+    a.d = d_;
+    a.cx = cx;
+    a.nonfinite = nonfinite;
+    // v half step: inputs txx tyy tzz txy txz tyz, updates vx vy vz
+    ElTiledMaps mv{};
+    for (int f = 0; f < 6; ++f) mv.f[f] = fmap_[TXX + f];
+    for (int f = 0; f < 3; ++f) a.out[f] = reinterpret_cast<float*>(f_[VX + f].p);
+    a.m0 = reinterpret_cast<const float*>(buoy_.p);
+    a.m1 = nullptr;
+    elastic_tiled<R, 0><<<grid, kElThreads, ElTiledCfg<R, 6>::smem_bytes(), st_>>>(mv, a);
+    STB_CHECK_LAUNCH();
+    // tau half step: inputs vx vy vz, updates the six stresses
+    ElTiledMaps mt{};
+    for (int f = 0; f < 3; ++f) mt.f[f] = fmap_[VX + f];
+    for (int f = 0; f < 6; ++f) a.out[f] = reinterpret_cast<float*>(f_[TXX + f].p);
+    a.m0 = reinterpret_cast<const float*>(lam_.p);
+    a.m1 = reinterpret_cast<const float*>(mu_.p);
+    elastic_tiled<R, 1><<<grid, kElThreads, ElTiledCfg<R, 3>::smem_bytes(), st_>>>(mt, a);
+    STB_CHECK_LAUNCH();
+  }
+
+  void launch_tiled(int* nonfinite) {
+    if constexpr (sizeof(T) == 4) {
+      switch (R_) {
+        case 1: launch_tiled_r<1>(nonfinite); break;
+        case 2: launch_tiled_r<2>(nonfinite); break;
+        case 3: launch_tiled_r<3>(nonfinite); break;
+        case 4: launch_tiled_r<4>(nonfinite); break;
+        default: throw Error(STB_ERR_ARG, "no tiled elastic kernel for this space order");
+      }
+    } else {
+      (void)nonfinite;
+    }
   }
 
   void set_sources(Support& s, const double* wav, int64_t nt_w, const double* scale,
@@ -629,7 +740,9 @@ class ElasticProp final : public stb_prop_s {
       // which flags the same blow-ups one half step later.
       A.nonfinite = guard_now ? guards.p + gi : nullptr;
       STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
-      switch (R_) {
+      if (tiled_) {
+        launch_tiled(A.nonfinite);
+      } else switch (R_) {
         case 1: launch_sweeps<T, 1>(st_, A); break;
         case 2: launch_sweeps<T, 2>(st_, A); break;
         case 3: launch_sweeps<T, 3>(st_, A); break;
@@ -724,7 +837,9 @@ class ElasticProp final : public stb_prop_s {
 
   std::string describe(int k) override {
     std::ostringstream os;
-    if (cx_ > 0)
+    if (tiled_)
+      os << "elastic_tiled<f32,R=" << R_ << "> (v + tau TMA plane rings, 16x32 tiles, x chunk 150)";
+    else if (cx_ > 0)
       os << "elastic_sweeps<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
          << "> (v + tau x-sweeps, 32x8 threads, cx=" << cx_ << ")";
     else
@@ -756,6 +871,8 @@ class ElasticProp final : public stb_prop_s {
   DevBuf<T> fac_[3];
   bool has_fac_ = false;
   int cx_ = 64;
+  bool tiled_ = false;
+  CUtensorMap fmap_[NFIELDS];
   int64_t t_next_ = 0;
   int64_t K_ = 0, src_nt_ = 0;
   DevBuf<T> series_;
