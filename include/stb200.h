@@ -210,6 +210,10 @@ int stb_prop_set_sources(stb_prop_t p, stb_support_t s, const double* wavelets,
  * must already be validated (margin = boundary_layers, engine.py:282-290). */
 int stb_prop_set_receivers(stb_prop_t p, const double* coords, int64_t nrec);
 
+/* Field the receivers record (same indices as stb_prop_read_field).  Default
+ * = the reference's: acoustic u, elastic txx (engine.py:327-332), TTI p.
+ * Extension for BASELINE cfg5 (vx / vz receivers). */
+int stb_prop_set_receiver_field(stb_prop_t p, int32_t field);
 /* Advance steps [t0, t0 + nsteps), time_height steps fused per HBM pass
  * (schedule.py:171-207 semantics; 0 = library default).  rec_out, when not
  * NULL, receives the (nsteps, nrec) f64 traces.  On a non-finite field at a

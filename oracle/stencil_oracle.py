@@ -798,6 +798,14 @@ def run(cfg, threads: int = 1, steps: int | None = None, keep_support=False) -> 
     else:
         raise ValueError(f"oracle has no physics {cfg.physics!r}")
     R = model.R
+    rfield = getattr(cfg, "receiver_field", None)
+    if rfield is not None:
+        # extension: record another field after injection,
+        # mirroring engine.py:327-332's record-after-inject order
+        if cfg.physics == "elastic":
+            gather_from = lambda t: model.lv(rfield, t)
+        elif cfg.physics == "tti":
+            gather_from = lambda t: model.lv(rfield, t)
 
     # sources (engine.py:258-279)
     sup = dcmp = None

@@ -218,6 +218,13 @@ STB_API int stb_tti_create(const stb_tti_desc* d, stb_prop_t* out) {
   })
 }
 
+STB_API int stb_prop_set_receiver_field(stb_prop_t p, int32_t field) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr, STB_ERR_ARG, "NULL handle");
+    p->set_receiver_field(field);
+  })
+}
+
 STB_API int stb_prop_stream(stb_prop_t p, void** stream) {
   STB_GUARD({
     STB_REQUIRE(p != nullptr && stream != nullptr, STB_ERR_ARG, "NULL argument");

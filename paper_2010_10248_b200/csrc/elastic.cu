@@ -680,6 +680,11 @@ class ElasticProp final : public stb_prop_s {
     STB_CUDA(cudaStreamSynchronize(st_));
   }
 
+  void set_receiver_field(int field) override {
+    STB_REQUIRE(field >= 0 && field < NFIELDS, STB_ERR_ARG, "elastic field index in [0, 9)");
+    rec_field_ = field;
+  }
+
   void set_receivers(const double* coords, int64_t nrec) override {
     nrec_ = nrec;
     if (nrec == 0) return;
@@ -765,7 +770,7 @@ class ElasticProp final : public stb_prop_s {
         all_launches_ += 3;
       }
       if (nrec_) {
-        gather_kernel<T><<<g1(nrec_), 256, 0, st_>>>(f_[TXX].p, rec_off_.p, rec_w_.p, nrec_,
+        gather_kernel<T><<<g1(nrec_), 256, 0, st_>>>(f_[rec_field_].p, rec_off_.p, rec_w_.p, nrec_,
                                                      rec_dev_.p + (t - t0) * nrec_);
         STB_CHECK_LAUNCH();
         ++all_launches_;
@@ -872,6 +877,7 @@ class ElasticProp final : public stb_prop_s {
   bool has_fac_ = false;
   int cx_ = 64;
   bool tiled_ = false;
+  int rec_field_ = TXX;      // engine.py:327-332 records txx
   CUtensorMap fmap_[NFIELDS];
   int64_t t_next_ = 0;
   int64_t K_ = 0, src_nt_ = 0;

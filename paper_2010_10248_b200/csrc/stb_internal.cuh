@@ -184,6 +184,10 @@ struct stb_prop_s {
   virtual void set_sources(stb::Support& s, const double* wav, int64_t nt_w,
                            const double* scale, int64_t nt) = 0;
   virtual void set_receivers(const double* coords, int64_t nrec) = 0;
+  // field the receivers record (default: the reference's -- u / txx / p)
+  virtual void set_receiver_field(int field) {
+    STB_REQUIRE(field == 0, STB_ERR_ARG, "this handle records field 0 only");
+  }
   virtual void run(int64_t t0, int64_t nsteps, int k, double* rec_out, int64_t* bad_step) = 0;
   virtual void read_field(int field, int64_t t, void* out) = 0;
   virtual void level_ptr(int field, int64_t t, void** dev, int64_t* plane, int64_t* pitch) = 0;

@@ -345,6 +345,11 @@ class TtiProp final : public stb_prop_s {
     STB_CUDA(cudaStreamSynchronize(st_));
   }
 
+  void set_receiver_field(int field) override {
+    STB_REQUIRE(field == 0 || field == 1, STB_ERR_ARG, "TTI field index: 0 = p, 1 = q");
+    rec_field_ = field;
+  }
+
   void set_receivers(const double* coords, int64_t nrec) override {
     nrec_ = nrec;
     if (nrec == 0) return;
@@ -431,7 +436,7 @@ class TtiProp final : public stb_prop_s {
         all_launches_ += 2;
       }
       if (nrec_) {
-        gather_kernel<T><<<g1t(nrec_), 256, 0, st_>>>(lv_[0][cur].p, rec_off_.p, rec_w_.p, nrec_,
+        gather_kernel<T><<<g1t(nrec_), 256, 0, st_>>>(lv_[rec_field_][cur].p, rec_off_.p, rec_w_.p, nrec_,
                                                       rec_dev_.p + (t - t0) * nrec_);
         STB_CHECK_LAUNCH();
         ++all_launches_;
@@ -606,6 +611,7 @@ class TtiProp final : public stb_prop_s {
 
   int r_ = 1;
   bool fused_ = false;
+  int rec_field_ = 0;        // p
   int cx_ = 150;
   TtiMaps maps_[2];           // [level buffer] p/q tensor maps (fused path)
   PDims d_{};

@@ -39,6 +39,9 @@ SNAPSHOT_HEADER = struct.Struct("<8sIiiiI")
 SNAPSHOT_HEADER_SIZE = 32
 
 SCHEDULE_KINDS = ("naive", "space", "wavefront", "gpu")
+_FIELD_NAMES = {"acoustic": ("u",),
+                "elastic": ("vx", "vy", "vz", "txx", "tyy", "tzz", "txy", "txz", "tyz"),
+                "tti": ("p", "q")}
 PHYSICS = ("acoustic", "elastic", "tti")
 
 
@@ -94,6 +97,7 @@ class RunConfig:
     threads: int = 1
     damping_decay: float | None = None
     validate: bool = False
+    receiver_field: str | None = None   # extension (cfg5 vx/vz); None = u / txx / p
 
     def __post_init__(self):
         if self.physics not in PHYSICS:
@@ -115,6 +119,10 @@ class RunConfig:
         if self.receiver_coords is not None:
             self.receiver_coords = np.atleast_2d(np.asarray(self.receiver_coords,
                                                             dtype=np.float64))
+        if self.receiver_field is not None and self.receiver_field not in _FIELD_NAMES[
+                self.physics]:
+            raise ConfigError("receiver_field", f"{self.physics} fields are "
+                              f"{_FIELD_NAMES[self.physics]}, got {self.receiver_field!r}")
 
     @property
     def dtype(self):
@@ -322,6 +330,9 @@ class _Prop:
         c = np.ascontiguousarray(coords, dtype=np.float64)
         _lib.check(_lib.lib().stb_prop_set_receivers(self.raw, _lib.dptr(c.reshape(-1)),
                                                      c.shape[0]))
+
+    def set_receiver_field(self, name):
+        _lib.check(_lib.lib().stb_prop_set_receiver_field(self.raw, self.fields.index(name)))
 
     def run(self, t0, nsteps, k, rec_out=None):
         bad = C.c_int64(-1)
@@ -602,6 +613,8 @@ def run(config: RunConfig) -> RunResult:
         validate_coords_in_extent(rc, grid, margin_points=grid.boundary_layers,
                                   what="receiver")
         prop.set_receivers(rc)
+        if config.receiver_field is not None:
+            prop.set_receiver_field(config.receiver_field)
         nrec = rc.shape[0]
         rec = np.zeros((nt, nrec), dtype=np.float64)
     precompute_s = time.perf_counter() - t_pre0

@@ -83,6 +83,8 @@ class DeviceSlab:
 
     def set_receivers(self, coords):
         self.prop.set_receivers(coords)
+        if getattr(self.config, "receiver_field", None) is not None:
+            self.prop.set_receiver_field(self.config.receiver_field)
         self.nrec = len(coords)
 
     def run(self, t0, n, k, rec_out=None):

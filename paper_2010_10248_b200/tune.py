@@ -162,6 +162,7 @@ def parse_config(doc: dict, seed: int | None = None) -> RunConfig:
     rdoc = _field(doc, "receivers")
     receivers = (np.asarray(_field(rdoc, "coords_m", "receivers", required=True),
                             dtype=np.float64) if rdoc else None)
+    rfield = _field(rdoc, "field", "receivers") if rdoc else None
     dt_ms = _field(doc, "dt_ms")
     decay = _field(doc, "damping_decay_per_s")
     try:
@@ -173,7 +174,8 @@ def parse_config(doc: dict, seed: int | None = None) -> RunConfig:
                          precision=int(_field(doc, "precision", default=32)),
                          threads=int(_field(doc, "threads", default=_env_threads())),
                          damping_decay=None if decay is None else float(decay),
-                         validate=bool(_field(doc, "validate", default=False)))
+                         validate=bool(_field(doc, "validate", default=False)),
+                         receiver_field=rfield)
     except ConfigError:
         raise
     except (TypeError, ValueError) as exc:

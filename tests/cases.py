@@ -121,6 +121,17 @@ def build_case(name: str) -> dict:
         c["src"] = dict(coords=[[640.3, 640.7, 200.5]], f0=10.0)
         c["receivers"] = np.stack([np.linspace(0.0, 1270.0, 101), np.full(101, 640.0),
                                    np.full(101, 20.0)], axis=1)
+    elif name == "el_cfg5_48":
+        # BASELINE cfg5 generators at 48^3 (vp in [2, 4] km/s smooth,
+        # vs = vp/1.7, rho in [1800, 2500] smooth, explosive 12 Hz Ricker,
+        # receivers on a line recording vx / vz via RunConfig.receiver_field)
+        shape, h = (48, 48, 48), (10.0,) * 3
+        vp = _smooth_field(rng, shape, 2000.0, 4000.0)
+        c.update(physics="elastic", shape=shape, spacing=h, bl=6, so=8, nt=24, dt=0.5e-3,
+                 medium=dict(vp=vp, vs=vp / 1.7, rho=_smooth_field(rng, shape, 1800.0, 2500.0)))
+        c["src"] = dict(coords=[[235.0, 236.5, 150.0]], f0=12.0)
+        c["receivers"] = np.stack([np.linspace(80.0, 390.0, 32), np.full(32, 235.0),
+                                   np.full(32, 80.0)], axis=1)
     elif name.startswith("tti_"):
         c.update(_tti_case(name, rng))
     else:
@@ -226,7 +237,8 @@ def to_config(case: dict, mod=None, **overrides):
                                medium=c["medium"], nt=c["nt"], time_ms=None, dt=c["dt"],
                                cfl_safety=0.9, sources=sources,
                                receiver_coords=c.get("receivers"), precision=c["precision"],
-                               damping_decay=c["damping_decay"])
+                               damping_decay=c["damping_decay"],
+                               receiver_field=c.get("receiver_field"))
     grid = mod.GridSpec(tuple(c["shape"]), tuple(c["spacing"]), tuple(c["origin"]),
                         boundary_layers=c["bl"])
     sources = None
@@ -238,6 +250,8 @@ def to_config(case: dict, mod=None, **overrides):
               medium=c["medium"], dt=c["dt"], sources=sources,
               receiver_coords=c.get("receivers"), precision=c["precision"],
               damping_decay=c["damping_decay"])
+    if c.get("receiver_field") is not None:
+        kw["receiver_field"] = c["receiver_field"]
     if "schedule" in c:
         kw["schedule"] = c["schedule"]
     return mod.RunConfig(**kw)

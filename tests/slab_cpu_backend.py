@@ -92,6 +92,7 @@ class OracleSlab:
         R = self.R
         targets = ("txx", "tyy", "tzz") if self.elastic else ("p", "q") if self.tti else ("u",)
         gather = "txx" if self.elastic else "p" if self.tti else "u"
+        gather = getattr(self.config, "receiver_field", None) or gather
         for t in range(t0, t0 + n):
             self.model.step(t)
             if self.pts is not None and len(self.pts):

@@ -414,3 +414,17 @@ def test_async_api_errors():
     dt, _ = resolve_steps(el, vmax)
     with pytest.raises(ValueError):
         build_propagator(el, dt, vmax).async_begin(0, 2)
+
+
+@pytest.mark.parametrize("field", [None, "vx", "vz"])
+def test_elastic_cfg5_receiver_fields(field):
+    """BASELINE cfg5 (elastic, vx/vz receivers) generators at 48^3: traces of
+    the selected field (RunConfig.receiver_field extension) and all nine
+    fields bit-exact vs the oracle; None records txx like the reference."""
+    case = dict(build_case("el_cfg5_48"), receiver_field=field)
+    res = stb.run(to_config(case, stb))
+    ref = so.run(to_config(case))
+    for k, v in ref.fields.items():
+        np.testing.assert_array_equal(res.fields[k], v, err_msg=k)
+    np.testing.assert_array_equal(res.receivers, ref.receivers)
+    assert np.abs(res.receivers).max() > 0

@@ -157,3 +157,14 @@ def test_arithmetic_intensity_formula():
         "acoustic", 4, 32)
     assert engine.arithmetic_intensity("acoustic", 4, 32) == pytest.approx(
         2 * engine.arithmetic_intensity("acoustic", 4, 64))
+
+
+def test_receiver_field_validation():
+    g = stb.GridSpec((8, 8, 8), (10.0,) * 3)
+    with pytest.raises(stb.ConfigError) as e:
+        stb.RunConfig(physics="acoustic", grid=g, space_order=4, nt=2,
+                      medium={"velocity": 2000.0}, receiver_field="vx")
+    assert e.value.field == "receiver_field"
+    cfg = stb.RunConfig(physics="elastic", grid=g, space_order=4, nt=2,
+                        medium={"vp": 3000.0, "vs": 1700.0, "rho": 2000.0}, receiver_field="vz")
+    assert cfg.receiver_field == "vz"

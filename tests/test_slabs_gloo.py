@@ -70,6 +70,10 @@ def _tti_case():
 def _make(kind, k):
     if kind == "tti":
         return _tti_case()
+    if kind == "elastic_vz":
+        cfg = _elastic_case()
+        cfg.receiver_field = "vz"
+        return cfg
     return _elastic_case() if kind == "elastic" else _case(k)
 
 
@@ -89,7 +93,8 @@ def _worker(rank, world, port, k, out_path, kind="acoustic"):
 
 @pytest.mark.parametrize("kind,world,k", [("acoustic", 2, 1), ("acoustic", 2, 2),
                                           ("acoustic", 3, 1), ("elastic", 2, 1),
-                                          ("elastic", 3, 1), ("tti", 2, 1), ("tti", 3, 1)])
+                                          ("elastic", 3, 1), ("elastic_vz", 2, 1),
+                                          ("tti", 2, 1), ("tti", 3, 1)])
 def test_xslab_matches_single_domain(kind, world, k, tmp_path):
     from oracle import stencil_oracle as so
     out = str(tmp_path / "res.npz")
