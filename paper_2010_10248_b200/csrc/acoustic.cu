@@ -141,6 +141,34 @@ __global__ void tile_fill_kernel(const int64_t* __restrict__ keys, int64_t K, Di
       }
 }
 
+// Per-thread source lists for the fused kernel of depth K: entry e of the
+// per-tile list (tile-major, x-ordered within a tile) goes to the consumer
+// thread (row, g) of that K's extended tile that owns its (y, z) point;
+// key = tile * nwork + row * g1 + g (INT_MAX: outside), value {x, id*4 + zz}.
+__global__ void thr_key_kernel(const int4* __restrict__ list, const int* __restrict__ tile_ptr,
+                               int ntiles, int64_t n, int ntz, int TY, int TZ, int hy1, int hz1,
+                               int hy1_rows, int g1, int* __restrict__ key,
+                               int2* __restrict__ val) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int lo = 0, hi = ntiles;                      // tile of entry i: last t with ptr[t] <= i
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    if (tile_ptr[mid] <= i) lo = mid; else hi = mid;
+  }
+  const int t = lo;
+  const int4 e = list[i];
+  const int y0 = (t / ntz) * TY, z0 = (t % ntz) * TZ;
+  const int row = e.y - (y0 - hy1), dz = e.z - (z0 - hz1);
+  if (row < 0 || row >= hy1_rows || dz < 0 || dz >= 4 * g1) {
+    key[i] = INT_MAX;
+    val[i] = make_int2(0, 0);
+    return;
+  }
+  key[i] = t * (hy1_rows * g1) + row * g1 + dz / 4;
+  val[i] = make_int2(e.x, e.w * 4 + (dz & 3));
+}
+
 __global__ void tile_ptr_kernel(const int* __restrict__ tkey, int64_t n, int ntiles,
                                 int* __restrict__ ptr) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -306,6 +334,43 @@ class AcousticProp final : public stb_prop_s {
     tile_ptr_kernel<<<g1(ntiles + 1), 256, 0, st_>>>(tkey2.p, n, ntiles, src_tile_ptr_.p);
     STB_CHECK_LAUNCH();
     STB_CUDA(cudaStreamSynchronize(st_));
+    src_n_ = n;
+    thr_.clear();
+  }
+
+  // Per-thread lists for the fused kernel <R, K> (built on first use).
+  struct ThrLists {
+    DevBuf<int> ptr;     // ntiles * nwork + 1
+    DevBuf<int2> list;
+  };
+  template <int R, int K>
+  const ThrLists* thr_lists() {
+    if (!K_ || src_n_ == 0) return nullptr;
+    auto it = thr_.find(K);
+    if (it != thr_.end()) return it->second.get();
+    using C = FusedCfg<R, K, kTY, kTZ, pf_for(R, K)>;
+    const int nty = (int)((d_.ny + kTY - 1) / kTY), ntz = (int)((d_.nz + kTZ - 1) / kTZ);
+    const int ntiles = nty * ntz;
+    const int64_t n = src_n_;
+    DevBuf<int> key(n), key2(n);
+    DevBuf<int2> val(n);
+    auto L = std::make_unique<ThrLists>();
+    L->list.alloc(n);
+    thr_key_kernel<<<g1(n), 256, 0, st_>>>(src_list_.p, src_tile_ptr_.p, ntiles, n, ntz, kTY,
+                                           kTZ, C::hy(1), C::hz(1), C::HY1, C::G1, key.p, val.p);
+    STB_CHECK_LAUNCH();
+    size_t tb = 0;
+    STB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, val.p, L->list.p,
+                                             (int)n, 0, 32, st_));
+    DevBuf<uint8_t> tmp(tb);
+    STB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key2.p, val.p, L->list.p,
+                                             (int)n, 0, 32, st_));
+    const int nk = ntiles * C::NWORK;
+    L->ptr.alloc(nk + 1);
+    tile_ptr_kernel<<<g1(nk + 1), 256, 0, st_>>>(key2.p, n, nk, L->ptr.p);
+    STB_CHECK_LAUNCH();
+    STB_CUDA(cudaStreamSynchronize(st_));
+    return thr_.emplace(K, std::move(L)).first->second.get();
   }
 
   void set_receivers(const double* coords, int64_t nrec) override {
@@ -670,9 +735,9 @@ class AcousticProp final : public stb_prop_s {
     a.zero_hi = zero_hi_ ? 1 : 0;
     a.t0 = (int)t;
     if (K_) {
-      a.src_plane = src_plane_.p;
-      a.src_list = src_list_.p;
-      a.src_tile_ptr = src_tile_ptr_.p;
+      const ThrLists* tl = thr_lists<R, K>();
+      a.thr_ptr = tl ? tl->ptr.p : nullptr;
+      a.thr_list = tl ? tl->list.p : nullptr;
       a.series = reinterpret_cast<const float*>(series_.p);
       a.n_src = (int)K_;
     }
@@ -779,6 +844,8 @@ class AcousticProp final : public stb_prop_s {
   DevBuf<int64_t> src_keys_;
   DevBuf<int4> src_list_;
   DevBuf<int> src_tile_ptr_;
+  int64_t src_n_ = 0;
+  std::map<int, std::unique_ptr<ThrLists>> thr_;
   // receivers
   int64_t nrec_ = 0;
   DevBuf<int64_t> rec_off_;

@@ -98,9 +98,8 @@ struct FusedArgs {
   int x_lo, x_hi;        // planes swept by this launch: [x_lo, x_hi) in cx_len chunks
   int zero_lo, zero_hi;  // planes < 0 / >= nx are the reference's zero halo
   int t0;                // time step of level 1
-  const int* src_plane;  // per-plane count of affected points
-  const int4* src_list;  // per-tile {x, y, z, id} sorted by x
-  const int* src_tile_ptr;
+  const int* thr_ptr;    // per (tile, consumer thread): range in thr_list
+  const int2* thr_list;  // {x, id*4 + z lane}, x ascending per thread
   const float* series;   // (nt, n_src), pre-rounded to fp32
   int n_src;
   int* nonfinite;
@@ -314,30 +313,51 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
   const int off1 = row * C::WZ1 + 4 * g;
   int bad = 0;
 
-  // Per-level cursors into this tile's source list, with the plane of the
-  // next entry cached in a register so planes without sources cost one
-  // compare (no load on the critical path).  Uniform across the CTA.
-  int cur[K + 1], next_x[K + 1];
+  // Fused injection: each consumer thread walks its own entry list (the
+  // points of its 4 z lanes, x ascending) with a two-entry window per level
+  // whose series values are loaded when the entry enters the window -- a
+  // plane without an entry for this thread costs one register compare, and
+  // consuming an entry never waits on memory (the next one, possibly on the
+  // very next plane, is already in the window).
   int e_end = 0;
-  const bool has_src = a.src_list != nullptr;
+  int cur[K];
+  int wk[K][2];          // (x << 2) | z lane of the two window entries per level
+  float wv[K][2];        // their series values
+  const bool has_src = a.thr_list != nullptr && work;
+  auto fetch = [&](int j, int c, int& k, float& v) {
+    if (c < e_end) {
+      const int2 e = __ldg(a.thr_list + c);
+      k = (e.x << 2) | (e.y & 3);
+      v = __ldg(a.series + (size_t)(a.t0 + j - 1) * a.n_src + (e.y >> 2));
+    } else {
+      k = 0x7fffffff;
+      v = 0.f;
+    }
+  };
 #pragma unroll
-  for (int j = 0; j <= K; ++j) {
+  for (int j = 0; j < K; ++j) {
     cur[j] = 0;
-    next_x[j] = 0x7fffffff;
+    wk[j][0] = wk[j][1] = 0x7fffffff;
+    wv[j][0] = wv[j][1] = 0.f;
   }
   if (has_src) {
-    const int e_beg = __ldg(a.src_tile_ptr + tile);
-    e_end = __ldg(a.src_tile_ptr + tile + 1);
-    const int first = e_beg < e_end ? __ldg(&a.src_list[e_beg].x) : 0x7fffffff;
+    const int base = tile * C::NWORK + tid;
+    const int c0 = __ldg(a.thr_ptr + base);
+    e_end = __ldg(a.thr_ptr + base + 1);
 #pragma unroll
-    for (int j = 0; j <= K; ++j) {
-      cur[j] = e_beg;
-      next_x[j] = first;
+    for (int j = 1; j <= K; ++j) {
+      // level j first computes plane x0 - (K - j) R: skip earlier entries
+      const int pfirst = x0 - (K - j) * R;
+      int c = c0;
+      while (c < e_end && __ldg(&a.thr_list[c].x) < pfirst) ++c;
+      fetch(j, c, wk[j - 1][0], wv[j - 1][0]);
+      fetch(j, c + 1, wk[j - 1][1], wv[j - 1][1]);
+      cur[j - 1] = c + 2;
     }
   }
 
   // guard (before injection, as the reference's NaN check sees the stencil
-  // result) then fused injection from this tile's entry list
+  // result) then fused injection from this thread's entry window
   auto sparse_epilogue = [&](float (&o)[4], int j, int p, bool active) {
     if constexpr (GUARD) {
       if (a.guard_mask & (1 << (j - 1))) {
@@ -348,22 +368,17 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
         }
       }
     }
-    if (next_x[j] <= p) {              // rare: this plane (or a skipped one) has entries
-      int c = cur[j];
-      while (c < e_end) {
-        const int4 e = __ldg(&a.src_list[c]);
-        if (e.x > p) break;
-        const int zz = e.z - z;
-        if (e.x == p && active && e.y == y && zz >= 0 && zz < 4) {
-          const float v = __ldg(a.series + (size_t)(a.t0 + j - 1) * a.n_src + e.w);
+    while ((wk[j - 1][0] >> 2) == p) {   // rare: an entry of this thread on this plane
+      if (active) {
+        const int lane = wk[j - 1][0] & 3;
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (i == zz) o[i] = __fadd_rn(o[i], v);
-        }
-        ++c;
+        for (int i = 0; i < 4; ++i)
+          if (i == lane) o[i] = __fadd_rn(o[i], wv[j - 1][0]);
       }
-      cur[j] = c;
-      next_x[j] = c < e_end ? __ldg(&a.src_list[c].x) : 0x7fffffff;
+      wk[j - 1][0] = wk[j - 1][1];
+      wv[j - 1][0] = wv[j - 1][1];
+      fetch(j, cur[j - 1], wk[j - 1][1], wv[j - 1][1]);
+      ++cur[j - 1];
     }
   };
 
