@@ -205,7 +205,7 @@ __device__ __forceinline__ void update4(const float (&xq)[Q][4], const int cs, c
 }
 
 template <int R, int K, int TY, int TZ, int PF, bool FAST, bool GUARD>
-__global__ void __launch_bounds__(FusedCfg<R, K, TY, TZ, PF>::NT, ((K == 1 && R < 6) || (K > 1 && R <= 2) ? 2 : 1))
+__global__ void __launch_bounds__(FusedCfg<R, K, TY, TZ, PF>::NT, (K == 1 || R <= 2 ? 2 : 1))
 acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ FusedArgs a) {
   using C = FusedCfg<R, K, TY, TZ, PF>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
