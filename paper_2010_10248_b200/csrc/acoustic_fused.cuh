@@ -319,10 +319,12 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
   // plane without an entry for this thread costs one register compare, and
   // consuming an entry never waits on memory (the next one, possibly on the
   // very next plane, is already in the window).
+  // window depth: two entries, one at R = 6 (register budget of 2 CTAs/SM)
+  constexpr int W = R >= 6 ? 1 : 2;
   int e_end = 0;
   int cur[K];
-  int wk[K][2];          // (x << 2) | z lane of the two window entries per level
-  float wv[K][2];        // their series values
+  int wk[K][W];          // (x << 2) | z lane of the window entries per level
+  float wv[K][W];        // their series values
   const bool has_src = a.thr_list != nullptr && work;
   auto fetch = [&](int j, int c, int& k, float& v) {
     if (c < e_end) {
@@ -337,8 +339,11 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     cur[j] = 0;
-    wk[j][0] = wk[j][1] = 0x7fffffff;
-    wv[j][0] = wv[j][1] = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      wk[j][w] = 0x7fffffff;
+      wv[j][w] = 0.f;
+    }
   }
   if (has_src) {
     const int base = tile * C::NWORK + tid;
@@ -350,9 +355,9 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
       const int pfirst = x0 - (K - j) * R;
       int c = c0;
       while (c < e_end && __ldg(&a.thr_list[c].x) < pfirst) ++c;
-      fetch(j, c, wk[j - 1][0], wv[j - 1][0]);
-      fetch(j, c + 1, wk[j - 1][1], wv[j - 1][1]);
-      cur[j - 1] = c + 2;
+#pragma unroll
+      for (int w = 0; w < W; ++w) fetch(j, c + w, wk[j - 1][w], wv[j - 1][w]);
+      cur[j - 1] = c + W;
     }
   }
 
@@ -375,9 +380,12 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
         for (int i = 0; i < 4; ++i)
           if (i == lane) o[i] = __fadd_rn(o[i], wv[j - 1][0]);
       }
-      wk[j - 1][0] = wk[j - 1][1];
-      wv[j - 1][0] = wv[j - 1][1];
-      fetch(j, cur[j - 1], wk[j - 1][1], wv[j - 1][1]);
+#pragma unroll
+      for (int w = 0; w + 1 < W; ++w) {
+        wk[j - 1][w] = wk[j - 1][w + 1];
+        wv[j - 1][w] = wv[j - 1][w + 1];
+      }
+      fetch(j, cur[j - 1], wk[j - 1][W - 1], wv[j - 1][W - 1]);
       ++cur[j - 1];
     }
   };
