@@ -319,8 +319,8 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
   // plane without an entry for this thread costs one register compare, and
   // consuming an entry never waits on memory (the next one, possibly on the
   // very next plane, is already in the window).
-  // window depth: two entries, one at R = 6 (register budget of 2 CTAs/SM)
-  constexpr int W = R >= 6 ? 1 : 2;
+  // window depth: two entries; one at R = 6 and for K >= 2 (register budget)
+  constexpr int W = (R >= 6 || K >= 2) ? 1 : 2;
   int e_end = 0;
   int cur[K];
   int wk[K][W];          // (x << 2) | z lane of the window entries per level
