@@ -516,7 +516,8 @@ class AcousticProp final : public stb_prop_s {
     if (nrec_ && (int64_t)rec_dev_.n < nsteps * nrec_) rec_dev_.alloc(nsteps * nrec_);
     launches_ = all_launches_ = 0;
     updates_ = 0;
-    ensure_events(1);
+    // up to three ranged launches per step (boundary, boundary, interior)
+    ensure_events(3 * nsteps + 1);
     STB_CUDA(cudaEventRecord(run_ev_[0], st_));
     as_open_ = true;
   }
@@ -537,7 +538,11 @@ class AcousticProp final : public stb_prop_s {
           gmask |= 1 << j;
           gflag = guards_.p + g;
         }
+    STB_REQUIRE(2 * launches_ + 1 < (int64_t)events_.size(), STB_ERR_ARG,
+                "more than three launches per step in the async window");
+    STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
     launch_fused_range(t, kb, gflag, gmask, (int)x_lo, (int)x_hi);
+    STB_CUDA(cudaEventRecord(events_[2 * launches_ + 1], st_));
     ++launches_;
     ++all_launches_;
     updates_ += (int64_t)kb * (x_hi - x_lo) * d_.ny * d_.nz;

@@ -302,24 +302,40 @@ class SlabRunner:
         neighbours.  sync=False: the transfers are ordered on the current CUDA
         stream (NCCL work.wait() is a stream wait) and the host does not block."""
         import torch.distributed as dist
-        ops = []
+        ops, unstage = [], []
         g_lo, g_hi = self.a - self.lo, self.hi - self.b
+        # gloo moves host tensors only: device planes are staged through host
+        # copies (test path: two processes on one GPU, no kernel waits on a
+        # peer); NCCL sends and receives the device planes directly.
+        staged = dist.get_backend(self.group) == "gloo"
+
+        def send(t, i, j, f, peer):
+            v = self.dev.planes(t, i, j, f)
+            if staged and v.is_cuda:
+                v = v.cpu()
+            ops.append(dist.P2POp(dist.isend, v, peer, group=self.group))
+
+        def recv(t, i, j, f, peer):
+            v = self.dev.planes(t, i, j, f)
+            if staged and v.is_cuda:
+                buf = v.new_empty(v.shape, device="cpu")
+                unstage.append((v, buf))
+                v = buf
+            ops.append(dist.P2POp(dist.irecv, v, peer, group=self.group))
+
         for t in levels:
             for f in fields:
-                pl = lambda i, j: self.dev.planes(t, i, j, f)   # noqa: E731
                 if self.rank > 0:
-                    ops.append(dist.P2POp(dist.isend, pl(g_lo, g_lo + g_lo), self.rank - 1,
-                                          group=self.group))
-                    ops.append(dist.P2POp(dist.irecv, pl(0, g_lo), self.rank - 1,
-                                          group=self.group))
+                    send(t, g_lo, g_lo + g_lo, f, self.rank - 1)
+                    recv(t, 0, g_lo, f, self.rank - 1)
                 if self.rank < self.world - 1:
-                    ops.append(dist.P2POp(dist.isend, pl(self.nl - g_hi - g_hi, self.nl - g_hi),
-                                          self.rank + 1, group=self.group))
-                    ops.append(dist.P2POp(dist.irecv, pl(self.nl - g_hi, self.nl),
-                                          self.rank + 1, group=self.group))
+                    send(t, self.nl - g_hi - g_hi, self.nl - g_hi, f, self.rank + 1)
+                    recv(t, self.nl - g_hi, self.nl, f, self.rank + 1)
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        for dev_view, buf in unstage:
+            dev_view.copy_(buf)
         if sync:
             self.dev.synchronize()
 
