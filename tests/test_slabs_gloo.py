@@ -125,20 +125,23 @@ def test_partition_and_ghosts():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k,overlap", [(1, "1"), (1, "0"), (2, "1")])
-def test_xslab_async_device_two_processes_gloo(k, overlap, tmp_path):
+@pytest.mark.parametrize("kind,k,overlap", [("acoustic", 1, "1"), ("acoustic", 1, "0"),
+                                            ("acoustic", 2, "1"), ("elastic", 1, "1"),
+                                            ("elastic_vz", 1, "1"), ("tti", 1, "1")])
+def test_xslab_async_device_two_processes_gloo(kind, k, overlap, tmp_path):
     """The multi-rank device path end to end -- DeviceSlab handles, the
-    asynchronous loop (library stream, side stream, events, boundary /
+    asynchronous loop (acoustic) or the per-block loop (elastic, TTI) (library stream, side stream, events, boundary /
     interior split, async gather), result gathering -- with two processes on
     one GPU.  gloo stages ghost planes through host memory, so no kernel waits
     on a peer (NCCL P2P kernels would; they need one GPU per rank).  Fields
     and traces equal the oracle bit for bit."""
     from oracle import stencil_oracle as so
     out = str(tmp_path / "res.npz")
-    mp.start_processes(_worker, args=(2, _free_port(), k, out, "acoustic", True,
+    mp.start_processes(_worker, args=(2, _free_port(), k, out, kind, True,
                                       {"STB_SLAB_OVERLAP": overlap}),
                        nprocs=2, join=True, start_method="spawn")
     got = np.load(out)
-    ref = so.run(_make("acoustic", k))
-    np.testing.assert_array_equal(got["u"], ref.fields["u"])
+    ref = so.run(_make(kind, k))
+    for name, arr in ref.fields.items():
+        np.testing.assert_array_equal(got[name], arr, err_msg=name)
     np.testing.assert_array_equal(got["traces"], ref.receivers)
