@@ -404,6 +404,7 @@ class AcousticProp final : public stb_prop_s {
     STB_REQUIRE(k >= 0, STB_ERR_PLAN, "time_height must be >= 1");
     STB_REQUIRE(K_ == 0 || t0 + nsteps <= src_nt_, STB_ERR_ARG,
                 "run extends past the decomposed source series");
+    if (k == 0) autotune_k(t0);
     const int kk = resolve_k(k);
     if (nrec_ && (int64_t)rec_dev_.n < nsteps * nrec_) rec_dev_.alloc(nsteps * nrec_);
     std::vector<int64_t> guard_steps;
@@ -625,11 +626,13 @@ class AcousticProp final : public stb_prop_s {
   std::string describe(int k) override {
     std::ostringstream os;
     const int kk = resolve_k(k);
-    if (path_ == Path::Fused)
+    if (path_ == Path::Fused) {
       os << "acoustic_fused<f32,R=" << R_ << ",TY=" << kTY << ",TZ=" << kTZ << ",PF=" << pf_for(R_, resolve_k(k))
          << "," << (fast_ ? "fma" : "exact") << "> k=" << kk << " cx=" << cx_len_
          << " bytes_per_point=" << (kk == 1 ? 16 : 20);
-    else if (path_ == Path::Tiled)
+      if (k == 0 && tuned_k_ && tune_ms_[0] > 0.f)
+        os << " autotuned(ms/step k1=" << tune_ms_[0] << " k2=" << tune_ms_[1] << ")";
+    } else if (path_ == Path::Tiled)
       os << "acoustic_tiled_step<f32,R=" << R_ << ",TY=16,TZ=64,PF=2> k=1 cx=" << cx_len_
          << " bytes_per_point=16";
     else
@@ -647,9 +650,40 @@ class AcousticProp final : public stb_prop_s {
 
   int slot(int64_t t) const { return (int)(((t % NB) + NB) % NB); }
 
+  // time_height = 0: fused steps per launch chosen by measurement on this
+  // handle's own grid.  A fused block is idempotent -- it recomputes levels
+  // t.. from t-1, t-2 (injection included) into ring slots the real block
+  // overwrites anyway -- so K = 1 and K = 2 launches are timed on the live
+  // state before the first real step, without perturbing it.
+  void autotune_k(int64_t t) {
+    if (tuned_k_ || path_ != Path::Fused || max_k_ < 2) return;
+    tuned_k_ = default_k_;
+    if (std::getenv("STB_DEFAULT_K") || (K_ && t + 2 > src_nt_)) return;
+    if (const char* e = std::getenv("STB_AUTOTUNE"))
+      if (std::atoi(e) == 0) return;
+    cudaEvent_t ev[3];
+    for (auto& e : ev) STB_CUDA(cudaEventCreate(&e));
+    launch_fused(t, 1, nullptr, 0);             // first launches: module load, maps
+    launch_fused(t, 2, nullptr, 0);
+    constexpr int kReps = 3;
+    STB_CUDA(cudaEventRecord(ev[0], st_));
+    for (int i = 0; i < kReps; ++i) launch_fused(t, 1, nullptr, 0);
+    STB_CUDA(cudaEventRecord(ev[1], st_));
+    for (int i = 0; i < kReps; ++i) launch_fused(t, 2, nullptr, 0);
+    STB_CUDA(cudaEventRecord(ev[2], st_));
+    STB_CUDA(cudaEventSynchronize(ev[2]));
+    float m1 = 0.f, m2 = 0.f;
+    STB_CUDA(cudaEventElapsedTime(&m1, ev[0], ev[1]));
+    STB_CUDA(cudaEventElapsedTime(&m2, ev[1], ev[2]));
+    for (auto& e : ev) cudaEventDestroy(e);
+    tune_ms_[0] = m1 / kReps;                   // per step
+    tune_ms_[1] = m2 / kReps / 2;
+    tuned_k_ = tune_ms_[1] < 0.95f * tune_ms_[0] ? 2 : 1;
+  }
+
   int resolve_k(int k) const {
     if (path_ != Path::Fused) return 1;
-    int kk = k < 1 ? default_k_ : k;
+    int kk = k < 1 ? (tuned_k_ ? tuned_k_ : default_k_) : k;
     if (kk > max_k_) kk = max_k_;
     return kk;
   }
@@ -836,6 +870,8 @@ class AcousticProp final : public stb_prop_s {
   bool fast_ = false;
   int arithmetic_ = 0;
   int max_k_ = 1, default_k_ = 1, last_k_ = 1;
+  int tuned_k_ = 0;                 // 0: not measured yet (time_height = 0)
+  float tune_ms_[2] = {0.f, 0.f};   // measured ms per step at K = 1, 2
   int cx_len_ = 0, nchunks_ = 1;
   int diag_cx_ = 0;                 // >0: K=2 blocks run as diagonal K=1 sweeps
   TiledCoefs tcf_{};

@@ -155,6 +155,11 @@ class SlabRunner:
         self.dt, self.nt = resolve_steps(config)
         k = _gpu_time_height(config)
         self.time_height = 1 if self.single_step else (k if k > 0 else DEFAULT_TIME_HEIGHT)
+        # one rank: time_height 0 lets the library measure k on this grid
+        # (AcousticProp::autotune_k); several ranks share the ghost depth of
+        # an explicit k
+        self.k_request = 0 if (world == 1 and k == 0 and not self.single_step) else \
+            self.time_height
         grid = config.grid
         nx = grid.shape[0]
         R = config.space_order // 2
@@ -222,7 +227,10 @@ class SlabRunner:
             # no exchange: one device call covers every block
             rec = (np.zeros((nsteps, len(self.rec_index)), dtype=np.float64)
                    if record and len(self.rec_index) else None)
-            self.dev.run(t0, nsteps, k, rec)
+            self.dev.run(t0, nsteps, self.k_request, rec)
+            if self.k_request == 0:
+                m = re.search(r"\bk=(\d+)", self.dev.describe(0))
+                self.time_height = int(m.group(1)) if m else self.time_height
             self._accumulate()
             if rec is not None:
                 self._traces.append((t0, rec))
@@ -409,7 +417,7 @@ class SlabRunner:
         return dict(getattr(self, "_acc", {}))
 
     def describe(self) -> str:
-        return self.dev.describe(self.time_height)
+        return self.dev.describe(self.k_request if self.k_request == 0 else self.time_height)
 
     def kernel_tag(self) -> str:
         return self.describe().split(" ")[0]
