@@ -168,3 +168,15 @@ def test_receiver_field_validation():
     cfg = stb.RunConfig(physics="elastic", grid=g, space_order=4, nt=2,
                         medium={"vp": 3000.0, "vs": 1700.0, "rho": 2000.0}, receiver_field="vz")
     assert cfg.receiver_field == "vz"
+
+
+def test_par_max_matches_numpy():
+    from paper_2010_10248_b200.physics import par_max
+    rng = np.random.default_rng(0)
+    a = rng.normal(size=(130, 180, 190))
+    assert par_max(a) == float(np.max(a))
+    a[77, 3, 4] = np.nan
+    assert np.isnan(par_max(a))
+    b = np.broadcast_to(np.arange(190.0)[None, None, :], (130, 180, 190))
+    assert par_max(b) == 189.0
+    assert par_max(3.5) == 3.5
