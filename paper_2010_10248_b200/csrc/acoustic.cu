@@ -201,6 +201,9 @@ class AcousticProp final : public stb_prop_s {
     zero_lo_ = x_begin_ == 0;
     zero_hi_ = x_begin_ + d_.nx == desc.geom.shape[0];
     STB_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    STB_CUDA(cudaStreamCreateWithFlags(&gst_, cudaStreamNonBlocking));
+    for (auto& e : gev_) STB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    STB_CUDA(cudaEventCreateWithFlags(&sev_, cudaEventDisableTiming));
     for (int a = 0; a < 3; ++a) active_[a] = desc.active[a] != 0;
     // coefficients, rounded once to T exactly as NumPy's weak-scalar rule
     // rounds the Python floats _center/_lap_terms (physics.py:158-164).
@@ -250,6 +253,10 @@ class AcousticProp final : public stb_prop_s {
     for (auto& e : events_) cudaEventDestroy(e);
     for (auto& e : run_ev_)
       if (e) cudaEventDestroy(e);
+    for (auto& e : gev_)
+      if (e) cudaEventDestroy(e);
+    if (sev_) cudaEventDestroy(sev_);
+    if (gst_) cudaStreamDestroy(gst_);
     if (st_) cudaStreamDestroy(st_);
   }
 
@@ -427,6 +434,10 @@ class AcousticProp final : public stb_prop_s {
           gflag = guards_.p + gi;
           ++gi;
         }
+      // receivers gather level s on a second stream (overlapping the next
+      // steps); the block that rewrites ring slot s first waits for it
+      if (nrec_)
+        for (int j = 0; j < kb; ++j) STB_CUDA(cudaStreamWaitEvent(st_, gev_[slot(t + j)], 0));
       STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
       if (path_ == Path::Fused && kb == 2 && diag_cx_ > 0 && R_ == 4) {
         // L2-streaming temporal blocking: step t on x-chunk c, then step t+1
@@ -467,17 +478,24 @@ class AcousticProp final : public stb_prop_s {
         ++all_launches_;
       }
       if (nrec_) {
+        STB_CUDA(cudaEventRecord(sev_, st_));
+        STB_CUDA(cudaStreamWaitEvent(gst_, sev_, 0));
         for (int j = 0; j < kb; ++j) {
           // levels t..t+kb-1 are all resident for kb <= 2 (the fused kernel
           // writes the last two levels), so receivers gather from HBM
           double* row = rec_dev_.p + (t + j - t0) * nrec_;
-          gather_kernel<T><<<g1(nrec_), 256, 0, st_>>>(lvl_[slot(t + j)].p, rec_off_.p,
-                                                       rec_w_.p, nrec_, row);
+          gather_kernel<T><<<g1(nrec_), 256, 0, gst_>>>(lvl_[slot(t + j)].p, rec_off_.p,
+                                                        rec_w_.p, nrec_, row);
           STB_CHECK_LAUNCH();
+          STB_CUDA(cudaEventRecord(gev_[slot(t + j)], gst_));
           ++all_launches_;
         }
       }
       t += kb;
+    }
+    if (nrec_) {                              // join the gather stream
+      STB_CUDA(cudaEventRecord(sev_, gst_));
+      STB_CUDA(cudaStreamWaitEvent(st_, sev_, 0));
     }
     STB_CUDA(cudaEventRecord(run_ev_[1], st_));
     updates_ = nsteps * d_.npoints();
@@ -871,6 +889,9 @@ class AcousticProp final : public stb_prop_s {
   int arithmetic_ = 0;
   int max_k_ = 1, default_k_ = 1, last_k_ = 1;
   int tuned_k_ = 0;                 // 0: not measured yet (time_height = 0)
+  cudaStream_t gst_ = nullptr;      // receiver gathers (overlap the next steps)
+  cudaEvent_t gev_[NB] = {};        // last gather of ring slot s
+  cudaEvent_t sev_ = nullptr;
   float tune_ms_[2] = {0.f, 0.f};   // measured ms per step at K = 1, 2
   int cx_len_ = 0, nchunks_ = 1;
   int diag_cx_ = 0;                 // >0: K=2 blocks run as diagonal K=1 sweeps
