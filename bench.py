@@ -336,8 +336,10 @@ def main():
     bpp = runner.bytes_per_point()
     steps_per_launch = max(k_used, 1)
     avg_launch_ms = st["stencil_ms"] / max(st["stencil_launches"], 1)
-    local_pts = runner.nl * SHAPE[1] * SHAPE[2]        # points one launch sweeps
-    achieved = bpp * local_pts / (avg_launch_ms / 1e3) / 1e9
+    # algorithmic bytes of all stencil launches / their summed device time:
+    # bpp is per point per launch of steps_per_launch fused steps, and
+    # "updates" counts point updates (steps x points, ranged launches too)
+    achieved = (bpp / steps_per_launch) * st["updates"] / (st["stencil_ms"] / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "latest_traffic.json")
     if os.path.exists(prof):
