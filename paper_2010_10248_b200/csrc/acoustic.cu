@@ -250,6 +250,10 @@ class AcousticProp final : public stb_prop_s {
   }
 
   ~AcousticProp() override {
+    // drain in-flight work: buffers are freed on stream 0, which a
+    // non-blocking stream does not order against
+    if (st_) cudaStreamSynchronize(st_);
+    if (gst_) cudaStreamSynchronize(gst_);
     for (auto& e : events_) cudaEventDestroy(e);
     for (auto& e : run_ev_)
       if (e) cudaEventDestroy(e);

@@ -556,6 +556,9 @@ class ElasticProp final : public stb_prop_s {
   }
 
   ~ElasticProp() override {
+    // drain in-flight work: buffers are freed on stream 0, which a
+    // non-blocking stream does not order against
+    if (st_) cudaStreamSynchronize(st_);
     for (auto& e : events_) cudaEventDestroy(e);
     for (auto& e : run_ev_)
       if (e) cudaEventDestroy(e);

@@ -229,7 +229,10 @@ class TtiProp final : public stb_prop_s {
         lv_[f][l].alloc(d_.total);
         lv_[f][l].zero(st_);
       }
-    for (int ax = 0; ax < 3; ++ax) {
+    // fused single-pass path (f32, 3-D): the gradient streams F, G stay on chip
+    fused_ = sizeof(T) == 4 && cf_.active[0] && cf_.active[1] && cf_.active[2];
+    if (const char* e = std::getenv("STB_TTI_PATH")) fused_ = fused_ && std::string(e) != "twopass";
+    for (int ax = 0; ax < 3 && !fused_; ++ax) {
       if (!cf_.active[ax]) continue;
       F_[ax].alloc(d_.total);
       G_[ax].alloc(d_.total);
@@ -270,17 +273,11 @@ class TtiProp final : public stb_prop_s {
     material(desc.d2, desc.d2_scalar, d2_, cf_.d2);
     for (int ax = 0; ax < 3; ++ax) material(desc.axis[ax], desc.axis_scalar[ax], n_[ax], cf_.n[ax]);
     has_fac_ = desc.damp[0] || desc.damp[1] || desc.damp[2];
-    fused_ = sizeof(T) == 4 && cf_.active[0] && cf_.active[1] && cf_.active[2];
-    if (const char* e = std::getenv("STB_TTI_PATH")) fused_ = fused_ && std::string(e) != "twopass";
     cx_ = 150;
     if (const char* e = std::getenv("STB_TTI_CX")) cx_ = std::max(1, std::atoi(e));
     if (fused_) {
-      // the gradient streams are never materialised on this path; scalar
-      // materials are, so the fused loop has no pointer tests
-      for (int ax = 0; ax < 3; ++ax) {
-        F_[ax].release();
-        G_[ax].release();
-      }
+      // scalar materials are materialised, so the fused loop has no pointer
+      // tests
       auto materialise = [&](DevBuf<T>& b, T v) {
         if (b.p) return;
         b.alloc(d_.total);
@@ -308,6 +305,9 @@ class TtiProp final : public stb_prop_s {
   }
 
   ~TtiProp() override {
+    // drain in-flight work: buffers are freed on stream 0, which a
+    // non-blocking stream does not order against
+    if (st_) cudaStreamSynchronize(st_);
     for (auto& e : events_) cudaEventDestroy(e);
     for (auto& e : run_ev_)
       if (e) cudaEventDestroy(e);
