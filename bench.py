@@ -122,7 +122,9 @@ def make_config(stb, v, src, rec, nt, k, arithmetic="exact", workload="cfg2"):
     if workload == "cfg4":
         return stb.RunConfig(physics="tti", grid=grid, space_order=SO, nt=nt, dt=DT_TTI,
                              medium=v, sources=stb.SourceSpec(src, f0=15.0),
-                             receiver_coords=rec, schedule=stb.ScheduleSpec("gpu", time_height=1))
+                             receiver_coords=rec,
+                             schedule=stb.ScheduleSpec("gpu", time_height=1,
+                                                       arithmetic=arithmetic))
     return stb.RunConfig(physics="acoustic", grid=grid, space_order=SO, nt=nt, dt=DT,
                          medium={"velocity": v}, sources=stb.SourceSpec(src, f0=15.0),
                          receiver_coords=rec,

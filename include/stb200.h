@@ -194,6 +194,9 @@ typedef struct {
   const double* damp[3];     /* per-axis sponge tables, as acoustic          */
   int64_t x_begin;           /* x slab, as in stb_acoustic_desc              */
   int64_t nx_local;
+  int32_t arithmetic;        /* 0 = EXACT (the oracle's operation order,
+                                bitwise); 1 = FMA (contracted products, within
+                                1e-5 relative L2; fused f32 3-D kernel only)  */
 } stb_tti_desc;
 
 int stb_acoustic_create(const stb_acoustic_desc* d, stb_prop_t* out);

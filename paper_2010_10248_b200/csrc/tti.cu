@@ -231,6 +231,9 @@ class TtiProp final : public stb_prop_s {
       }
     // fused single-pass path (f32, 3-D): the gradient streams F, G stay on chip
     fused_ = sizeof(T) == 4 && cf_.active[0] && cf_.active[1] && cf_.active[2];
+    fast_ = desc.arithmetic == 1;
+    STB_REQUIRE(!fast_ || fused_, STB_ERR_CONFIG,
+                "schedule.arithmetic: 'fma' needs the fused f32 3-D TTI kernel");
     if (const char* e = std::getenv("STB_TTI_PATH")) fused_ = fused_ && std::string(e) != "twopass";
     for (int ax = 0; ax < 3 && !fused_; ++ax) {
       if (!cf_.active[ax]) continue;
@@ -513,6 +516,7 @@ class TtiProp final : public stb_prop_s {
     if (fused_) {
       const int bpp = (int)sizeof(T) * (2 + 2 + 2 + nmat);
       os << "tti_fused<f32,r=" << r_ << ",ring=" << m_for_r(r_) << "x" << (2 * r_ + 1)
+         << "," << (fast_ ? "fma" : "exact")
          << "> (TMA p/q plane ring, 16x32 tile, x chunk " << cx_
          << ", F/G on chip) k=1 requested_k=" << k << " bytes_per_point=" << bpp;
     } else {
@@ -532,7 +536,11 @@ class TtiProp final : public stb_prop_s {
   template <int r>
   void set_fused_attr() {
     constexpr int M = m_for_r(r);
-    STB_CUDA(cudaFuncSetAttribute(tti_fused<r, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    STB_CUDA(cudaFuncSetAttribute(tti_fused<r, M, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)TtiFusedCfg<r, M>::smem_bytes()));
+    STB_CUDA(cudaFuncSetAttribute(tti_fused<r, M, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)TtiFusedCfg<r, M>::smem_bytes()));
   }
 
@@ -566,7 +574,12 @@ class TtiProp final : public stb_prop_s {
     dim3 grid((unsigned)((d_.nz + kTtiTZ - 1) / kTtiTZ), (unsigned)((d_.ny + kTtiTY - 1) / kTtiTY),
               (unsigned)((d_.nx + cx_ - 1) / cx_));
     constexpr int M = m_for_r(r);
-    tti_fused<r, M><<<grid, kTtiThreads, TtiFusedCfg<r, M>::smem_bytes(), st_>>>(maps_[prev], fa);
+    if (fast_)
+      tti_fused<r, M, true><<<grid, kTtiThreads, TtiFusedCfg<r, M>::smem_bytes(), st_>>>(
+          maps_[prev], fa);
+    else
+      tti_fused<r, M, false><<<grid, kTtiThreads, TtiFusedCfg<r, M>::smem_bytes(), st_>>>(
+          maps_[prev], fa);
   }
 
   void launch_fused(const TtiArgs<T>& A, int prev) {
@@ -611,6 +624,7 @@ class TtiProp final : public stb_prop_s {
 
   int r_ = 1;
   bool fused_ = false;
+  bool fast_ = false;
   int rec_field_ = 0;        // p
   int cx_ = 150;
   TtiMaps maps_[2];           // [level buffer] p/q tensor maps (fused path)

@@ -92,19 +92,27 @@ __device__ __forceinline__ float ld_cg(const float* p) {
   return v;
 }
 
+// acc + d*c: EXACT keeps the oracle's separate rounding of the product and
+// the sum; FAST (ScheduleSpec.arithmetic = "fma") contracts them
+template <bool FAST>
+__device__ __forceinline__ float mac(float acc, float d, float c) {
+  if constexpr (FAST) return __fmaf_rn(d, c, acc);
+  else return radd(acc, rmul(d, c));
+}
+
 // centred first derivative from a strided shared-memory accessor
-template <int r>
+template <int r, bool FAST>
 __device__ __forceinline__ float d1s(const float* c0, int s, const float* c) {
   float acc = rmul(rsub(c0[s], c0[-s]), c[0]);
 #pragma unroll
-  for (int k = 2; k <= r; ++k) acc = radd(acc, rmul(rsub(c0[k * s], c0[-k * s]), c[k - 1]));
+  for (int k = 2; k <= r; ++k) acc = mac<FAST>(acc, rsub(c0[k * s], c0[-k * s]), c[k - 1]);
   return acc;
 }
 
 // pass 1 at one point: gradients of p, q (x via ring slots, y/z in-plane),
 // w_p, w_q, then F_a, G_a.  ps[d] points at the (y, z) position of p in the
 // slot of plane xa + d - r (d = 0..2r); q sits QOFF floats further.
-template <int r, int PZ, int QOFF>
+template <int r, int PZ, int QOFF, bool FAST>
 __device__ __forceinline__ void tti_point_pass1(const float* const* ps, const float* cx,
                                                 const float* cy, const float* cz,
                                                 const float n[3], float F[3], float G[3]) {
@@ -112,18 +120,24 @@ __device__ __forceinline__ void tti_point_pass1(const float* const* ps, const fl
   float gqx = rmul(rsub(ps[r + 1][QOFF], ps[r - 1][QOFF]), cx[0]);
 #pragma unroll
   for (int k = 2; k <= r; ++k) {
-    gpx = radd(gpx, rmul(rsub(ps[r + k][0], ps[r - k][0]), cx[k - 1]));
-    gqx = radd(gqx, rmul(rsub(ps[r + k][QOFF], ps[r - k][QOFF]), cx[k - 1]));
+    gpx = mac<FAST>(gpx, rsub(ps[r + k][0], ps[r - k][0]), cx[k - 1]);
+    gqx = mac<FAST>(gqx, rsub(ps[r + k][QOFF], ps[r - k][QOFF]), cx[k - 1]);
   }
-  const float gpy = d1s<r>(ps[r], PZ, cy);
-  const float gqy = d1s<r>(ps[r] + QOFF, PZ, cy);
-  const float gpz = d1s<r>(ps[r], 1, cz);
-  const float gqz = d1s<r>(ps[r] + QOFF, 1, cz);
-  const float wp = radd(radd(rmul(gpx, n[0]), rmul(gpy, n[1])), rmul(gpz, n[2]));
-  const float wq = radd(radd(rmul(gqx, n[0]), rmul(gqy, n[1])), rmul(gqz, n[2]));
-  F[0] = rsub(gpx, rmul(wp, n[0]));
-  F[1] = rsub(gpy, rmul(wp, n[1]));
-  F[2] = rsub(gpz, rmul(wp, n[2]));
+  const float gpy = d1s<r, FAST>(ps[r], PZ, cy);
+  const float gqy = d1s<r, FAST>(ps[r] + QOFF, PZ, cy);
+  const float gpz = d1s<r, FAST>(ps[r], 1, cz);
+  const float gqz = d1s<r, FAST>(ps[r] + QOFF, 1, cz);
+  const float wp = mac<FAST>(mac<FAST>(rmul(gpx, n[0]), gpy, n[1]), gpz, n[2]);
+  const float wq = mac<FAST>(mac<FAST>(rmul(gqx, n[0]), gqy, n[1]), gqz, n[2]);
+  if constexpr (FAST) {
+    F[0] = __fmaf_rn(-wp, n[0], gpx);
+    F[1] = __fmaf_rn(-wp, n[1], gpy);
+    F[2] = __fmaf_rn(-wp, n[2], gpz);
+  } else {
+    F[0] = rsub(gpx, rmul(wp, n[0]));
+    F[1] = rsub(gpy, rmul(wp, n[1]));
+    F[2] = rsub(gpz, rmul(wp, n[2]));
+  }
   G[0] = rmul(wq, n[0]);
   G[1] = rmul(wq, n[1]);
   G[2] = rmul(wq, n[2]);
@@ -131,7 +145,7 @@ __device__ __forceinline__ void tti_point_pass1(const float* const* ps, const fl
 
 constexpr int pmod(int a, int m) { return ((a % m) + m) % m; }
 
-template <int r, int M>
+template <int r, int M, bool FAST>
 __global__ void __launch_bounds__(kTtiThreads, 1)
 tti_fused(const __grid_constant__ TtiMaps maps, TtiFusedArgs a) {
   using C = TtiFusedCfg<r, M>;
@@ -300,7 +314,7 @@ tti_fused(const __grid_constant__ TtiMaps maps, TtiFusedArgs a) {
 #pragma unroll
         for (int dd = 0; dd <= 2 * r; ++dd) ps[dd] = sp + ((u + dd) % NS) * C::SLOT + core_off;
         float F[3] = {0.f, 0.f, 0.f}, G[3] = {0.f, 0.f, 0.f};
-        if (xa_in && core_in) tti_point_pass1<r, C::PZ, QOFF>(ps, c0, c1, c2, ncur, F, G);
+        if (xa_in && core_in) tti_point_pass1<r, C::PZ, QOFF, FAST>(ps, c0, c1, c2, ncur, F, G);
         qF[u % Q] = F[0];
         qG[u % Q] = G[0];
         fgb[0 * C::EPL + ecore] = F[1];
@@ -314,7 +328,7 @@ tti_fused(const __grid_constant__ TtiMaps maps, TtiFusedArgs a) {
 #pragma unroll
         for (int dd = 0; dd <= 2 * r; ++dd) ps[dd] = sp + ((u + dd) % NS) * C::SLOT + halo_off;
         float F[3] = {0.f, 0.f, 0.f}, G[3] = {0.f, 0.f, 0.f};
-        if (xa_in && h_in) tti_point_pass1<r, C::PZ, QOFF>(ps, c0, c1, c2, nhcur, F, G);
+        if (xa_in && h_in) tti_point_pass1<r, C::PZ, QOFF, FAST>(ps, c0, c1, c2, nhcur, F, G);
         const int comp = h_yrole ? 0 : 2;
         fgb[comp * C::EPL + ehalo] = h_yrole ? F[1] : F[2];
         fgb[(comp + 1) * C::EPL + ehalo] = h_yrole ? G[1] : G[2];
@@ -327,10 +341,10 @@ tti_fused(const __grid_constant__ TtiMaps maps, TtiFusedArgs a) {
       }
 
       // y / z divergence terms at plane xa
-      qDyF[u % Q] = d1s<r>(fgb + 0 * C::EPL + ecore, C::EZ, c1);
-      qDyG[u % Q] = d1s<r>(fgb + 1 * C::EPL + ecore, C::EZ, c1);
-      qDzF[u % Q] = d1s<r>(fgb + 2 * C::EPL + ecore, 1, c2);
-      qDzG[u % Q] = d1s<r>(fgb + 3 * C::EPL + ecore, 1, c2);
+      qDyF[u % Q] = d1s<r, FAST>(fgb + 0 * C::EPL + ecore, C::EZ, c1);
+      qDyG[u % Q] = d1s<r, FAST>(fgb + 1 * C::EPL + ecore, C::EZ, c1);
+      qDzF[u % Q] = d1s<r, FAST>(fgb + 2 * C::EPL + ecore, 1, c2);
+      qDzG[u % Q] = d1s<r, FAST>(fgb + 3 * C::EPL + ecore, 1, c2);
 
       // output plane x = xa - r: F_x of plane x + k sits at position
       // (u - r + k) mod Q; the y/z terms of plane x at (u - r) mod Q
@@ -340,16 +354,21 @@ tti_fused(const __grid_constant__ TtiMaps maps, TtiFusedArgs a) {
         float dxG = rmul(rsub(qG[pmod(u - r + 1, Q)], qG[pmod(u - r - 1, Q)]), c0[0]);
 #pragma unroll
         for (int k = 2; k <= r; ++k) {
-          dxF = radd(dxF, rmul(rsub(qF[pmod(u - r + k, Q)], qF[pmod(u - r - k, Q)]), c0[k - 1]));
-          dxG = radd(dxG, rmul(rsub(qG[pmod(u - r + k, Q)], qG[pmod(u - r - k, Q)]), c0[k - 1]));
+          dxF = mac<FAST>(dxF, rsub(qF[pmod(u - r + k, Q)], qF[pmod(u - r - k, Q)]), c0[k - 1]);
+          dxG = mac<FAST>(dxG, rsub(qG[pmod(u - r + k, Q)], qG[pmod(u - r - k, Q)]), c0[k - 1]);
         }
         const int pr = pmod(u - r, Q);
         const float lxy = radd(radd(dxF, qDyF[pr]), qDzF[pr]);
         const float lzz = radd(radd(dxG, qDyG[pr]), qDzG[pr]);
         float op = rsub(rmul(p1, 2.f), ocur[0]);
         float oq = rsub(rmul(q1, 2.f), ocur[1]);
-        op = radd(op, rmul(radd(rmul(lxy, ocur[3]), rmul(lzz, ocur[4])), ocur[2]));
-        oq = radd(oq, rmul(radd(rmul(lxy, ocur[4]), lzz), ocur[2]));
+        if constexpr (FAST) {
+          op = __fmaf_rn(__fmaf_rn(lzz, ocur[4], rmul(lxy, ocur[3])), ocur[2], op);
+          oq = __fmaf_rn(__fmaf_rn(lxy, ocur[4], lzz), ocur[2], oq);
+        } else {
+          op = radd(op, rmul(radd(rmul(lxy, ocur[3]), rmul(lzz, ocur[4])), ocur[2]));
+          oq = radd(oq, rmul(radd(rmul(lxy, ocur[4]), lzz), ocur[2]));
+        }
         if (has_fac) {
           // min(min(fx, fy), fz) == min(fx, min(fy, fz)): min is exact
           const float fac = tmin(ocur[5], fyz);

@@ -504,6 +504,10 @@ def _build_tti(config: RunConfig, dt: float, tables, x_begin: int, nx_local: int
     d.geom = _lib.geometry(grid)
     d.space_order, d.precision, d.dt, d.dt2 = config.space_order, config.precision, dt, dt ** 2
     d.x_begin, d.nx_local = int(x_begin), int(nx_local)
+    mode = getattr(config.schedule, "arithmetic", "exact")
+    if mode not in ("exact", "fma"):
+        raise ConfigError("schedule.arithmetic", f"must be 'exact' or 'fma', got {mode!r}")
+    d.arithmetic = 1 if mode == "fma" else 0
     d1 = tti_coefficients(grid, config.space_order)
     for a in range(3):
         d.active[a] = int(grid.shape[a] > 1)

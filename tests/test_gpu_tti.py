@@ -85,3 +85,22 @@ def test_tti_unstable_when_delta_exceeds_epsilon_is_reported():
         so.run(to_config(case))
     with pytest.raises(stb.StabilityError):
         stb.run(to_config(case, stb))
+
+
+@pytest.mark.parametrize("name", ["tti_so8_het_32", "tti_so4_layered", "tti_so12_scalar",
+                                  "tti_dense_src"])
+def test_tti_fma_within_north_star_tolerance(name):
+    """arithmetic="fma" contracts products into FFMA (fused kernel): fields and
+    traces within the north-star 1e-5 relative L2 of the oracle."""
+    case = build_case(name)
+    res = stb.run(to_config(case, stb, schedule=stb.ScheduleSpec("gpu", arithmetic="fma")))
+    ref = so.run(to_config(case))
+    rep = stb.compare_runs(res, ref)
+    assert rep.max_rel_l2 <= L2_TOL, list(rep.lines())
+    assert "fma" in res.report.schedule["device_plan"]
+
+
+def test_tti_fma_needs_fused_path():
+    case = build_case("tti_so8_het_32_f64")
+    with pytest.raises(stb.ConfigError):
+        stb.run(to_config(case, stb, schedule=stb.ScheduleSpec("gpu", arithmetic="fma")))
