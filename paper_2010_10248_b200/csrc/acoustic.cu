@@ -703,6 +703,29 @@ class AcousticProp final : public stb_prop_s {
     tuned_k_ = tune_ms_[1] < 0.95f * tune_ms_[0] ? 2 : 1;
   }
 
+  // x-chunk length for a launch over L planes: minimise waves x iterations,
+  // ceil(c*tiles / slots) * (ceil(L/c) + 2KR), over the chunk count c
+  // (592-plane grid: 4 chunks, as before; an 8-rank slab interior of 64
+  // planes: 3 chunks instead of 1, i.e. 3.75 instead of 1.25 waves).
+  int chunk_len(int L, int K, int ctas_per_sm) {
+    if (L <= 0) return 1;
+    if (std::getenv("STB_NCHUNK")) return cx_len_;
+    if (!sm_count_) STB_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, 0));
+    const int64_t tiles = ((d_.ny + kTY - 1) / kTY) * ((d_.nz + kTZ - 1) / kTZ);
+    const int64_t slots = (int64_t)sm_count_ * ctas_per_sm;
+    int best_c = 1;
+    int64_t best = INT64_MAX;
+    for (int c = 1; c <= std::max(1, L / 8); ++c) {
+      const int64_t waves = (c * tiles + slots - 1) / slots;
+      const int64_t cost = waves * ((L + c - 1) / c + 2 * K * R_);
+      if (cost < best) {
+        best = cost;
+        best_c = c;
+      }
+    }
+    return (L + best_c - 1) / best_c;
+  }
+
   int resolve_k(int k) const {
     if (path_ != Path::Fused) return 1;
     int kk = k < 1 ? (tuned_k_ ? tuned_k_ : default_k_) : k;
@@ -768,7 +791,7 @@ class AcousticProp final : public stb_prop_s {
   void launch_fused_rk(int64_t t, int* gflag, int gmask, int x_lo = 0, int x_hi = -1,
                        int cx = 0) {
     if (x_hi < 0) x_hi = (int)d_.nx;
-    if (cx <= 0) cx = cx_len_;
+    if (cx <= 0) cx = chunk_len(x_hi - x_lo, K, (K == 1 || R <= 2) ? 2 : 1);
     // tensor maps are cached per (K, input slots)
     const int s_l0 = slot(t - 1), s_lm1 = slot(t - 2);
     const int key = (K * NB + s_l0) * NB + s_lm1;
@@ -898,6 +921,7 @@ class AcousticProp final : public stb_prop_s {
   cudaEvent_t sev_ = nullptr;
   float tune_ms_[2] = {0.f, 0.f};   // measured ms per step at K = 1, 2
   int cx_len_ = 0, nchunks_ = 1;
+  int sm_count_ = 0;
   int diag_cx_ = 0;                 // >0: K=2 blocks run as diagonal K=1 sweeps
   TiledCoefs tcf_{};
   CUtensorMap map_ext_[NB]{}, map_tile_[NB]{}, map_inv_{};

@@ -256,11 +256,12 @@ class SlabRunner:
     def _run_async(self, t0: int, nsteps: int, record: bool):
         """Device-ordered stepping: nothing waits on the host inside the loop.
 
-        k = 1 (default): per step, the owned boundary planes (G each side) are
-        computed first; the NCCL exchange of their newest level runs on a side
-        stream as soon as they are done, while the interior planes compute on
-        the library's stream; the receiver gather waits for both.  Ghost
-        planes are not computed (they are overwritten by the exchange).
+        k = 1: per step one launch over the owned planes (ghost planes are not
+        computed: the exchange overwrites them), then the NCCL exchange of the
+        newest level, then the receiver gather -- all ordered on the device.
+        With STB_SLAB_OVERLAP=1 the owned boundary planes (G each side) are
+        computed first and the exchange runs on a side stream while the
+        interior planes compute.
         k >= 2: every held plane is computed (the fused levels consume the
         ghost zones), then the last two levels are exchanged."""
         import torch
@@ -270,8 +271,13 @@ class SlabRunner:
             self._side = torch.cuda.Stream()
         side = self._side
         a_loc, b_loc, G = self.a - self.lo, self.b - self.lo, self.G
+        # boundary/interior split: measured on one B200 for cfg2 slabs, the
+        # two extra ranged launches per step (thin boundary chunks pay the
+        # sweep warm-up) cost more than the exchange they hide (8 ranks:
+        # 129 us split vs 91 us single launch per step), so the single launch
+        # is the default and the split an option
         overlap = (k == 1 and b_loc - a_loc > 2 * G
-                   and os.environ.get("STB_SLAB_OVERLAP", "1") != "0")
+                   and os.environ.get("STB_SLAB_OVERLAP", "0") == "1")
         self.dev.async_begin(t0, nsteps)
         t = t0
         while t < t0 + nsteps:
