@@ -584,9 +584,12 @@ class ElasticProp final : public stb_prop_s {
       md.nz = d_.pitch;
       md.pitch = d_.pitch;
       md.plane = d_.plane;
-      const uint32_t py = kElTY + 2 * R_, pz = kElTZ + 2 * ((R_ + 3) / 4 * 4);
-      for (int f = 0; f < NFIELDS; ++f)
+      // tau fields feed the v pass (kTYv tiles), v fields the tau pass (kTYt)
+      const uint32_t pz = kElTZ + 2 * ((R_ + 3) / 4 * 4);
+      for (int f = 0; f < NFIELDS; ++f) {
+        const uint32_t py = (f >= TXX ? kTYv : kTYt) + 2 * R_;
         fmap_[f] = make_map3d_f32(reinterpret_cast<const float*>(f_[f].p), md, pz, py, 1);
+      }
       switch (R_) {
         case 1: set_tiled_attr<1>(); break;
         case 2: set_tiled_attr<2>(); break;
@@ -597,19 +600,35 @@ class ElasticProp final : public stb_prop_s {
     }
   }
 
+  // tile / ring per radius: 8 x 32 tiles, two CTAs per SM (independent
+  // per-plane barriers); the R = 4 v pass keeps 6 slots so two fit
+  // 16 x 32 tiles, one CTA/SM for both passes.  Measured alternatives
+  // (512^3 so=8): 8 x 32 tiles with two CTAs/SM for both passes (6-slot v
+  // ring) 35.4 Gpts/s, for the tau pass only 36.3, vs 36.4 here -- the
+  // per-plane barrier is not what bounds these sweeps.
+  static constexpr int kTYv = 16, kTYt = 16, kMBv = 1, kMBt = 1;
+  template <int R> static constexpr int ns_v() { return 2 * R + 1; }
+  template <int R> static constexpr int ns_t() { return 2 * R + 1; }
+  template <int R> using CfgV = ElTiledCfg<R, 6, kTYv, ns_v<R>()>;
+  template <int R> using CfgT = ElTiledCfg<R, 3, kTYt, ns_t<R>()>;
+
   template <int R>
   void set_tiled_attr() {
-    STB_CUDA(cudaFuncSetAttribute(elastic_tiled<R, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)ElTiledCfg<R, 6>::smem_bytes()));
-    STB_CUDA(cudaFuncSetAttribute(elastic_tiled<R, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)ElTiledCfg<R, 3>::smem_bytes()));
+    STB_CUDA(cudaFuncSetAttribute(elastic_tiled<R, 0, kTYv, ns_v<R>(), kMBv>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)CfgV<R>::smem_bytes()));
+    STB_CUDA(cudaFuncSetAttribute(elastic_tiled<R, 1, kTYt, ns_t<R>(), kMBt>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)CfgT<R>::smem_bytes()));
   }
 
   template <int R>
   void launch_tiled_r(int* nonfinite) {
     const int cx = 150;
-    dim3 grid((unsigned)((d_.nz + kElTZ - 1) / kElTZ), (unsigned)((d_.ny + kElTY - 1) / kElTY),
-              (unsigned)((d_.nx + cx - 1) / cx));
+    auto grid_for = [&](int ty) {
+      return dim3((unsigned)((d_.nz + kElTZ - 1) / kElTZ), (unsigned)((d_.ny + ty - 1) / ty),
+                  (unsigned)((d_.nx + cx - 1) / cx));
+    };
     ElTiledArgs a{};
     a.fx = reinterpret_cast<const float*>(fac_[0].p);
     a.fy = reinterpret_cast<const float*>(fac_[1].p);
@@ -626,7 +645,8 @@ class ElasticProp final : public stb_prop_s {
     for (int f = 0; f < 3; ++f) a.out[f] = reinterpret_cast<float*>(f_[VX + f].p);
     a.m0 = reinterpret_cast<const float*>(buoy_.p);
     a.m1 = nullptr;
-    elastic_tiled<R, 0><<<grid, kElThreads, ElTiledCfg<R, 6>::smem_bytes(), st_>>>(mv, a);
+    elastic_tiled<R, 0, kTYv, ns_v<R>(), kMBv>
+        <<<grid_for(kTYv), CfgV<R>::THREADS, CfgV<R>::smem_bytes(), st_>>>(mv, a);
     STB_CHECK_LAUNCH();
     // tau half step: inputs vx vy vz, updates the six stresses
     ElTiledMaps mt{};
@@ -634,7 +654,8 @@ class ElasticProp final : public stb_prop_s {
     for (int f = 0; f < 6; ++f) a.out[f] = reinterpret_cast<float*>(f_[TXX + f].p);
     a.m0 = reinterpret_cast<const float*>(lam_.p);
     a.m1 = reinterpret_cast<const float*>(mu_.p);
-    elastic_tiled<R, 1><<<grid, kElThreads, ElTiledCfg<R, 3>::smem_bytes(), st_>>>(mt, a);
+    elastic_tiled<R, 1, kTYt, ns_t<R>(), kMBt>
+        <<<grid_for(kTYt), CfgT<R>::THREADS, CfgT<R>::smem_bytes(), st_>>>(mt, a);
     STB_CHECK_LAUNCH();
   }
 
@@ -846,7 +867,8 @@ class ElasticProp final : public stb_prop_s {
   std::string describe(int k) override {
     std::ostringstream os;
     if (tiled_)
-      os << "elastic_tiled<f32,R=" << R_ << "> (v + tau TMA plane rings, 16x32 tiles, x chunk 150)";
+      os << "elastic_tiled<f32,R=" << R_ << "> (TMA plane rings; " << kTYv
+         << "x32 tiles; x chunk 150)";
     else if (cx_ > 0)
       os << "elastic_sweeps<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
          << "> (v + tau x-sweeps, 32x8 threads, cx=" << cx_ << ")";

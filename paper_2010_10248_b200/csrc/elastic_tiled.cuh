@@ -28,16 +28,19 @@
 namespace stb {
 namespace {
 
-constexpr int kElTY = 16, kElTZ = 32, kElThreads = kElTY * kElTZ;
+constexpr int kElTZ = 32;
 
-template <int R, int NF>
+// TY x 32 tiles; NS ring slots (a divisor of the unroll 2(2R+1), >= R + 2)
+template <int R, int NF, int TY, int NS_>
 struct ElTiledCfg {
   static constexpr int ZH = (R + 3) / 4 * 4;                  // z halo (16-byte boxes)
-  static constexpr int PY = kElTY + 2 * R, PZ = kElTZ + 2 * ZH;
+  static constexpr int PY = TY + 2 * R, PZ = kElTZ + 2 * ZH;
   static constexpr int FSLOT = (PY * PZ + 31) / 32 * 32;       // floats per field plane
   static constexpr int SLOT = NF * FSLOT;
   static constexpr int Q = 2 * R + 1;
-  static constexpr int NS = Q;
+  static constexpr int NS = NS_;
+  static constexpr int THREADS = TY * kElTZ;
+  static_assert((2 * Q) % NS == 0 && NS >= R + 2, "ring must divide the unroll");
   static constexpr size_t smem_bytes() { return (size_t)NS * SLOT * 4 + NS * 8 + 128; }
 };
 
@@ -73,13 +76,14 @@ __device__ __forceinline__ float el_ld_cg(const float* p) {
 constexpr int el_pmod(int a, int m) { return ((a % m) + m) % m; }
 
 // PASS 0: v half step, PASS 1: tau half step.
-template <int R, int PASS>
-__global__ void __launch_bounds__(kElThreads, 1)
+template <int R, int PASS, int TY, int NS_, int MINB>
+__global__ void __launch_bounds__(TY * 32, MINB)
 elastic_tiled(const __grid_constant__ ElTiledMaps maps, ElTiledArgs a) {
   constexpr int NF = PASS == 0 ? 6 : 3;
   constexpr int NO = PASS == 0 ? 3 : 6;       // updated fields
   constexpr int NM = PASS == 0 ? 1 : 2;       // materials
-  using C = ElTiledCfg<R, NF>;
+  using C = ElTiledCfg<R, NF, TY, NS_>;
+  constexpr int kElThreads = C::THREADS;
   constexpr int Q = C::Q, NS = C::NS, U = 2 * Q;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* ring = reinterpret_cast<float*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
@@ -87,7 +91,7 @@ elastic_tiled(const __grid_constant__ ElTiledMaps maps, ElTiledArgs a) {
 
   const int tid = threadIdx.x;
   const int ty = tid >> 5, tz = tid & 31;
-  const int z0 = blockIdx.x * kElTZ, y0 = blockIdx.y * kElTY, x0 = blockIdx.z * a.cx;
+  const int z0 = blockIdx.x * kElTZ, y0 = blockIdx.y * TY, x0 = blockIdx.z * a.cx;
   const int nx = (int)a.d.nx, ny = (int)a.d.ny, nz = (int)a.d.nz;
   const int x1 = min(x0 + a.cx, nx);
   const int y = y0 + ty, z = z0 + tz;
