@@ -457,6 +457,9 @@ def build_propagator(config: RunConfig, dt: float, v_max: float, x_begin: int = 
         return _Prop(raw, config.dtype, ACOUSTIC_FIELDS)
     if config.physics == "tti":
         return _build_tti(config, dt, tables, x_begin, nx_local)
+    if getattr(config.schedule, "arithmetic", "exact") != "exact":
+        raise ConfigError("schedule.arithmetic",
+                          "elastic kernels run the reference's exact operation order only")
     vp = np.asarray(config.medium["vp"], dtype=np.float64)
     vs = np.asarray(config.medium["vs"], dtype=np.float64)
     rho = np.asarray(config.medium["rho"], dtype=np.float64)

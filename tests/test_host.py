@@ -180,3 +180,14 @@ def test_par_max_matches_numpy():
     b = np.broadcast_to(np.arange(190.0)[None, None, :], (130, 180, 190))
     assert par_max(b) == 189.0
     assert par_max(3.5) == 3.5
+
+
+def test_elastic_rejects_fma():
+    from paper_2010_10248_b200.engine import build_propagator
+    g = stb.GridSpec((8, 8, 8), (10.0,) * 3)
+    cfg = stb.RunConfig(physics="elastic", grid=g, space_order=4, nt=2,
+                        medium={"vp": 3000.0, "vs": 1700.0, "rho": 2000.0},
+                        schedule=stb.ScheduleSpec("gpu", arithmetic="fma"))
+    with pytest.raises(stb.ConfigError) as e:
+        build_propagator(cfg, 1e-3, 3000.0)
+    assert e.value.field == "schedule.arithmetic"
