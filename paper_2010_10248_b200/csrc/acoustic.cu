@@ -260,6 +260,11 @@ class AcousticProp final : public stb_prop_s {
     for (auto& e : gev_)
       if (e) cudaEventDestroy(e);
     if (sev_) cudaEventDestroy(sev_);
+    for (auto& e : cev_) cudaEventDestroy(e);
+    if (cst_) {
+      cudaStreamSynchronize(cst_);
+      cudaStreamDestroy(cst_);
+    }
     if (gst_) cudaStreamDestroy(gst_);
     if (st_) cudaStreamDestroy(st_);
   }
@@ -425,6 +430,11 @@ class AcousticProp final : public stb_prop_s {
     guards_.zero(st_);
     ensure_events(nsteps + 1);
     STB_CUDA(cudaEventRecord(run_ev_[0], st_));
+    // traces of completed step chunks are copied out (copy stream) while
+    // later steps compute; chunk c = steps [c*kTraceChunk, ...) of this run
+    const bool stream_traces =
+        nrec_ && rec_out && (size_t)nsteps * nrec_ * sizeof(double) >= ((size_t)64 << 20);
+    std::vector<int64_t> chunk_end;           // exclusive step index (relative)
     size_t gi = 0;
     int64_t t = t0;
     while (t < t0 + nsteps) {
@@ -494,6 +504,17 @@ class AcousticProp final : public stb_prop_s {
           STB_CUDA(cudaEventRecord(gev_[slot(t + j)], gst_));
           ++all_launches_;
         }
+        const int64_t done = t + kb - t0;
+        if (stream_traces && (done / kTraceChunk > (done - kb) / kTraceChunk || t + kb == t0 + nsteps)) {
+          const size_t c = chunk_end.size();
+          while (cev_.size() <= c) {
+            cudaEvent_t e;
+            STB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            cev_.push_back(e);
+          }
+          STB_CUDA(cudaEventRecord(cev_[c], gst_));
+          chunk_end.push_back(done);
+        }
       }
       t += kb;
     }
@@ -504,7 +525,18 @@ class AcousticProp final : public stb_prop_s {
     STB_CUDA(cudaEventRecord(run_ev_[1], st_));
     updates_ = nsteps * d_.npoints();
     last_k_ = kk;
-    if (nrec_ && rec_out) rec_dev_.download(rec_out, nsteps * nrec_, st_);
+    if (stream_traces) {
+      if (!cst_) STB_CUDA(cudaStreamCreateWithFlags(&cst_, cudaStreamNonBlocking));
+      int64_t r0 = 0;
+      for (size_t c = 0; c < chunk_end.size(); ++c) {
+        STB_CUDA(cudaStreamWaitEvent(cst_, cev_[c], 0));
+        device_to_host(rec_out + r0 * nrec_, rec_dev_.p + r0 * nrec_,
+                       (size_t)(chunk_end[c] - r0) * nrec_ * sizeof(double), cst_);
+        r0 = chunk_end[c];
+      }
+    } else if (nrec_ && rec_out) {
+      rec_dev_.download(rec_out, nsteps * nrec_, st_);
+    }
     std::vector<int> gh(guard_steps.size() + 1, 0);
     if (!guard_steps.empty()) guards_.download(gh.data(), guard_steps.size(), st_);
     STB_CUDA(cudaStreamSynchronize(st_));
@@ -919,6 +951,9 @@ class AcousticProp final : public stb_prop_s {
   cudaStream_t gst_ = nullptr;      // receiver gathers (overlap the next steps)
   cudaEvent_t gev_[NB] = {};        // last gather of ring slot s
   cudaEvent_t sev_ = nullptr;
+  static constexpr int64_t kTraceChunk = 64;     // steps per streamed trace chunk
+  cudaStream_t cst_ = nullptr;                   // trace copies
+  std::vector<cudaEvent_t> cev_;
   float tune_ms_[2] = {0.f, 0.f};   // measured ms per step at K = 1, 2
   int cx_len_ = 0, nchunks_ = 1;
   int sm_count_ = 0;
