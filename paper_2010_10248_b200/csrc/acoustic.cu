@@ -775,6 +775,7 @@ class AcousticProp final : public stb_prop_s {
       const char* e = std::getenv("STB_PATH");
       if (e && std::strcmp(e, "reference") == 0) return;
       tcf_.c0 = cf_.c0;
+      tcf_.nz = -0.0f;
       for (int r = 0; r < 8; ++r) {
         tcf_.cx[r] = cf_.c[0][r];
         tcf_.cy[r] = cf_.c[1][r];

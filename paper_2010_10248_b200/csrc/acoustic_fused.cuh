@@ -112,23 +112,24 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 
 // One Laplacian term for two packed points: lap + (p + m) * c.
 template <bool FAST>
-__device__ __forceinline__ f2 term2(f2 lap, f2 p, f2 m, float c) {
+__device__ __forceinline__ f2 term2(f2 lap, f2 p, f2 m, float c, f2 nz) {
   const f2 s = add2(p, m);
   if constexpr (FAST)
     return fma2(s, bcast(c), lap);
   else
-    return add2(lap, smul2(s, c));
+    return add2(lap, xmul2(s, bcast(c), nz));
 }
 
 // Same term when the two sums come from scalars (odd z offsets, where the
 // packed operands would straddle register pairs).
 template <bool FAST>
-__device__ __forceinline__ f2 term2s(f2 lap, float p0, float m0, float p1, float m1, float c) {
+__device__ __forceinline__ f2 term2s(f2 lap, float p0, float m0, float p1, float m1, float c,
+                                     f2 nz) {
   const f2 s = pk(__fadd_rn(p0, m0), __fadd_rn(p1, m1));
   if constexpr (FAST)
     return fma2(s, bcast(c), lap);
   else
-    return add2(lap, smul2(s, c));
+    return add2(lap, xmul2(s, bcast(c), nz));
 }
 
 // Update of 4 consecutive z points.  xq: register queue of the input level
@@ -141,28 +142,29 @@ __device__ __forceinline__ void update4(const float (&xq)[Q][4], const int cs, c
                                         float (&o)[4]) {
   const f2 c01 = pk(xq[cs][0], xq[cs][1]);
   const f2 c23 = pk(xq[cs][2], xq[cs][3]);
+  const f2 nz = bcast(cf.nz);
   f2 L01, L23;
   if constexpr (FAST) {
     L01 = mul2(c01, bcast(cf.c0));
     L23 = mul2(c23, bcast(cf.c0));
   } else {
-    L01 = smul2(c01, cf.c0);
-    L23 = smul2(c23, cf.c0);
+    L01 = xmul2(c01, bcast(cf.c0), nz);
+    L23 = xmul2(c23, bcast(cf.c0), nz);
   }
   // x neighbours (axis 0 first, r ascending -- the reference's term order)
 #pragma unroll
   for (int r = 1; r <= R; ++r) {
     const int sp = (cs + r) % Q, sm = (cs - r + Q) % Q;
-    L01 = term2<FAST>(L01, pk(xq[sp][0], xq[sp][1]), pk(xq[sm][0], xq[sm][1]), cf.cx[r - 1]);
-    L23 = term2<FAST>(L23, pk(xq[sp][2], xq[sp][3]), pk(xq[sm][2], xq[sm][3]), cf.cx[r - 1]);
+    L01 = term2<FAST>(L01, pk(xq[sp][0], xq[sp][1]), pk(xq[sm][0], xq[sm][1]), cf.cx[r - 1], nz);
+    L23 = term2<FAST>(L23, pk(xq[sp][2], xq[sp][3]), pk(xq[sm][2], xq[sm][3]), cf.cx[r - 1], nz);
   }
   // y neighbours
 #pragma unroll
   for (int r = 1; r <= R; ++r) {
     const float4 pp = *reinterpret_cast<const float4*>(cen + r * W);
     const float4 mm = *reinterpret_cast<const float4*>(cen - r * W);
-    L01 = term2<FAST>(L01, pk(pp.x, pp.y), pk(mm.x, mm.y), cf.cy[r - 1]);
-    L23 = term2<FAST>(L23, pk(pp.z, pp.w), pk(mm.z, mm.w), cf.cy[r - 1]);
+    L01 = term2<FAST>(L01, pk(pp.x, pp.y), pk(mm.x, mm.y), cf.cy[r - 1], nz);
+    L23 = term2<FAST>(L23, pk(pp.z, pp.w), pk(mm.z, mm.w), cf.cy[r - 1], nz);
   }
   // z neighbours: window [z - RP, z + 4 + RP)
   float win[4 + 2 * RP];
@@ -175,14 +177,14 @@ __device__ __forceinline__ void update4(const float (&xq)[Q][4], const int cs, c
   for (int r = 1; r <= R; ++r) {
     if ((RP + r) % 2 == 0) {
       L01 = term2<FAST>(L01, pk(win[RP + r], win[RP + r + 1]), pk(win[RP - r], win[RP - r + 1]),
-                        cf.cz[r - 1]);
+                        cf.cz[r - 1], nz);
       L23 = term2<FAST>(L23, pk(win[RP + r + 2], win[RP + r + 3]),
-                        pk(win[RP - r + 2], win[RP - r + 3]), cf.cz[r - 1]);
+                        pk(win[RP - r + 2], win[RP - r + 3]), cf.cz[r - 1], nz);
     } else {
       L01 = term2s<FAST>(L01, win[RP + r], win[RP - r], win[RP + r + 1], win[RP - r + 1],
-                         cf.cz[r - 1]);
+                         cf.cz[r - 1], nz);
       L23 = term2s<FAST>(L23, win[RP + r + 2], win[RP - r + 2], win[RP + r + 3],
-                         win[RP - r + 3], cf.cz[r - 1]);
+                         win[RP - r + 3], cf.cz[r - 1], nz);
     }
   }
   // epilogue: o = ((c*2 - u0) + lap*inv) * fac   (c*2 == c+c exactly)
@@ -192,16 +194,13 @@ __device__ __forceinline__ void update4(const float (&xq)[Q][4], const int cs, c
     v01 = fma2(L01, pk(iv[0], iv[1]), v01);
     v23 = fma2(L23, pk(iv[2], iv[3]), v23);
   } else {
-    float l0, l1, l2, l3;
-    upk(L01, l0, l1);
-    upk(L23, l2, l3);
-    v01 = add2(v01, pk(__fmul_rn(l0, iv[0]), __fmul_rn(l1, iv[1])));
-    v23 = add2(v23, pk(__fmul_rn(l2, iv[2]), __fmul_rn(l3, iv[3])));
+    v01 = add2(v01, xmul2(L01, pk(iv[0], iv[1]), nz));
+    v23 = add2(v23, xmul2(L23, pk(iv[2], iv[3]), nz));
   }
+  v01 = xmul2(v01, pk(fac[0], fac[1]), nz);
+  v23 = xmul2(v23, pk(fac[2], fac[3]), nz);
   upk(v01, o[0], o[1]);
   upk(v23, o[2], o[3]);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) o[i] = __fmul_rn(o[i], fac[i]);
 }
 
 template <int R, int K, int TY, int TZ, int PF, bool FAST, bool GUARD>

@@ -43,6 +43,7 @@ struct TiledCfg {
 struct TiledCoefs {
   float c0;
   float cx[8], cy[8], cz[8];
+  float nz;     // -0.0f, a runtime value on purpose (see xmul2 in f32x2.cuh)
 };
 
 template <int R, int TY, int TZ, int PF>
