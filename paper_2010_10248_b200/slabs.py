@@ -69,7 +69,14 @@ class DeviceSlab:
     """Local propagator of one x-slab on the current CUDA device."""
 
     def __init__(self, config, dt, v_max, x_begin, nx_local):
+        import torch
         self.config = config
+        # libstb200 links its own CUDA runtime, whose per-thread current
+        # device is independent of torch's: bind it to the rank's device
+        # (torch.cuda.set_device(local_rank)) so the slab's buffers, the torch
+        # views of its ghost planes and the NCCL transfers share one GPU
+        if torch.cuda.is_available():
+            _lib.check(_lib.lib().stb_set_device(torch.cuda.current_device()))
         self.prop: _Prop = build_propagator(config, dt, v_max, x_begin=x_begin,
                                             nx_local=nx_local)
         self.item = np.dtype(config.dtype).itemsize
