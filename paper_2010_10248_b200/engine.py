@@ -29,7 +29,7 @@ from . import _lib
 from .errors import ConfigError, InvalidPlanError
 from .grid import GridSpec, centered_first_weights, fd_weights, staggered_fd_weights
 from .physics import (_field_op, acoustic_coefficients, damping_tables, elastic_coefficients,
-                      par_max, ricker, tti_coefficients, tti_medium)
+                      par_max, par_max_of, ricker, tti_coefficients, tti_medium)
 from .precompute import _Handle
 from .sparse import nearest_scales_from_velocity, validate_coords_in_extent
 
@@ -215,8 +215,8 @@ def medium_velocity_bounds(physics: str, medium: dict) -> float:
         if vp.ndim == 0 and eps.ndim == 0:
             return float(np.max(vp * np.sqrt(1.0 + 2.0 * np.maximum(eps, 0.0))))
         shape = np.broadcast_shapes(vp.shape, eps.shape)
-        fast = _field_op(shape, lambda v, e: v * np.sqrt(1.0 + 2.0 * np.maximum(e, 0.0)), vp, eps)
-        return par_max(fast)
+        return par_max_of(shape, lambda v, e: v * np.sqrt(1.0 + 2.0 * np.maximum(e, 0.0)),
+                          vp, eps)
     for key in ("vp", "vs", "rho"):
         if key not in medium:
             raise ConfigError(f"medium.{key}", "elastic runs need vp, vs, rho")

@@ -128,6 +128,18 @@ def _chunked(n: int, fn) -> None:
         list(ex.map(lambda ab: fn(*ab), [(a, b) for a, b in zip(edges[:-1], edges[1:]) if b > a]))
 
 
+def par_max_of(shape, fn, *inputs) -> float:
+    """float(np.max(fn(*inputs))) over x chunks on host threads without
+    materialising fn's full result (max is exact and order-independent)."""
+    arrs = [np.broadcast_to(np.asarray(a, dtype=np.float64), shape) for a in inputs]
+    parts = {}
+
+    def work(lo, hi):
+        parts[lo] = np.max(fn(*(a[lo:hi] for a in arrs)))
+    _chunked(shape[0], work)
+    return float(np.max(np.array([parts[k] for k in sorted(parts)])))
+
+
 def par_max(values) -> float:
     """float(np.max(values)) over x chunks on host threads: max is exact and
     NaN-propagating per chunk, so the result is identical (1.66 GB cfg2
@@ -163,9 +175,20 @@ def tti_axis(theta, phi, shape=None):
     ph = np.asarray(phi, dtype=np.float64)
     if shape is None or (th.ndim == 0 and ph.ndim == 0):
         return (np.sin(th) * np.cos(ph), np.sin(th) * np.sin(ph), np.cos(th))
-    return (_field_op(shape, lambda t, p: np.sin(t) * np.cos(p), th, ph),
-            _field_op(shape, lambda t, p: np.sin(t) * np.sin(p), th, ph),
-            _field_op(shape, lambda t: np.cos(t), th))
+    # one threaded pass, sin(theta) evaluated once per point (the same ufunc
+    # calls on the same values as above, so the results are identical)
+    tb = np.broadcast_to(th, shape)
+    pb = np.broadcast_to(ph, shape)
+    out = tuple(np.empty(shape, dtype=np.float64) for _ in range(3))
+
+    def work(lo, hi):
+        t, p = tb[lo:hi], pb[lo:hi]
+        st = np.sin(t)
+        np.multiply(st, np.cos(p), out=out[0][lo:hi])
+        np.multiply(st, np.sin(p), out=out[1][lo:hi])
+        np.cos(t, out=out[2][lo:hi])
+    _chunked(shape[0], work)
+    return out
 
 
 @dataclass
