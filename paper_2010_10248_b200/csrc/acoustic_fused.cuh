@@ -513,12 +513,10 @@ struct FusedLauncher {
   using C = FusedCfg<R, K, TY, TZ, PF>;
   template <bool GUARD>
   static void launch_g(cudaStream_t st, const FusedMaps& maps, const FusedArgs& a, int nchunks) {
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<uint64_t> configured{0};
+    if (first_use_on_device(configured))
       STB_CUDA(cudaFuncSetAttribute(acoustic_fused<R, K, TY, TZ, PF, FAST, GUARD>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      configured = true;
-    }
     const int nty = (int)((a.d.ny + TY - 1) / TY);
     dim3 grid((unsigned)(a.ntz * nty), (unsigned)nchunks);
     acoustic_fused<R, K, TY, TZ, PF, FAST, GUARD><<<grid, C::NT, C::SMEM, st>>>(maps, a);

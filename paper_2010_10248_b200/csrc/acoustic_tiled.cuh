@@ -216,12 +216,10 @@ template <int R, int TY, int TZ, int PF>
 struct TiledAcousticLauncher {
   using C = TiledCfg<R, TY, TZ, PF>;
   static void configure() {
-    static bool done = false;
-    if (!done) {
+    static std::atomic<uint64_t> done{0};
+    if (first_use_on_device(done))
       STB_CUDA(cudaFuncSetAttribute(acoustic_tiled_step<R, TY, TZ, PF>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      done = true;
-    }
   }
   static void launch(cudaStream_t st, const CUtensorMap& m_u1, const CUtensorMap& m_u0,
                      const CUtensorMap& m_inv, float* out, const float* fx, const float* fy,

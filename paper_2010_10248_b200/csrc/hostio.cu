@@ -103,11 +103,19 @@ class HostIO {
   static constexpr size_t kChunk = (size_t)32 << 20;
   static constexpr int kBufs = 3;
 
+  // one instance per device (its events belong to that device; the pinned
+  // buffers are portable).  Intentionally leaked: pinned memory and events
+  // must not be released during static destruction (after the CUDA runtime
+  // may have shut down).
   static HostIO& get() {
-    // intentionally leaked: pinned memory and events must not be released
-    // during static destruction (after the CUDA runtime may have shut down)
-    static HostIO* io = new HostIO();
-    return *io;
+    static std::mutex m;
+    static HostIO* io[64] = {};
+    int dev = 0;
+    STB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(m);
+    HostIO*& p = io[dev & 63];
+    if (!p) p = new HostIO();
+    return *p;
   }
 
   std::mutex mu;
@@ -115,7 +123,7 @@ class HostIO {
   void ensure() {
     if (buf_[0]) return;
     for (int b = 0; b < kBufs; ++b) {
-      STB_CUDA(cudaHostAlloc(&buf_[b], kChunk, cudaHostAllocDefault));
+      STB_CUDA(cudaHostAlloc(&buf_[b], kChunk, cudaHostAllocPortable));
       STB_CUDA(cudaEventCreateWithFlags(&ev_[b], cudaEventDisableTiming));
     }
   }

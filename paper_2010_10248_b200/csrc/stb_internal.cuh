@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -54,6 +56,15 @@ inline void retain_freed_memory() {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   done_for = dev;
+}
+
+// Kernel attributes (cudaFuncSetAttribute) are per device: true the first
+// time this kernel's configuration is needed on the current device.
+inline bool first_use_on_device(std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  STB_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  return (mask.fetch_or(bit) & bit) == 0;
 }
 
 // Owning device buffer.
