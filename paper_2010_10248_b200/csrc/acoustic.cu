@@ -27,6 +27,7 @@
 #include "acoustic_fused.cuh"
 #include "acoustic_kernels.cuh"
 #include "acoustic_tiled.cuh"
+#include "acoustic_wtb.cuh"
 #include "sparse_ops.cuh"
 
 namespace stb {
@@ -179,6 +180,45 @@ __global__ void tile_ptr_kernel(const int* __restrict__ tkey, int64_t n, int nti
     if (tkey[mid] < t) lo = mid + 1; else hi = mid;
   }
   ptr[t] = (int)lo;
+}
+
+// Per-thread source lists for the two-level wavefront kernel (acoustic_wtb2):
+// entry e of the per-tile list is keyed once for the level-1 thread owning
+// its (y, z) point in the tile widened by (hy1, hz1) and once for the
+// level-2 thread owning it in the tile itself (rows per thread ry); value
+// {x, id*8 + (row % ry)*4 + (dz % 4)}.  Slots per tile: n1 + n2.
+__global__ void wtb_key_kernel(const int4* __restrict__ list, const int* __restrict__ tile_ptr,
+                               int ntiles, int64_t n, int ntz, int TY, int TZ, int hy1, int hz1,
+                               int ry, int g1, int n1, int n2, int* __restrict__ key,
+                               int2* __restrict__ val) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int lo = 0, hi = ntiles;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    if (tile_ptr[mid] <= i) lo = mid; else hi = mid;
+  }
+  const int t = lo;
+  const int4 e = list[i];
+  const int y0 = (t / ntz) * TY, z0 = (t % ntz) * TZ;
+  const int base = t * (n1 + n2);
+  int row = e.y - (y0 - hy1), dz = e.z - (z0 - hz1);
+  if (row >= 0 && row < TY + 2 * hy1 && dz >= 0 && dz < TZ + 2 * hz1) {
+    key[2 * i] = base + (row / ry) * g1 + dz / 4;
+    val[2 * i] = make_int2(e.x, e.w * 8 + (row % ry) * 4 + (dz & 3));
+  } else {
+    key[2 * i] = INT_MAX;
+    val[2 * i] = make_int2(0, 0);
+  }
+  row = e.y - y0;
+  dz = e.z - z0;
+  if (row >= 0 && row < TY && dz >= 0 && dz < TZ) {
+    key[2 * i + 1] = base + n1 + (row / ry) * (TZ / 4) + dz / 4;
+    val[2 * i + 1] = make_int2(e.x, e.w * 8 + (row % ry) * 4 + (dz & 3));
+  } else {
+    key[2 * i + 1] = INT_MAX;
+    val[2 * i + 1] = make_int2(0, 0);
+  }
 }
 
 constexpr int NB = 6;
@@ -352,6 +392,7 @@ class AcousticProp final : public stb_prop_s {
     STB_CUDA(cudaStreamSynchronize(st_));
     src_n_ = n;
     thr_.clear();
+    wtb_thr_.reset();
   }
 
   // Per-thread lists for the fused kernel <R, K> (built on first use).
@@ -387,6 +428,38 @@ class AcousticProp final : public stb_prop_s {
     STB_CHECK_LAUNCH();
     STB_CUDA(cudaStreamSynchronize(st_));
     return thr_.emplace(K, std::move(L)).first->second.get();
+  }
+
+  // Per-thread lists for the two-level wavefront kernel (built on first use).
+  template <int R>
+  const ThrLists* wtb_thr_lists() {
+    if (!K_ || src_n_ == 0) return nullptr;
+    if (wtb_thr_) return wtb_thr_.get();
+    using C = WtbCfg<R, kWtbRY, kWtbPF>;
+    const int nty = (int)((d_.ny + kTY - 1) / kTY), ntz = (int)((d_.nz + kTZ - 1) / kTZ);
+    const int ntiles = nty * ntz;
+    const int64_t n = 2 * src_n_;
+    DevBuf<int> key(n), key2(n);
+    DevBuf<int2> val(n);
+    auto L = std::make_unique<ThrLists>();
+    L->list.alloc(n);
+    wtb_key_kernel<<<g1(src_n_), 256, 0, st_>>>(src_list_.p, src_tile_ptr_.p, ntiles, src_n_, ntz,
+                                                kTY, kTZ, R, C::HZ1, kWtbRY, C::G1, C::NW1T,
+                                                C::NW2T, key.p, val.p);
+    STB_CHECK_LAUNCH();
+    size_t tb = 0;
+    STB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, val.p, L->list.p,
+                                             (int)n, 0, 32, st_));
+    DevBuf<uint8_t> tmp(tb);
+    STB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key2.p, val.p, L->list.p,
+                                             (int)n, 0, 32, st_));
+    const int nk = ntiles * C::NTHR;
+    L->ptr.alloc(nk + 1);
+    tile_ptr_kernel<<<g1(nk + 1), 256, 0, st_>>>(key2.p, n, nk, L->ptr.p);
+    STB_CHECK_LAUNCH();
+    STB_CUDA(cudaStreamSynchronize(st_));
+    wtb_thr_ = std::move(L);
+    return wtb_thr_.get();
   }
 
   void set_receivers(const double* coords, int64_t nrec) override {
@@ -698,6 +771,7 @@ class AcousticProp final : public stb_prop_s {
  private:
   enum class Path { Reference, Tiled, Fused };
   static constexpr int kTY = 16, kTZ = 64;
+  static constexpr int kWtbRY = 2, kWtbPF = 2;   // two-level kernel: rows per thread, prefetch
   // TMA prefetch depth: R = 6 stages 40% larger planes; PF = 2 keeps two
   // CTAs per SM resident (smem), PF = 3 elsewhere.
   static constexpr int pf_for(int R, int K = 1) { return (R >= 6 || (R <= 2 && K > 1)) ? 2 : 3; }
@@ -802,6 +876,7 @@ class AcousticProp final : public stb_prop_s {
       default_k_ = 1;
       if (const char* kd = std::getenv("STB_DEFAULT_K")) default_k_ = std::atoi(kd);
       if (const char* dc = std::getenv("STB_DIAG_CX")) diag_cx_ = std::atoi(dc);
+      if (const char* w = std::getenv("STB_WTB")) wtb_ = w[0] != '0';
       if (default_k_ < 1) default_k_ = 1;
       if (default_k_ > max_k_) default_k_ = max_k_;
       path_ = Path::Fused;
@@ -867,11 +942,72 @@ class AcousticProp final : public stb_prop_s {
       FusedLauncher<R, K, kTY, kTZ, pf_for(R, K), false>::launch(st_, it->second, a, nch);
   }
 
+  // Two-level wavefront kernel (acoustic_wtb.cuh): K = 2 steps per pass.
+  template <int R>
+  void launch_wtb_rk(int64_t t, int* gflag, int gmask, int x_lo = 0, int x_hi = -1) {
+    using C = WtbCfg<R, kWtbRY, kWtbPF>;
+    if (x_hi < 0) x_hi = (int)d_.nx;
+    int cx = chunk_len(x_hi - x_lo, 2, 1);
+    if (cx + 4 * R > C::MAXN) cx = C::MAXN - 4 * R;   // per-CTA damping table
+    const int s_l0 = slot(t - 1), s_lm1 = slot(t - 2);
+    const int key = s_l0 * NB + s_lm1;
+    auto it = wmaps_.find(key);
+    if (it == wmaps_.end()) {
+      WtbMaps m{};
+      const float* l0 = reinterpret_cast<const float*>(lvl_[s_l0].p);
+      m.l0 = make_map3d_f32(l0, d_, C::WZ0, C::HY0, 1);
+      m.lm1 = make_map3d_f32(reinterpret_cast<const float*>(lvl_[s_lm1].p), d_, C::WZ1, C::HY1,
+                             1);
+      m.c1 = make_map3d_f32(l0, d_, C::WZ1, C::TY, 1);
+      if (inv_.p) {
+        const float* iv = reinterpret_cast<const float*>(inv_.p);
+        m.inv1 = make_map3d_f32(iv, d_, C::WZ1, C::HY1, 1);
+        m.inv2 = make_map3d_f32(iv, d_, C::WZ1, C::TY, 1);
+      }
+      it = wmaps_.emplace(key, m).first;
+    }
+    FusedArgs a{};
+    a.out_km1 = reinterpret_cast<float*>(lvl_[slot(t)].p);
+    a.out_k = reinterpret_cast<float*>(lvl_[slot(t + 1)].p);
+    a.fx = reinterpret_cast<const float*>(fac_[0].p);
+    a.fy = reinterpret_cast<const float*>(fac_[1].p);
+    a.fz = reinterpret_cast<const float*>(fac_[2].p);
+    a.inv_scalar = (float)inv_scalar_;
+    a.use_inv = inv_.p ? 1 : 0;
+    a.cf = tcf_;
+    a.d = d_;
+    a.cx_len = cx;
+    a.x_lo = x_lo;
+    a.x_hi = x_hi;
+    a.ntz = (int)((d_.nz + kTZ - 1) / kTZ);
+    a.zero_lo = zero_lo_ ? 1 : 0;
+    a.zero_hi = zero_hi_ ? 1 : 0;
+    a.t0 = (int)t;
+    if (K_) {
+      const ThrLists* tl = wtb_thr_lists<R>();
+      a.thr_ptr = tl ? tl->ptr.p : nullptr;
+      a.thr_list = tl ? tl->list.p : nullptr;
+      a.series = reinterpret_cast<const float*>(series_.p);
+      a.n_src = (int)K_;
+    }
+    a.nonfinite = gflag;
+    a.guard_mask = gmask;
+    const int nch = (x_hi - x_lo + cx - 1) / cx;
+    if (fast_)
+      WtbLauncher<R, kWtbRY, kWtbPF, true>::launch(st_, it->second, a, nch);
+    else
+      WtbLauncher<R, kWtbRY, kWtbPF, false>::launch(st_, it->second, a, nch);
+  }
+
   void launch_fused_range(int64_t t, int kb, int* gflag, int gmask, int x_lo, int x_hi) {
     if constexpr (sizeof(T) == 4) {
-      if (R_ == 4 && kb == 2) return launch_fused_rk<4, 2>(t, gflag, gmask, x_lo, x_hi);
+      if (R_ == 4 && kb == 2)
+        return wtb_ ? launch_wtb_rk<4>(t, gflag, gmask, x_lo, x_hi)
+                    : launch_fused_rk<4, 2>(t, gflag, gmask, x_lo, x_hi);
       if (R_ == 4) return launch_fused_rk<4, 1>(t, gflag, gmask, x_lo, x_hi);
-      if (R_ == 2 && kb == 2) return launch_fused_rk<2, 2>(t, gflag, gmask, x_lo, x_hi);
+      if (R_ == 2 && kb == 2)
+        return wtb_ ? launch_wtb_rk<2>(t, gflag, gmask, x_lo, x_hi)
+                    : launch_fused_rk<2, 2>(t, gflag, gmask, x_lo, x_hi);
       if (R_ == 2) return launch_fused_rk<2, 1>(t, gflag, gmask, x_lo, x_hi);
       if (R_ == 6) return launch_fused_rk<6, 1>(t, gflag, gmask, x_lo, x_hi);
       throw Error(STB_ERR_ARG, "no fused kernel for this space order");
@@ -880,9 +1016,11 @@ class AcousticProp final : public stb_prop_s {
 
   void launch_fused(int64_t t, int kb, int* gflag, int gmask) {
     if constexpr (sizeof(T) == 4) {
-      if (R_ == 4 && kb == 2) return launch_fused_rk<4, 2>(t, gflag, gmask);
+      if (R_ == 4 && kb == 2)
+        return wtb_ ? launch_wtb_rk<4>(t, gflag, gmask) : launch_fused_rk<4, 2>(t, gflag, gmask);
       if (R_ == 4) return launch_fused_rk<4, 1>(t, gflag, gmask);
-      if (R_ == 2 && kb == 2) return launch_fused_rk<2, 2>(t, gflag, gmask);
+      if (R_ == 2 && kb == 2)
+        return wtb_ ? launch_wtb_rk<2>(t, gflag, gmask) : launch_fused_rk<2, 2>(t, gflag, gmask);
       if (R_ == 2) return launch_fused_rk<2, 1>(t, gflag, gmask);
       if (R_ == 6) return launch_fused_rk<6, 1>(t, gflag, gmask);
       throw Error(STB_ERR_ARG, "no fused kernel for this space order");
@@ -962,6 +1100,8 @@ class AcousticProp final : public stb_prop_s {
   TiledCoefs tcf_{};
   CUtensorMap map_ext_[NB]{}, map_tile_[NB]{}, map_inv_{};
   std::unordered_map<int, FusedMaps> fmaps_;
+  std::unordered_map<int, WtbMaps> wmaps_;
+  bool wtb_ = true;                 // K = 2 runs the two-level wavefront kernel
   // sources
   int64_t K_ = 0, src_nt_ = 0;
   DevBuf<T> series_;
@@ -972,6 +1112,7 @@ class AcousticProp final : public stb_prop_s {
   DevBuf<int> src_tile_ptr_;
   int64_t src_n_ = 0;
   std::map<int, std::unique_ptr<ThrLists>> thr_;
+  std::unique_ptr<ThrLists> wtb_thr_;
   // receivers
   int64_t nrec_ = 0;
   DevBuf<int64_t> rec_off_;
