@@ -753,7 +753,12 @@ class AcousticProp final : public stb_prop_s {
   std::string describe(int k) override {
     std::ostringstream os;
     const int kk = resolve_k(k);
-    if (path_ == Path::Fused) {
+    if (path_ == Path::Fused && kk == 2 && wtb_) {
+      os << "acoustic_wtb2<f32,R=" << R_ << ",TY=" << kTY << ",TZ=" << kTZ << ",RY=" << kWtbRY
+         << ",PF=" << kWtbPF << "," << (fast_ ? "fma" : "exact") << "> k=2 bytes_per_point=20";
+      if (k == 0 && tuned_k_ && tune_ms_[0] > 0.f)
+        os << " autotuned(ms/step k1=" << tune_ms_[0] << " k2=" << tune_ms_[1] << ")";
+    } else if (path_ == Path::Fused) {
       os << "acoustic_fused<f32,R=" << R_ << ",TY=" << kTY << ",TZ=" << kTZ << ",PF=" << pf_for(R_, resolve_k(k))
          << "," << (fast_ ? "fma" : "exact") << "> k=" << kk << " cx=" << cx_len_
          << " bytes_per_point=" << (kk == 1 ? 16 : 20);
@@ -771,7 +776,7 @@ class AcousticProp final : public stb_prop_s {
  private:
   enum class Path { Reference, Tiled, Fused };
   static constexpr int kTY = 16, kTZ = 64;
-  static constexpr int kWtbRY = 2, kWtbPF = 2;   // two-level kernel: rows per thread, prefetch
+  static constexpr int kWtbRY = 2, kWtbPF = 3;   // two-level kernel: rows per thread, prefetch
   // TMA prefetch depth: R = 6 stages 40% larger planes; PF = 2 keeps two
   // CTAs per SM resident (smem), PF = 3 elsewhere.
   static constexpr int pf_for(int R, int K = 1) { return (R >= 6 || (R <= 2 && K > 1)) ? 2 : 3; }

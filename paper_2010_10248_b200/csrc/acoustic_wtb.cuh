@@ -277,9 +277,9 @@ struct WtbLane {
       fetch(a, level);
     }
   }
-  __device__ __forceinline__ void store(const FusedArgs& a, float* dst, const float (&o)[RY][4],
+  __device__ __forceinline__ void store(const FusedArgs& a, float* gb, const float (&o)[RY][4],
                                         int p) const {
-    float* base = dst + (int64_t)p * a.d.plane + (int64_t)y * a.d.pitch + z;
+    float* base = gb + (int64_t)p * a.d.plane;
 #pragma unroll
     for (int r = 0; r < RY; ++r)
       if (own[r])
@@ -390,7 +390,7 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
   // CTA-uniform: does the level-1 region leave the grid?  Interior CTAs skip
   // the zero-halo masking.
   const bool edge = (y0 - R < 0) || (y0 + TY + R > a.d.ny) || (z0 - C::HZ1 < 0) ||
-                    (z0 + TZ + C::HZ1 > a.d.nz) || (x0 - R < 0) || (x1 + R > a.d.nx);
+                    (z0 + TZ + C::HZ1 > a.d.nz);
 
   const int cnt = r1 ? N : N - 2 * R;
   const int noff = r1 ? 0 : 2 * R;
@@ -402,7 +402,8 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
   const int offP = r1 ? (row + R) * W + 4 * g + (C::HZ0 - C::HZ1) : (row + R) * W + 4 * g + C::HZ1;
   const int offA = r1 ? row * C::WZ1 + 4 * g : 2 * C::E1 + row * C::WZ1 + 4 * g + C::HZ1;
   const int invA = r1 ? C::E1 : C::ET;
-  float* dst = r1 ? a.out_km1 : a.out_k;
+  // this thread's (y, z) column in the output level; plane offsets added per store
+  float* dst = (r1 ? a.out_km1 : a.out_k) + ((int64_t)ylo * a.d.pitch + zlo);
   const int offW = row * W + 4 * g;              // level 1: own point in the level-1 ring
 
   float q[Q][RY][4];
@@ -463,8 +464,10 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
 #pragma unroll
               for (int i = 0; i < 4; ++i) fac[r][i] = tmin(fxx, L.fyz[r][i]);
             wtb_update<FAST, R, Q, RY, W>(q, cs, pring + ys * ES + offP, u0, iv, fac, a.cf, o);
-            if (edge) {
-              const bool live = (p >= 0 && p < a.d.nx) || (p < 0 ? !a.zero_lo : !a.zero_hi);
+            // zero halo: planes outside the grid (uniform), points outside
+            // the y/z extent (edge CTAs only)
+            const bool live = (p >= 0 && p < a.d.nx) || (p < 0 ? !a.zero_lo : !a.zero_hi);
+            if (edge || !live) {
 #pragma unroll
               for (int r = 0; r < RY; ++r)
 #pragma unroll
