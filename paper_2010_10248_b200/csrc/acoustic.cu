@@ -222,6 +222,10 @@ __global__ void wtb_key_kernel(const int4* __restrict__ list, const int* __restr
 }
 
 constexpr int NB = 6;
+#ifndef STB_WTB_RY
+#define STB_WTB_RY 0
+#endif
+constexpr int kWtbRYOverride = STB_WTB_RY;   // build-time A/B of the rows per thread
 
 }  // namespace
 
@@ -435,7 +439,7 @@ class AcousticProp final : public stb_prop_s {
   const ThrLists* wtb_thr_lists() {
     if (!K_ || src_n_ == 0) return nullptr;
     if (wtb_thr_) return wtb_thr_.get();
-    using C = WtbCfg<R, kWtbRY, kWtbPF>;
+    using C = WtbCfg<R, wtb_ry(R), kWtbPF>;
     const int nty = (int)((d_.ny + kTY - 1) / kTY), ntz = (int)((d_.nz + kTZ - 1) / kTZ);
     const int ntiles = nty * ntz;
     const int64_t n = 2 * src_n_;
@@ -444,7 +448,7 @@ class AcousticProp final : public stb_prop_s {
     auto L = std::make_unique<ThrLists>();
     L->list.alloc(n);
     wtb_key_kernel<<<g1(src_n_), 256, 0, st_>>>(src_list_.p, src_tile_ptr_.p, ntiles, src_n_, ntz,
-                                                kTY, kTZ, R, C::HZ1, kWtbRY, C::G1, C::NW1T,
+                                                kTY, kTZ, R, C::HZ1, wtb_ry(R), C::G1, C::NW1T,
                                                 C::NW2T, key.p, val.p);
     STB_CHECK_LAUNCH();
     size_t tb = 0;
@@ -754,7 +758,7 @@ class AcousticProp final : public stb_prop_s {
     std::ostringstream os;
     const int kk = resolve_k(k);
     if (path_ == Path::Fused && kk == 2 && wtb_) {
-      os << "acoustic_wtb2<f32,R=" << R_ << ",TY=" << kTY << ",TZ=" << kTZ << ",RY=" << kWtbRY
+      os << "acoustic_wtb2<f32,R=" << R_ << ",TY=" << kTY << ",TZ=" << kTZ << ",RY=" << (R_ == 2 ? wtb_ry(2) : wtb_ry(4))
          << ",PF=" << kWtbPF << "," << (fast_ ? "fma" : "exact") << "> k=2 bytes_per_point=20";
       if (k == 0 && tuned_k_ && tune_ms_[0] > 0.f)
         os << " autotuned(ms/step k1=" << tune_ms_[0] << " k2=" << tune_ms_[1] << ")";
@@ -776,7 +780,10 @@ class AcousticProp final : public stb_prop_s {
  private:
   enum class Path { Reference, Tiled, Fused };
   static constexpr int kTY = 16, kTZ = 64;
-  static constexpr int kWtbRY = 2, kWtbPF = 3;   // two-level kernel: rows per thread, prefetch
+  static constexpr int kWtbPF = 3;                // two-level kernel: TMA prefetch depth
+  // rows per thread: 2 (measured at R = 2: RY = 1 gives 21 warps instead of
+  // 11 but doubles the per-plane bookkeeping per point, 274 vs 328 GPts/s)
+  static constexpr int wtb_ry(int) { return kWtbRYOverride ? kWtbRYOverride : 2; }
   // TMA prefetch depth: R = 6 stages 40% larger planes; PF = 2 keeps two
   // CTAs per SM resident (smem), PF = 3 elsewhere.
   static constexpr int pf_for(int R, int K = 1) { return (R >= 6 || (R <= 2 && K > 1)) ? 2 : 3; }
@@ -950,7 +957,7 @@ class AcousticProp final : public stb_prop_s {
   // Two-level wavefront kernel (acoustic_wtb.cuh): K = 2 steps per pass.
   template <int R>
   void launch_wtb_rk(int64_t t, int* gflag, int gmask, int x_lo = 0, int x_hi = -1) {
-    using C = WtbCfg<R, kWtbRY, kWtbPF>;
+    using C = WtbCfg<R, wtb_ry(R), kWtbPF>;
     if (x_hi < 0) x_hi = (int)d_.nx;
     int cx = chunk_len(x_hi - x_lo, 2, 1);
     if (cx + 4 * R > C::MAXN) cx = C::MAXN - 4 * R;   // per-CTA damping table
@@ -999,9 +1006,9 @@ class AcousticProp final : public stb_prop_s {
     a.guard_mask = gmask;
     const int nch = (x_hi - x_lo + cx - 1) / cx;
     if (fast_)
-      WtbLauncher<R, kWtbRY, kWtbPF, true>::launch(st_, it->second, a, nch);
+      WtbLauncher<R, wtb_ry(R), kWtbPF, true>::launch(st_, it->second, a, nch);
     else
-      WtbLauncher<R, kWtbRY, kWtbPF, false>::launch(st_, it->second, a, nch);
+      WtbLauncher<R, wtb_ry(R), kWtbPF, false>::launch(st_, it->second, a, nch);
   }
 
   void launch_fused_range(int64_t t, int kb, int* gflag, int gmask, int x_lo, int x_hi) {
