@@ -226,6 +226,10 @@ constexpr int NB = 6;
 #define STB_WTB_RY 0
 #endif
 constexpr int kWtbRYOverride = STB_WTB_RY;   // build-time A/B of the rows per thread
+#ifndef STB_WTB_TY
+#define STB_WTB_TY 0
+#endif
+constexpr int kWtbTYOverride = STB_WTB_TY;   // build-time A/B of the tile height
 
 }  // namespace
 
@@ -361,10 +365,19 @@ class AcousticProp final : public stb_prop_s {
     const int hy = (max_k_ - 1) * R_;
     int hz = 0;
     for (int j = 1; j < max_k_; ++j) hz = (hz + R_ + 3) / 4 * 4;
-    const int nty = (int)((d_.ny + kTY - 1) / kTY), ntz = (int)((d_.nz + kTZ - 1) / kTZ);
+    src_n_ = tile_lists(kTY, kTZ, hy, hz, src_list_, src_tile_ptr_);
+    thr_.clear();
+    wtb_thr_.reset();
+  }
+
+  // Point k of the inspector support is listed for every TY x TZ tile whose
+  // region widened by (hy, hz) holds it; lists tile-major, x-ordered within a
+  // tile (stable sort of the lexicographic support).  Returns the entry count.
+  int64_t tile_lists(int TY, int TZ, int hy, int hz, DevBuf<int4>& list, DevBuf<int>& tptr) {
+    const int nty = (int)((d_.ny + TY - 1) / TY), ntz = (int)((d_.nz + TZ - 1) / TZ);
     const int ntiles = nty * ntz;
     DevBuf<int> cnt(K_), off(K_ + 1);
-    tile_count_kernel<<<g1(K_), 256, 0, st_>>>(src_keys_.p, K_, d_, kTY, kTZ, hy, hz, nty, ntz,
+    tile_count_kernel<<<g1(K_), 256, 0, st_>>>(src_keys_.p, K_, d_, TY, TZ, hy, hz, nty, ntz,
                                                cnt.p);
     STB_CHECK_LAUNCH();
     size_t tb = 0;
@@ -378,25 +391,23 @@ class AcousticProp final : public stb_prop_s {
     const int64_t n = (int64_t)last_off + last_cnt;
     DevBuf<int> tkey(n), tkey2(n);
     DevBuf<int4> ent(n);
-    src_list_.alloc(n);
-    tile_fill_kernel<<<g1(K_), 256, 0, st_>>>(src_keys_.p, K_, d_, kTY, kTZ, hy, hz, nty, ntz,
+    list.alloc(n);
+    tile_fill_kernel<<<g1(K_), 256, 0, st_>>>(src_keys_.p, K_, d_, TY, TZ, hy, hz, nty, ntz,
                                               off.p, tkey.p, ent.p);
     STB_CHECK_LAUNCH();
     int bits = 1;
     while ((1 << bits) <= ntiles) ++bits;
     tb = 0;
-    STB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkey.p, tkey2.p, ent.p, src_list_.p,
-                                             (int)n, 0, bits, st_));
+    STB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkey.p, tkey2.p, ent.p, list.p, (int)n,
+                                             0, bits, st_));
     tmp.alloc(tb);
-    STB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, tkey.p, tkey2.p, ent.p, src_list_.p,
-                                             (int)n, 0, bits, st_));
-    src_tile_ptr_.alloc(ntiles + 1);
-    tile_ptr_kernel<<<g1(ntiles + 1), 256, 0, st_>>>(tkey2.p, n, ntiles, src_tile_ptr_.p);
+    STB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, tkey.p, tkey2.p, ent.p, list.p, (int)n,
+                                             0, bits, st_));
+    tptr.alloc(ntiles + 1);
+    tile_ptr_kernel<<<g1(ntiles + 1), 256, 0, st_>>>(tkey2.p, n, ntiles, tptr.p);
     STB_CHECK_LAUNCH();
     STB_CUDA(cudaStreamSynchronize(st_));
-    src_n_ = n;
-    thr_.clear();
-    wtb_thr_.reset();
+    return n;
   }
 
   // Per-thread lists for the fused kernel <R, K> (built on first use).
@@ -439,17 +450,34 @@ class AcousticProp final : public stb_prop_s {
   const ThrLists* wtb_thr_lists() {
     if (!K_ || src_n_ == 0) return nullptr;
     if (wtb_thr_) return wtb_thr_.get();
-    using C = WtbCfg<R, wtb_ry(R), kWtbPF>;
-    const int nty = (int)((d_.ny + kTY - 1) / kTY), ntz = (int)((d_.nz + kTZ - 1) / kTZ);
+    using C = WtbCfg<R, wtb_ry(R), kWtbPF, wtb_ty(R)>;
+    const int nty = (int)((d_.ny + C::TY - 1) / C::TY), ntz = (int)((d_.nz + kTZ - 1) / kTZ);
     const int ntiles = nty * ntz;
-    const int64_t n = 2 * src_n_;
+    // tile lists of this kernel's tile shape (the K = 1/2 fused lists when equal)
+    DevBuf<int4> own_list;
+    DevBuf<int> own_ptr;
+    const int4* tl = src_list_.p;
+    const int* tp = src_tile_ptr_.p;
+    int64_t ne = src_n_;
+    if (C::TY != kTY || C::HZ1 != (R + 3) / 4 * 4 || max_k_ < 2) {
+      ne = tile_lists(C::TY, kTZ, R, C::HZ1, own_list, own_ptr);
+      tl = own_list.p;
+      tp = own_ptr.p;
+    }
+    auto L = std::make_unique<ThrLists>();
+    if (ne == 0) {
+      L->ptr.alloc(ntiles * C::NTHR + 1);
+      L->ptr.zero(st_);
+      STB_CUDA(cudaStreamSynchronize(st_));
+      wtb_thr_ = std::move(L);
+      return wtb_thr_.get();
+    }
+    const int64_t n = 2 * ne;
     DevBuf<int> key(n), key2(n);
     DevBuf<int2> val(n);
-    auto L = std::make_unique<ThrLists>();
     L->list.alloc(n);
-    wtb_key_kernel<<<g1(src_n_), 256, 0, st_>>>(src_list_.p, src_tile_ptr_.p, ntiles, src_n_, ntz,
-                                                kTY, kTZ, R, C::HZ1, wtb_ry(R), C::G1, C::NW1T,
-                                                C::NW2T, key.p, val.p);
+    wtb_key_kernel<<<g1(ne), 256, 0, st_>>>(tl, tp, ntiles, ne, ntz, C::TY, kTZ, R, C::HZ1,
+                                            wtb_ry(R), C::G1, C::NW1T, C::NW2T, key.p, val.p);
     STB_CHECK_LAUNCH();
     size_t tb = 0;
     STB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, val.p, L->list.p,
@@ -758,7 +786,8 @@ class AcousticProp final : public stb_prop_s {
     std::ostringstream os;
     const int kk = resolve_k(k);
     if (path_ == Path::Fused && kk == 2 && wtb_) {
-      os << "acoustic_wtb2<f32,R=" << R_ << ",TY=" << kTY << ",TZ=" << kTZ << ",RY=" << (R_ == 2 ? wtb_ry(2) : wtb_ry(4))
+      os << "acoustic_wtb2<f32,R=" << R_ << ",TY=" << (R_ == 2 ? wtb_ty(2) : wtb_ty(4)) << ",TZ=" << kTZ
+         << ",RY=" << (R_ == 2 ? wtb_ry(2) : wtb_ry(4))
          << ",PF=" << kWtbPF << "," << (fast_ ? "fma" : "exact") << "> k=2 bytes_per_point=20";
       if (k == 0 && tuned_k_ && tune_ms_[0] > 0.f)
         os << " autotuned(ms/step k1=" << tune_ms_[0] << " k2=" << tune_ms_[1] << ")";
@@ -784,6 +813,11 @@ class AcousticProp final : public stb_prop_s {
   // rows per thread: 2 (measured at R = 2: RY = 1 gives 21 warps instead of
   // 11 but doubles the per-plane bookkeeping per point, 274 vs 328 GPts/s)
   static constexpr int wtb_ry(int) { return kWtbRYOverride ? kWtbRYOverride : 2; }
+  // tile height: 24 at R = 2 (15 warps fit the register file, level-1
+  // redundancy 1.31 instead of 1.41), 16 at R = 4 (160 registers x 12 warps)
+  static constexpr int wtb_ty(int R) {
+    return kWtbTYOverride ? kWtbTYOverride : (R == 2 ? 24 : 16);
+  }
   // TMA prefetch depth: R = 6 stages 40% larger planes; PF = 2 keeps two
   // CTAs per SM resident (smem), PF = 3 elsewhere.
   static constexpr int pf_for(int R, int K = 1) { return (R >= 6 || (R <= 2 && K > 1)) ? 2 : 3; }
@@ -957,7 +991,7 @@ class AcousticProp final : public stb_prop_s {
   // Two-level wavefront kernel (acoustic_wtb.cuh): K = 2 steps per pass.
   template <int R>
   void launch_wtb_rk(int64_t t, int* gflag, int gmask, int x_lo = 0, int x_hi = -1) {
-    using C = WtbCfg<R, wtb_ry(R), kWtbPF>;
+    using C = WtbCfg<R, wtb_ry(R), kWtbPF, wtb_ty(R)>;
     if (x_hi < 0) x_hi = (int)d_.nx;
     int cx = chunk_len(x_hi - x_lo, 2, 1);
     if (cx + 4 * R > C::MAXN) cx = C::MAXN - 4 * R;   // per-CTA damping table
@@ -1006,9 +1040,9 @@ class AcousticProp final : public stb_prop_s {
     a.guard_mask = gmask;
     const int nch = (x_hi - x_lo + cx - 1) / cx;
     if (fast_)
-      WtbLauncher<R, wtb_ry(R), kWtbPF, true>::launch(st_, it->second, a, nch);
+      WtbLauncher<R, wtb_ry(R), kWtbPF, wtb_ty(R), true>::launch(st_, it->second, a, nch);
     else
-      WtbLauncher<R, wtb_ry(R), kWtbPF, false>::launch(st_, it->second, a, nch);
+      WtbLauncher<R, wtb_ry(R), kWtbPF, wtb_ty(R), false>::launch(st_, it->second, a, nch);
   }
 
   void launch_fused_range(int64_t t, int kb, int* gflag, int gmask, int x_lo, int x_hi) {

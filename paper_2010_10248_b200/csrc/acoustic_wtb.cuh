@@ -43,9 +43,9 @@
 
 namespace stb {
 
-template <int R, int RY, int PF>
+template <int R, int RY, int PF, int TY_ = 16>
 struct WtbCfg {
-  static constexpr int TY = 16, TZ = 64;
+  static constexpr int TY = TY_, TZ = 64;
   static constexpr int RP = kRoundUp4(R);
   static constexpr int HZ1 = RP;                      // level-1 z halo (float4 aligned)
   static constexpr int HZ0 = kRoundUp4(RP + R);       // staged u[t-1] z halo
@@ -288,10 +288,10 @@ struct WtbLane {
   }
 };
 
-template <int R, int RY, int PF, bool FAST, bool GUARD>
-__global__ void __launch_bounds__(WtbCfg<R, RY, PF>::NT, 1)
+template <int R, int RY, int PF, int TY_, bool FAST, bool GUARD>
+__global__ void __launch_bounds__(WtbCfg<R, RY, PF, TY_>::NT, 1)
 acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ FusedArgs a) {
-  using C = WtbCfg<R, RY, PF>;
+  using C = WtbCfg<R, RY, PF, TY_>;
   constexpr int TY = C::TY, TZ = C::TZ, Q = C::Q, W = C::WZ0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* ring1 = reinterpret_cast<float*>(smem_raw);
@@ -506,18 +506,18 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
   }
 }
 
-template <int R, int RY, int PF, bool FAST>
+template <int R, int RY, int PF, int TY_, bool FAST>
 struct WtbLauncher {
-  using C = WtbCfg<R, RY, PF>;
+  using C = WtbCfg<R, RY, PF, TY_>;
   template <bool GUARD>
   static void launch_g(cudaStream_t st, const WtbMaps& maps, const FusedArgs& a, int nchunks) {
     static std::atomic<uint64_t> configured{0};
     if (first_use_on_device(configured))
-      STB_CUDA(cudaFuncSetAttribute(acoustic_wtb2<R, RY, PF, FAST, GUARD>,
+      STB_CUDA(cudaFuncSetAttribute(acoustic_wtb2<R, RY, PF, TY_, FAST, GUARD>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     const int nty = (int)((a.d.ny + C::TY - 1) / C::TY);
     dim3 grid((unsigned)(a.ntz * nty), (unsigned)nchunks);
-    acoustic_wtb2<R, RY, PF, FAST, GUARD><<<grid, C::NT, C::SMEM, st>>>(maps, a);
+    acoustic_wtb2<R, RY, PF, TY_, FAST, GUARD><<<grid, C::NT, C::SMEM, st>>>(maps, a);
     STB_CHECK_LAUNCH();
   }
   static void launch(cudaStream_t st, const WtbMaps& maps, const FusedArgs& a, int nchunks) {
