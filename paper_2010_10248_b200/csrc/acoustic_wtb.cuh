@@ -41,6 +41,14 @@
 
 #include "acoustic_fused.cuh"
 
+// consumer-side barrier waits: plain try_wait spin (STB_WTB_SLEEP=1: with the
+// suspend-time hint)
+#if defined(STB_WTB_SLEEP) && STB_WTB_SLEEP
+#define STB_WTB_WAIT mbar_wait_sleep
+#else
+#define STB_WTB_WAIT mbar_wait
+#endif
+
 namespace stb {
 
 template <int R, int RY, int PF, int TY_ = 16>
@@ -435,8 +443,8 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
       if (c < cnt) {
         const unsigned un = (unsigned)(c + noff);
         const int sb = (int)(un % C::NSB);
-        mbar_wait_sleep(&full[sb], (uint32_t)((un / C::NSB) & 1u));
-        if (!r1) mbar_wait_sleep(&lfull[ps], (uint32_t)pph);
+        STB_WTB_WAIT(&full[sb], (uint32_t)((un / C::NSB) & 1u));
+        if (!r1) STB_WTB_WAIT(&lfull[ps], (uint32_t)pph);
         if (work) ld_rows<RY>(q[qq], pring + ps * ES + offP, W);
         if (c >= 2 * R) {
           const int p = c + pofs;
@@ -478,7 +486,7 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
           if (p >= x0 && p < x1) L.store(a, dst, o, p);
           if (r1) {
             // hand the plane to level 2
-            if (c - 2 * R >= C::NL) mbar_wait_sleep(&lempty[ls], (uint32_t)(lph ^ 1));
+            if (c - 2 * R >= C::NL) STB_WTB_WAIT(&lempty[ls], (uint32_t)(lph ^ 1));
             if (work) {
               float* lb = lbuf + ls * C::EL + offW;
 #pragma unroll
