@@ -182,7 +182,7 @@ __global__ void tile_ptr_kernel(const int* __restrict__ tkey, int64_t n, int nti
   ptr[t] = (int)lo;
 }
 
-// Per-thread source lists for the two-level wavefront kernel (acoustic_wtb2):
+// Per-thread source lists for the wavefront kernels (acoustic_wtb, 1 or 2 levels):
 // entry e of the per-tile list is keyed once for the level-1 thread owning
 // its (y, z) point in the tile widened by (hy1, hz1) and once for the
 // level-2 thread owning it in the tile itself (rows per thread ry); value
@@ -212,7 +212,7 @@ __global__ void wtb_key_kernel(const int4* __restrict__ list, const int* __restr
   }
   row = e.y - y0;
   dz = e.z - z0;
-  if (row >= 0 && row < TY && dz >= 0 && dz < TZ) {
+  if (n2 > 0 && row >= 0 && row < TY && dz >= 0 && dz < TZ) {
     key[2 * i + 1] = base + n1 + (row / ry) * (TZ / 4) + dz / 4;
     val[2 * i + 1] = make_int2(e.x, e.w * 8 + (row % ry) * 4 + (dz & 3));
   } else {
@@ -367,7 +367,8 @@ class AcousticProp final : public stb_prop_s {
     for (int j = 1; j < max_k_; ++j) hz = (hz + R_ + 3) / 4 * 4;
     src_n_ = tile_lists(kTY, kTZ, hy, hz, src_list_, src_tile_ptr_);
     thr_.clear();
-    wtb_thr_.reset();
+    wtb_thr_[0].reset();
+    wtb_thr_[1].reset();
   }
 
   // Point k of the inspector support is listed for every TY x TZ tile whose
@@ -446,11 +447,12 @@ class AcousticProp final : public stb_prop_s {
   }
 
   // Per-thread lists for the two-level wavefront kernel (built on first use).
-  template <int R>
+  template <int R, int LV>
   const ThrLists* wtb_thr_lists() {
+    auto& cache = wtb_thr_[LV - 1];
     if (!K_ || src_n_ == 0) return nullptr;
-    if (wtb_thr_) return wtb_thr_.get();
-    using C = WtbCfg<R, wtb_ry(R), kWtbPF, wtb_ty(R)>;
+    if (cache) return cache.get();
+    using C = WtbCfg<R, LV, wtb_ry(R), kWtbPF, wtb_ty(R, LV)>;
     const int nty = (int)((d_.ny + C::TY - 1) / C::TY), ntz = (int)((d_.nz + kTZ - 1) / kTZ);
     const int ntiles = nty * ntz;
     // tile lists of this kernel's tile shape (the K = 1/2 fused lists when equal)
@@ -459,8 +461,8 @@ class AcousticProp final : public stb_prop_s {
     const int4* tl = src_list_.p;
     const int* tp = src_tile_ptr_.p;
     int64_t ne = src_n_;
-    if (C::TY != kTY || C::HZ1 != (R + 3) / 4 * 4 || max_k_ < 2) {
-      ne = tile_lists(C::TY, kTZ, R, C::HZ1, own_list, own_ptr);
+    if (C::TY != kTY || C::H1 != (max_k_ - 1) * R || C::HZ1 != (max_k_ > 1 ? (R + 3) / 4 * 4 : 0)) {
+      ne = tile_lists(C::TY, kTZ, C::H1, C::HZ1, own_list, own_ptr);
       tl = own_list.p;
       tp = own_ptr.p;
     }
@@ -469,14 +471,14 @@ class AcousticProp final : public stb_prop_s {
       L->ptr.alloc(ntiles * C::NTHR + 1);
       L->ptr.zero(st_);
       STB_CUDA(cudaStreamSynchronize(st_));
-      wtb_thr_ = std::move(L);
-      return wtb_thr_.get();
+      cache = std::move(L);
+      return cache.get();
     }
     const int64_t n = 2 * ne;
     DevBuf<int> key(n), key2(n);
     DevBuf<int2> val(n);
     L->list.alloc(n);
-    wtb_key_kernel<<<g1(ne), 256, 0, st_>>>(tl, tp, ntiles, ne, ntz, C::TY, kTZ, R, C::HZ1,
+    wtb_key_kernel<<<g1(ne), 256, 0, st_>>>(tl, tp, ntiles, ne, ntz, C::TY, kTZ, C::H1, C::HZ1,
                                             wtb_ry(R), C::G1, C::NW1T, C::NW2T, key.p, val.p);
     STB_CHECK_LAUNCH();
     size_t tb = 0;
@@ -490,8 +492,8 @@ class AcousticProp final : public stb_prop_s {
     tile_ptr_kernel<<<g1(nk + 1), 256, 0, st_>>>(key2.p, n, nk, L->ptr.p);
     STB_CHECK_LAUNCH();
     STB_CUDA(cudaStreamSynchronize(st_));
-    wtb_thr_ = std::move(L);
-    return wtb_thr_.get();
+    cache = std::move(L);
+    return cache.get();
   }
 
   void set_receivers(const double* coords, int64_t nrec) override {
@@ -785,8 +787,12 @@ class AcousticProp final : public stb_prop_s {
   std::string describe(int k) override {
     std::ostringstream os;
     const int kk = resolve_k(k);
-    if (path_ == Path::Fused && kk == 2 && wtb_) {
-      os << "acoustic_wtb2<f32,R=" << R_ << ",TY=" << (R_ == 2 ? wtb_ty(2) : wtb_ty(4)) << ",TZ=" << kTZ
+    if (path_ == Path::Fused && kk == 1 && (wtb1_mask_ & (1 << R_))) {
+      os << "acoustic_wtb<f32,R=" << R_ << ",LV=1,TY=" << wtb_ty(R_, 1) << ",TZ=" << kTZ
+         << ",RY=" << wtb_ry(R_) << ",PF=" << kWtbPF << "," << (fast_ ? "fma" : "exact")
+         << "> k=1 bytes_per_point=16";
+    } else if (path_ == Path::Fused && kk == 2 && wtb_) {
+      os << "acoustic_wtb<f32,R=" << R_ << ",LV=2,TY=" << (R_ == 2 ? wtb_ty(2) : wtb_ty(4)) << ",TZ=" << kTZ
          << ",RY=" << (R_ == 2 ? wtb_ry(2) : wtb_ry(4))
          << ",PF=" << kWtbPF << "," << (fast_ ? "fma" : "exact") << "> k=2 bytes_per_point=20";
       if (k == 0 && tuned_k_ && tune_ms_[0] > 0.f)
@@ -813,10 +819,11 @@ class AcousticProp final : public stb_prop_s {
   // rows per thread: 2 (measured at R = 2: RY = 1 gives 21 warps instead of
   // 11 but doubles the per-plane bookkeeping per point, 274 vs 328 GPts/s)
   static constexpr int wtb_ry(int) { return kWtbRYOverride ? kWtbRYOverride : 2; }
-  // tile height: 24 at R = 2 (15 warps fit the register file, level-1
-  // redundancy 1.31 instead of 1.41), 16 at R = 4 (160 registers x 12 warps)
-  static constexpr int wtb_ty(int R) {
-    return kWtbTYOverride ? kWtbTYOverride : (R == 2 ? 24 : 16);
+  // tile height.  Two levels: 24 at R = 2 (15 warps fit the register file,
+  // level-1 redundancy 1.31 instead of 1.41), 16 at R = 4 (160 registers x 12
+  // warps).  One level: 32 (8 consumer warps of 2 rows x 4 z points).
+  static constexpr int wtb_ty(int R, int LV = 2) {
+    return LV == 1 ? 32 : kWtbTYOverride ? kWtbTYOverride : (R == 2 ? 24 : 16);
   }
   // TMA prefetch depth: R = 6 stages 40% larger planes; PF = 2 keeps two
   // CTAs per SM resident (smem), PF = 3 elsewhere.
@@ -859,11 +866,11 @@ class AcousticProp final : public stb_prop_s {
   // ceil(c*tiles / slots) * (ceil(L/c) + 2KR), over the chunk count c
   // (592-plane grid: 4 chunks, as before; an 8-rank slab interior of 64
   // planes: 3 chunks instead of 1, i.e. 3.75 instead of 1.25 waves).
-  int chunk_len(int L, int K, int ctas_per_sm) {
+  int chunk_len(int L, int K, int ctas_per_sm, int ty = kTY) {
     if (L <= 0) return 1;
     if (std::getenv("STB_NCHUNK")) return cx_len_;
     if (!sm_count_) STB_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, 0));
-    const int64_t tiles = ((d_.ny + kTY - 1) / kTY) * ((d_.nz + kTZ - 1) / kTZ);
+    const int64_t tiles = ((d_.ny + ty - 1) / ty) * ((d_.nz + kTZ - 1) / kTZ);
     const int64_t slots = (int64_t)sm_count_ * ctas_per_sm;
     int best_c = 1;
     int64_t best = INT64_MAX;
@@ -923,6 +930,7 @@ class AcousticProp final : public stb_prop_s {
       if (const char* kd = std::getenv("STB_DEFAULT_K")) default_k_ = std::atoi(kd);
       if (const char* dc = std::getenv("STB_DIAG_CX")) diag_cx_ = std::atoi(dc);
       if (const char* w = std::getenv("STB_WTB")) wtb_ = w[0] != '0';
+      if (const char* w = std::getenv("STB_WTB1")) wtb1_mask_ = std::atoi(w);
       if (default_k_ < 1) default_k_ = 1;
       if (default_k_ > max_k_) default_k_ = max_k_;
       path_ = Path::Fused;
@@ -988,15 +996,15 @@ class AcousticProp final : public stb_prop_s {
       FusedLauncher<R, K, kTY, kTZ, pf_for(R, K), false>::launch(st_, it->second, a, nch);
   }
 
-  // Two-level wavefront kernel (acoustic_wtb.cuh): K = 2 steps per pass.
-  template <int R>
+  // Wavefront kernel (acoustic_wtb.cuh): LV = 1 or 2 steps per pass.
+  template <int R, int LV>
   void launch_wtb_rk(int64_t t, int* gflag, int gmask, int x_lo = 0, int x_hi = -1) {
-    using C = WtbCfg<R, wtb_ry(R), kWtbPF, wtb_ty(R)>;
+    using C = WtbCfg<R, LV, wtb_ry(R), kWtbPF, wtb_ty(R, LV)>;
     if (x_hi < 0) x_hi = (int)d_.nx;
-    int cx = chunk_len(x_hi - x_lo, 2, 1);
-    if (cx + 4 * R > C::MAXN) cx = C::MAXN - 4 * R;   // per-CTA damping table
+    int cx = chunk_len(x_hi - x_lo, LV, 1, C::TY);
+    if (cx + 2 * LV * R > C::MAXN) cx = C::MAXN - 2 * LV * R;   // per-CTA damping table
     const int s_l0 = slot(t - 1), s_lm1 = slot(t - 2);
-    const int key = s_l0 * NB + s_lm1;
+    const int key = (LV * NB + s_l0) * NB + s_lm1;
     auto it = wmaps_.find(key);
     if (it == wmaps_.end()) {
       WtbMaps m{};
@@ -1004,17 +1012,17 @@ class AcousticProp final : public stb_prop_s {
       m.l0 = make_map3d_f32(l0, d_, C::WZ0, C::HY0, 1);
       m.lm1 = make_map3d_f32(reinterpret_cast<const float*>(lvl_[s_lm1].p), d_, C::WZ1, C::HY1,
                              1);
-      m.c1 = make_map3d_f32(l0, d_, C::WZ1, C::TY, 1);
+      if (LV == 2) m.c1 = make_map3d_f32(l0, d_, C::WZ1, C::TY, 1);
       if (inv_.p) {
         const float* iv = reinterpret_cast<const float*>(inv_.p);
         m.inv1 = make_map3d_f32(iv, d_, C::WZ1, C::HY1, 1);
-        m.inv2 = make_map3d_f32(iv, d_, C::WZ1, C::TY, 1);
+        if (LV == 2) m.inv2 = make_map3d_f32(iv, d_, C::WZ1, C::TY, 1);
       }
       it = wmaps_.emplace(key, m).first;
     }
     FusedArgs a{};
     a.out_km1 = reinterpret_cast<float*>(lvl_[slot(t)].p);
-    a.out_k = reinterpret_cast<float*>(lvl_[slot(t + 1)].p);
+    a.out_k = reinterpret_cast<float*>(lvl_[slot(t + LV - 1)].p);
     a.fx = reinterpret_cast<const float*>(fac_[0].p);
     a.fy = reinterpret_cast<const float*>(fac_[1].p);
     a.fz = reinterpret_cast<const float*>(fac_[2].p);
@@ -1030,7 +1038,7 @@ class AcousticProp final : public stb_prop_s {
     a.zero_hi = zero_hi_ ? 1 : 0;
     a.t0 = (int)t;
     if (K_) {
-      const ThrLists* tl = wtb_thr_lists<R>();
+      const ThrLists* tl = wtb_thr_lists<R, LV>();
       a.thr_ptr = tl ? tl->ptr.p : nullptr;
       a.thr_list = tl ? tl->list.p : nullptr;
       a.series = reinterpret_cast<const float*>(series_.p);
@@ -1040,22 +1048,31 @@ class AcousticProp final : public stb_prop_s {
     a.guard_mask = gmask;
     const int nch = (x_hi - x_lo + cx - 1) / cx;
     if (fast_)
-      WtbLauncher<R, wtb_ry(R), kWtbPF, wtb_ty(R), true>::launch(st_, it->second, a, nch);
+      WtbLauncher<R, LV, wtb_ry(R), kWtbPF, wtb_ty(R, LV), true>::launch(st_, it->second, a, nch);
     else
-      WtbLauncher<R, wtb_ry(R), kWtbPF, wtb_ty(R), false>::launch(st_, it->second, a, nch);
+      WtbLauncher<R, LV, wtb_ry(R), kWtbPF, wtb_ty(R, LV), false>::launch(st_, it->second, a,
+                                                                          nch);
+  }
+
+  // K = 1 launches: the one-level wavefront kernel where it was measured
+  // faster (bit k of wtb1_mask_ set for R = k), else acoustic_fused<R, 1>
+  template <int R>
+  void launch_k1(int64_t t, int* gflag, int gmask, int x_lo = 0, int x_hi = -1) {
+    if (wtb1_mask_ & (1 << R)) return launch_wtb_rk<R, 1>(t, gflag, gmask, x_lo, x_hi);
+    launch_fused_rk<R, 1>(t, gflag, gmask, x_lo, x_hi);
   }
 
   void launch_fused_range(int64_t t, int kb, int* gflag, int gmask, int x_lo, int x_hi) {
     if constexpr (sizeof(T) == 4) {
       if (R_ == 4 && kb == 2)
-        return wtb_ ? launch_wtb_rk<4>(t, gflag, gmask, x_lo, x_hi)
+        return wtb_ ? launch_wtb_rk<4, 2>(t, gflag, gmask, x_lo, x_hi)
                     : launch_fused_rk<4, 2>(t, gflag, gmask, x_lo, x_hi);
-      if (R_ == 4) return launch_fused_rk<4, 1>(t, gflag, gmask, x_lo, x_hi);
+      if (R_ == 4) return launch_k1<4>(t, gflag, gmask, x_lo, x_hi);
       if (R_ == 2 && kb == 2)
-        return wtb_ ? launch_wtb_rk<2>(t, gflag, gmask, x_lo, x_hi)
+        return wtb_ ? launch_wtb_rk<2, 2>(t, gflag, gmask, x_lo, x_hi)
                     : launch_fused_rk<2, 2>(t, gflag, gmask, x_lo, x_hi);
-      if (R_ == 2) return launch_fused_rk<2, 1>(t, gflag, gmask, x_lo, x_hi);
-      if (R_ == 6) return launch_fused_rk<6, 1>(t, gflag, gmask, x_lo, x_hi);
+      if (R_ == 2) return launch_k1<2>(t, gflag, gmask, x_lo, x_hi);
+      if (R_ == 6) return launch_k1<6>(t, gflag, gmask, x_lo, x_hi);
       throw Error(STB_ERR_ARG, "no fused kernel for this space order");
     }
   }
@@ -1063,12 +1080,12 @@ class AcousticProp final : public stb_prop_s {
   void launch_fused(int64_t t, int kb, int* gflag, int gmask) {
     if constexpr (sizeof(T) == 4) {
       if (R_ == 4 && kb == 2)
-        return wtb_ ? launch_wtb_rk<4>(t, gflag, gmask) : launch_fused_rk<4, 2>(t, gflag, gmask);
-      if (R_ == 4) return launch_fused_rk<4, 1>(t, gflag, gmask);
+        return wtb_ ? launch_wtb_rk<4, 2>(t, gflag, gmask) : launch_fused_rk<4, 2>(t, gflag, gmask);
+      if (R_ == 4) return launch_k1<4>(t, gflag, gmask);
       if (R_ == 2 && kb == 2)
-        return wtb_ ? launch_wtb_rk<2>(t, gflag, gmask) : launch_fused_rk<2, 2>(t, gflag, gmask);
-      if (R_ == 2) return launch_fused_rk<2, 1>(t, gflag, gmask);
-      if (R_ == 6) return launch_fused_rk<6, 1>(t, gflag, gmask);
+        return wtb_ ? launch_wtb_rk<2, 2>(t, gflag, gmask) : launch_fused_rk<2, 2>(t, gflag, gmask);
+      if (R_ == 2) return launch_k1<2>(t, gflag, gmask);
+      if (R_ == 6) return launch_k1<6>(t, gflag, gmask);
       throw Error(STB_ERR_ARG, "no fused kernel for this space order");
     }
   }
@@ -1148,6 +1165,7 @@ class AcousticProp final : public stb_prop_s {
   std::unordered_map<int, FusedMaps> fmaps_;
   std::unordered_map<int, WtbMaps> wmaps_;
   bool wtb_ = true;                 // K = 2 runs the two-level wavefront kernel
+  int wtb1_mask_ = 0;               // bit R: K = 1 runs the one-level wavefront kernel
   // sources
   int64_t K_ = 0, src_nt_ = 0;
   DevBuf<T> series_;
@@ -1158,7 +1176,7 @@ class AcousticProp final : public stb_prop_s {
   DevBuf<int> src_tile_ptr_;
   int64_t src_n_ = 0;
   std::map<int, std::unique_ptr<ThrLists>> thr_;
-  std::unique_ptr<ThrLists> wtb_thr_;
+  std::unique_ptr<ThrLists> wtb_thr_[2];   // acoustic_wtb lists per level count
   // receivers
   int64_t nrec_ = 0;
   DevBuf<int64_t> rec_off_;

@@ -51,30 +51,38 @@
 
 namespace stb {
 
-template <int R, int RY, int PF, int TY_ = 16>
+template <int R, int LV, int RY, int PF, int TY_ = 16>
 struct WtbCfg {
+  static_assert(LV == 1 || LV == 2, "one or two levels per sweep");
   static constexpr int TY = TY_, TZ = 64;
   static constexpr int RP = kRoundUp4(R);
-  static constexpr int HZ1 = RP;                      // level-1 z halo (float4 aligned)
-  static constexpr int HZ0 = kRoundUp4(RP + R);       // staged u[t-1] z halo
-  static constexpr int HY1 = TY + 2 * R, WZ1 = TZ + 2 * HZ1;
-  static constexpr int HY0 = TY + 4 * R, WZ0 = TZ + 2 * HZ0;
-  static_assert(HY1 % RY == 0 && TY % RY == 0, "rows per thread must tile the regions");
+  static constexpr int H1 = (LV - 1) * R;             // level-1 y halo
+  static constexpr int HZ1 = LV == 2 ? RP : 0;        // level-1 z halo (float4 aligned)
+  static constexpr int HZ0 = kRoundUp4(HZ1 + R);      // staged u[t-1] z halo
+  static constexpr int HY1 = TY + 2 * H1, WZ1 = TZ + 2 * HZ1;
+  static constexpr int HY0 = HY1 + 2 * R, WZ0 = TZ + 2 * HZ0;
+  static_assert(HY1 % RY == 0 && TY % RY == 0 && H1 % RY == 0,
+                "rows per thread must tile the regions");
   static constexpr int G1 = WZ1 / 4, G2 = TZ / 4;
   static constexpr int NW1T = (HY1 / RY) * G1;        // level-1 work threads
-  static constexpr int NW2T = (TY / RY) * G2;         // level-2 work threads
+  static constexpr int NW2T = LV == 2 ? (TY / RY) * G2 : 0;   // level-2 work threads
   static constexpr int NTHR = NW1T + NW2T;            // per-tile thread slots (source lists)
   static constexpr int NW1 = (NW1T + 31) / 32, NW2 = (NW2T + 31) / 32;
   static constexpr int NT = 32 * (1 + NW1 + NW2);
+  // per-thread register cap for one CTA per SM: registers are allocated for
+  // whole 4-warp groups (a 288-thread CTA is charged as 384 threads)
+  static constexpr int NTA = (NT + 127) / 128 * 128;
+  static constexpr int MAXREG = (65536 / NTA) / 8 * 8 > 255 ? 255 : (65536 / NTA) / 8 * 8;
   static constexpr int Q = 2 * R + 1;
   static constexpr int NSB = PF + 1;                  // iteration ring (aux boxes, barriers)
   static constexpr int NS1 = R + NSB;                 // staged u[t-1] planes
-  static constexpr int NL = R + 2;                    // level-1 plane ring
+  static constexpr int NL = LV == 2 ? R + 2 : 0;      // level-1 plane ring
   static constexpr int E0 = HY0 * WZ0, E1 = HY1 * WZ1;
   static constexpr int ET = TY * WZ1;                 // level-2 aux boxes: tile rows, WZ1 wide
   static constexpr int EL = HY1 * WZ0;                // level-1 ring plane (row stride WZ0)
-  static constexpr int AUX = 2 * E1 + 2 * ET;         // u[t-2], inv (level 1); u[t-1], inv (level 2)
-  static constexpr int MAXN = 1024;                   // planes per CTA sweep (x chunk + 4R)
+  // u[t-2], inv (level 1); u[t-1], inv (level 2)
+  static constexpr int AUX = 2 * E1 + (LV == 2 ? 2 * ET : 0);
+  static constexpr int MAXN = 1024;                   // planes per CTA sweep (x chunk + 2 LV R)
   static constexpr size_t RING1 = (size_t)NS1 * E0 * 4;
   static constexpr size_t RING2 = (size_t)NSB * AUX * 4;
   static constexpr size_t LBUF = (size_t)NL * EL * 4;
@@ -296,10 +304,10 @@ struct WtbLane {
   }
 };
 
-template <int R, int RY, int PF, int TY_, bool FAST, bool GUARD>
-__global__ void __launch_bounds__(WtbCfg<R, RY, PF, TY_>::NT, 1)
-acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ FusedArgs a) {
-  using C = WtbCfg<R, RY, PF, TY_>;
+template <int R, int LV, int RY, int PF, int TY_, bool FAST, bool GUARD>
+__global__ void __maxnreg__((WtbCfg<R, LV, RY, PF, TY_>::MAXREG))
+acoustic_wtb(const __grid_constant__ WtbMaps maps, const __grid_constant__ FusedArgs a) {
+  using C = WtbCfg<R, LV, RY, PF, TY_>;
   constexpr int TY = C::TY, TZ = C::TZ, Q = C::Q, W = C::WZ0;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* ring1 = reinterpret_cast<float*>(smem_raw);
@@ -320,12 +328,13 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
   const int z0 = (tile % a.ntz) * TZ;
   const int x0 = a.x_lo + blockIdx.y * a.cx_len;
   const int x1 = min(x0 + a.cx_len, a.x_hi);
-  const int N = (x1 - x0) + 4 * R;
-  const int ibase = x0 - 2 * R;
+  const int N = (x1 - x0) + 2 * LV * R;
+  const int ibase = x0 - LV * R;
+  const int pofs1 = x0 - (LV + 1) * R;          // level-1 plane of loop counter c: c + pofs1
 
-  // damping x factors of the planes this CTA touches: fxs[j] = fx(x0 - 3R + j)
+  // damping x factors of the planes this CTA touches: fxs[j] = fx(pofs1 + j)
   for (int j = tid; j < N; j += blockDim.x)
-    fxs[j] = __ldg(a.fx + min(max(x0 - 3 * R + j, 0), (int)a.d.nx - 1));
+    fxs[j] = __ldg(a.fx + min(max(pofs1 + j, 0), (int)a.d.nx - 1));
   if (tid == 0) {
     for (int s = 0; s < C::NSB; ++s) {
       mbar_init(&full[s], 1);
@@ -346,23 +355,24 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
     if (lane == 0) {
       prefetch_map(&maps.l0);
       prefetch_map(&maps.lm1);
-      prefetch_map(&maps.c1);
+      if (LV == 2) prefetch_map(&maps.c1);
       for (int n = 0; n < N; ++n) {
         const int sb = n % C::NSB;
         if (n >= C::NSB) mbar_wait_sleep(&done[sb], (uint32_t)(((n / C::NSB) - 1) & 1));
         uint32_t bytes = (uint32_t)C::E0 * 4u;
         if (n >= 2 * R) bytes += (uint32_t)C::E1 * (use_inv ? 8u : 4u);
-        if (n >= 4 * R) bytes += (uint32_t)C::ET * (use_inv ? 8u : 4u);
+        if (LV == 2 && n >= 4 * R) bytes += (uint32_t)C::ET * (use_inv ? 8u : 4u);
         mbar_arrive_expect_tx(&full[sb], bytes);
-        tma_load_3d(ring1 + (size_t)(n % C::NS1) * C::E0, &maps.l0, z0 - C::HZ0, y0 - 2 * R,
-                    ibase + n, &full[sb]);
+        tma_load_3d(ring1 + (size_t)(n % C::NS1) * C::E0, &maps.l0, z0 - C::HZ0,
+                    y0 - C::H1 - R, ibase + n, &full[sb]);
         float* ab = ring2 + (size_t)sb * C::AUX;
         if (n >= 2 * R) {
-          tma_load_3d(ab, &maps.lm1, z0 - C::HZ1, y0 - R, ibase + n - R, &full[sb]);
+          tma_load_3d(ab, &maps.lm1, z0 - C::HZ1, y0 - C::H1, ibase + n - R, &full[sb]);
           if (use_inv)
-            tma_load_3d(ab + C::E1, &maps.inv1, z0 - C::HZ1, y0 - R, ibase + n - R, &full[sb]);
+            tma_load_3d(ab + C::E1, &maps.inv1, z0 - C::HZ1, y0 - C::H1, ibase + n - R,
+                        &full[sb]);
         }
-        if (n >= 4 * R) {
+        if (LV == 2 && n >= 4 * R) {
           tma_load_3d(ab + 2 * C::E1, &maps.c1, z0 - C::HZ1, y0, ibase + n - 2 * R, &full[sb]);
           if (use_inv)
             tma_load_3d(ab + 2 * C::E1 + C::ET, &maps.inv2, z0 - C::HZ1, y0, ibase + n - 2 * R,
@@ -386,23 +396,24 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
   const int gw = r1 ? C::G1 : C::G2;
   const int row = work ? (t / gw) * RY : 0;
   const int g = work ? t % gw : 0;
-  const int ylo = r1 ? y0 - R + row : y0 + row;
+  const int ylo = r1 ? y0 - C::H1 + row : y0 + row;
   const int zlo = r1 ? z0 - C::HZ1 + 4 * g : z0 + 4 * g;
-  // level 1: rows of a thread are all in or all out of the tile (R, TY multiples of RY)
+  // level 1: rows of a thread are all in or all out of the tile (H1, TY multiples of RY)
   const bool in_tile =
-      !r1 || (row >= R && row < R + TY && 4 * g >= C::HZ1 && 4 * g < C::HZ1 + TZ);
+      !r1 || (row >= C::H1 && row < C::H1 + TY && 4 * g >= C::HZ1 && 4 * g < C::HZ1 + TZ);
   WtbLane<RY> L;
   L.init(a, work, ylo, zlo, in_tile);
   const int level = r1 ? 1 : 2;
-  L.src_init(a, work, tile * C::NTHR + (r1 ? t : C::NW1T + t), r1 ? x0 - R : x0, level);
+  L.src_init(a, work, tile * C::NTHR + (r1 ? t : C::NW1T + t), r1 ? x0 - C::H1 : x0, level);
   // CTA-uniform: does the level-1 region leave the grid?  Interior CTAs skip
-  // the zero-halo masking.
-  const bool edge = (y0 - R < 0) || (y0 + TY + R > a.d.ny) || (z0 - C::HZ1 < 0) ||
-                    (z0 + TZ + C::HZ1 > a.d.nz);
+  // the zero-halo masking.  (One level: nothing reads values outside the
+  // grid, and they are never stored.)
+  const bool edge = LV == 2 && ((y0 - R < 0) || (y0 + TY + R > a.d.ny) || (z0 - C::HZ1 < 0) ||
+                                (z0 + TZ + C::HZ1 > a.d.nz));
 
   const int cnt = r1 ? N : N - 2 * R;
   const int noff = r1 ? 0 : 2 * R;
-  const int pofs = r1 ? x0 - 3 * R : x0 - 2 * R;
+  const int pofs = r1 ? pofs1 : x0 - 2 * R;
   const int fxo = r1 ? 0 : R;
   const int NS = r1 ? C::NS1 : C::NL;
   const int ES = r1 ? C::E0 : C::EL;
@@ -411,7 +422,7 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
   const int offA = r1 ? row * C::WZ1 + 4 * g : 2 * C::E1 + row * C::WZ1 + 4 * g + C::HZ1;
   const int invA = r1 ? C::E1 : C::ET;
   // this thread's (y, z) column in the output level; plane offsets added per store
-  float* dst = (r1 ? a.out_km1 : a.out_k) + ((int64_t)ylo * a.d.pitch + zlo);
+  float* dst = ((r1 && LV == 2) ? a.out_km1 : a.out_k) + ((int64_t)ylo * a.d.pitch + zlo);
   const int offW = row * W + 4 * g;              // level 1: own point in the level-1 ring
 
   float q[Q][RY][4];
@@ -428,7 +439,7 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
 
   // level 2 starts at iteration 2R; it still releases iterations 0..2R-1
   // (after their TMA completed, so the arrivals land in the right phase)
-  if (!r1) {
+  if (LV == 2 && !r1) {
     for (int n = 0; n < 2 * R; ++n) {
       mbar_wait_sleep(&full[n % C::NSB], (uint32_t)((n / C::NSB) & 1));
       __syncwarp();
@@ -484,7 +495,7 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
           }
           L.template epilogue<GUARD>(a, o, level, p, x0, x1, work);
           if (p >= x0 && p < x1) L.store(a, dst, o, p);
-          if (r1) {
+          if (LV == 2 && r1) {
             // hand the plane to level 2
             if (c - 2 * R >= C::NL) STB_WTB_WAIT(&lempty[ls], (uint32_t)(lph ^ 1));
             if (work) {
@@ -514,18 +525,18 @@ acoustic_wtb2(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fuse
   }
 }
 
-template <int R, int RY, int PF, int TY_, bool FAST>
+template <int R, int LV, int RY, int PF, int TY_, bool FAST>
 struct WtbLauncher {
-  using C = WtbCfg<R, RY, PF, TY_>;
+  using C = WtbCfg<R, LV, RY, PF, TY_>;
   template <bool GUARD>
   static void launch_g(cudaStream_t st, const WtbMaps& maps, const FusedArgs& a, int nchunks) {
     static std::atomic<uint64_t> configured{0};
     if (first_use_on_device(configured))
-      STB_CUDA(cudaFuncSetAttribute(acoustic_wtb2<R, RY, PF, TY_, FAST, GUARD>,
+      STB_CUDA(cudaFuncSetAttribute(acoustic_wtb<R, LV, RY, PF, TY_, FAST, GUARD>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     const int nty = (int)((a.d.ny + C::TY - 1) / C::TY);
     dim3 grid((unsigned)(a.ntz * nty), (unsigned)nchunks);
-    acoustic_wtb2<R, RY, PF, TY_, FAST, GUARD><<<grid, C::NT, C::SMEM, st>>>(maps, a);
+    acoustic_wtb<R, LV, RY, PF, TY_, FAST, GUARD><<<grid, C::NT, C::SMEM, st>>>(maps, a);
     STB_CHECK_LAUNCH();
   }
   static void launch(cudaStream_t st, const WtbMaps& maps, const FusedArgs& a, int nchunks) {

@@ -100,7 +100,7 @@ class DeviceSlab:
     # asynchronous stepping (fused acoustic path): see SlabRunner._run_async
     def supports_async(self) -> bool:
         return self.config.physics == "acoustic" and self.prop.describe(1).startswith(
-            "acoustic_fused")
+            ("acoustic_fused", "acoustic_wtb"))
 
     def stream_ptr(self) -> int:
         return self.prop.stream_ptr()
