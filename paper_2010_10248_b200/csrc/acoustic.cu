@@ -792,8 +792,8 @@ class AcousticProp final : public stb_prop_s {
          << ",RY=" << wtb_ry(R_) << ",PF=" << kWtbPF << "," << (fast_ ? "fma" : "exact")
          << "> k=1 bytes_per_point=16";
     } else if (path_ == Path::Fused && kk == 2 && wtb_) {
-      os << "acoustic_wtb<f32,R=" << R_ << ",LV=2,TY=" << (R_ == 2 ? wtb_ty(2) : wtb_ty(4)) << ",TZ=" << kTZ
-         << ",RY=" << (R_ == 2 ? wtb_ry(2) : wtb_ry(4))
+      os << "acoustic_wtb<f32,R=" << R_ << ",LV=2,TY=" << wtb_ty(R_) << ",TZ=" << kTZ
+         << ",RY=" << wtb_ry(R_)
          << ",PF=" << kWtbPF << "," << (fast_ ? "fma" : "exact") << "> k=2 bytes_per_point=20";
       if (k == 0 && tuned_k_ && tune_ms_[0] > 0.f)
         os << " autotuned(ms/step k1=" << tune_ms_[0] << " k2=" << tune_ms_[1] << ")";
@@ -823,7 +823,7 @@ class AcousticProp final : public stb_prop_s {
   // level-1 redundancy 1.31 instead of 1.41), 16 at R = 4 (160 registers x 12
   // warps).  One level: 32 (8 consumer warps of 2 rows x 4 z points).
   static constexpr int wtb_ty(int R, int LV = 2) {
-    return LV == 1 ? 32 : kWtbTYOverride ? kWtbTYOverride : (R == 2 ? 24 : 16);
+    return LV == 1 ? 32 : kWtbTYOverride ? kWtbTYOverride : (R <= 2 ? 24 : 16);
   }
   // TMA prefetch depth: R = 6 stages 40% larger planes; PF = 2 keeps two
   // CTAs per SM resident (smem), PF = 3 elsewhere.
@@ -898,7 +898,7 @@ class AcousticProp final : public stb_prop_s {
     path_ = Path::Reference;
     if constexpr (sizeof(T) == 4) {
       if (!(active_[0] && active_[1] && active_[2])) return;
-      if (R_ != 2 && R_ != 4 && R_ != 6) return;
+      if (R_ != 1 && R_ != 2 && R_ != 4 && R_ != 6) return;
       const char* e = std::getenv("STB_PATH");
       if (e && std::strcmp(e, "reference") == 0) return;
       tcf_.c0 = cf_.c0;
@@ -925,7 +925,7 @@ class AcousticProp final : public stb_prop_s {
         path_ = Path::Tiled;
         return;
       }
-      max_k_ = (R_ == 4 || R_ == 2) ? 2 : 1;
+      max_k_ = (R_ == 4 || R_ == 2 || R_ == 1) ? 2 : 1;
       default_k_ = 1;
       if (const char* kd = std::getenv("STB_DEFAULT_K")) default_k_ = std::atoi(kd);
       if (const char* dc = std::getenv("STB_DIAG_CX")) diag_cx_ = std::atoi(dc);
@@ -1072,6 +1072,10 @@ class AcousticProp final : public stb_prop_s {
         return wtb_ ? launch_wtb_rk<2, 2>(t, gflag, gmask, x_lo, x_hi)
                     : launch_fused_rk<2, 2>(t, gflag, gmask, x_lo, x_hi);
       if (R_ == 2) return launch_k1<2>(t, gflag, gmask, x_lo, x_hi);
+      if (R_ == 1 && kb == 2)
+        return wtb_ ? launch_wtb_rk<1, 2>(t, gflag, gmask, x_lo, x_hi)
+                    : launch_fused_rk<1, 2>(t, gflag, gmask, x_lo, x_hi);
+      if (R_ == 1) return launch_fused_rk<1, 1>(t, gflag, gmask, x_lo, x_hi);
       if (R_ == 6) return launch_k1<6>(t, gflag, gmask, x_lo, x_hi);
       throw Error(STB_ERR_ARG, "no fused kernel for this space order");
     }
@@ -1085,6 +1089,9 @@ class AcousticProp final : public stb_prop_s {
       if (R_ == 2 && kb == 2)
         return wtb_ ? launch_wtb_rk<2, 2>(t, gflag, gmask) : launch_fused_rk<2, 2>(t, gflag, gmask);
       if (R_ == 2) return launch_k1<2>(t, gflag, gmask);
+      if (R_ == 1 && kb == 2)
+        return wtb_ ? launch_wtb_rk<1, 2>(t, gflag, gmask) : launch_fused_rk<1, 2>(t, gflag, gmask);
+      if (R_ == 1) return launch_fused_rk<1, 1>(t, gflag, gmask);
       if (R_ == 6) return launch_k1<6>(t, gflag, gmask);
       throw Error(STB_ERR_ARG, "no fused kernel for this space order");
     }

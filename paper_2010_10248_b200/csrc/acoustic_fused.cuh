@@ -58,20 +58,23 @@ struct FusedCfg {
   static constexpr int NS1 = R + NSB;                 // staged u[t-1] planes
   static constexpr int E0 = HY0 * WZ0;
   static constexpr int E1 = HY1 * WZ1;
+  // TMA destinations start 128-byte aligned: slots and boxes padded to 32 floats
+  static constexpr int pad32(int v) { return (v + 31) / 32 * 32; }
+  static constexpr int E0S = pad32(E0);
   static constexpr int ebox(int j) { return (TY + 2 * hy(j)) * (TZ + 2 * hz(j)); }
   static constexpr int aux_floats() {
-    int s = E1;
-    for (int j = 1; j <= K; ++j) s += ebox(j);
+    int s = pad32(E1);
+    for (int j = 1; j <= K; ++j) s += pad32(ebox(j));
     return s;
   }
   static constexpr int AUX = aux_floats();
   static constexpr int aux_inv_off(int j) {
-    int s = E1;
-    for (int jj = 1; jj < j; ++jj) s += ebox(jj);
+    int s = pad32(E1);
+    for (int jj = 1; jj < j; ++jj) s += pad32(ebox(jj));
     return s;
   }
   static constexpr int NBUF = K > 1 ? (K - 1) : 0;
-  static constexpr size_t RING1 = (size_t)NS1 * E0 * 4;
+  static constexpr size_t RING1 = (size_t)NS1 * E0S * 4;
   static constexpr size_t RING2 = (size_t)NSB * AUX * 4;
   static constexpr size_t BUFS = (size_t)NBUF * 2 * E1 * 4;
   static constexpr size_t BARS = (size_t)(2 * NSB) * 8;
@@ -251,7 +254,7 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
           }
         }
         mbar_arrive_expect_tx(&full[sb], bytes);
-        tma_load_3d(ring1 + (size_t)(n % C::NS1) * C::E0, &maps.l0, z0 - C::hz(0),
+        tma_load_3d(ring1 + (size_t)(n % C::NS1) * C::E0S, &maps.l0, z0 - C::hz(0),
                     y0 - C::hy(0), ibase + n, &full[sb]);
         if (n >= 2 * R) {
           float* ab = ring2 + (size_t)sb * C::AUX;
@@ -412,7 +415,7 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
         mbar_wait_sleep(&full[sb], (uint32_t)((un / C::NSB) & 1u));
         if (work) {
           const float4 v =
-              *reinterpret_cast<const float4*>(ring1 + (size_t)(un % C::NS1) * C::E0 + off0);
+              *reinterpret_cast<const float4*>(ring1 + (size_t)(un % C::NS1) * C::E0S + off0);
           q[0][qq][0] = v.x; q[0][qq][1] = v.y; q[0][qq][2] = v.z; q[0][qq][3] = v.w;
         }
         const int cs = (qq - R + C::Q) % C::Q;          // centre slot (plane of level j)
@@ -424,7 +427,7 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
             const int p = ibase + n - R;
             float o[4] = {0.f, 0.f, 0.f, 0.f};
             if (work) {
-              const float* cen = ring1 + (size_t)((un - R) % C::NS1) * C::E0 + off0;
+              const float* cen = ring1 + (size_t)((un - R) % C::NS1) * C::E0S + off0;
               const float4 u04 = *reinterpret_cast<const float4*>(aux + off1);
               const float u0[4] = {u04.x, u04.y, u04.z, u04.w};
               float iv[4];

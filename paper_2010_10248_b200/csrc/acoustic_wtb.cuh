@@ -56,7 +56,9 @@ struct WtbCfg {
   static_assert(LV == 1 || LV == 2, "one or two levels per sweep");
   static constexpr int TY = TY_, TZ = 64;
   static constexpr int RP = kRoundUp4(R);
-  static constexpr int H1 = (LV - 1) * R;             // level-1 y halo
+  // level-1 y halo: R rows, rounded up so a thread's rows are all inside
+  // or all outside the tile
+  static constexpr int H1 = LV == 2 ? (R + RY - 1) / RY * RY : 0;
   static constexpr int HZ1 = LV == 2 ? RP : 0;        // level-1 z halo (float4 aligned)
   static constexpr int HZ0 = kRoundUp4(HZ1 + R);      // staged u[t-1] z halo
   static constexpr int HY1 = TY + 2 * H1, WZ1 = TZ + 2 * HZ1;
@@ -78,6 +80,8 @@ struct WtbCfg {
   static constexpr int NS1 = R + NSB;                 // staged u[t-1] planes
   static constexpr int NL = LV == 2 ? R + 2 : 0;      // level-1 plane ring
   static constexpr int E0 = HY0 * WZ0, E1 = HY1 * WZ1;
+  static_assert(E0 % 32 == 0 && E1 % 32 == 0 && (TY * WZ1) % 32 == 0 && (HY1 * WZ0) % 4 == 0,
+                "TMA destinations must stay 128-byte aligned");
   static constexpr int ET = TY * WZ1;                 // level-2 aux boxes: tile rows, WZ1 wide
   static constexpr int EL = HY1 * WZ0;                // level-1 ring plane (row stride WZ0)
   // u[t-2], inv (level 1); u[t-1], inv (level 2)
@@ -153,8 +157,13 @@ __device__ __forceinline__ void wtb_update(const float (&xq)[Q][RY][4], const in
     float win[4 + 2 * R];
     const float* cr = cen + r * W;
     {
+      // left part [-R, 0): scalar / float2 heads up to 16-byte alignment
       int d = -R;
-      if (R % 4 == 2) {
+      if (d & 1) {
+        win[d + R] = cr[d];
+        d += 1;
+      }
+      if (((d % 4) + 4) % 4 == 2) {
         const float2 v = *reinterpret_cast<const float2*>(cr + d);
         win[d + R] = v.x; win[d + R + 1] = v.y;
         d += 2;
@@ -166,16 +175,19 @@ __device__ __forceinline__ void wtb_update(const float (&xq)[Q][RY][4], const in
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) win[R + i] = xq[cs][r][i];
+      // right part [4, 4 + R): float4 body, float2 / scalar tails
       d = 4;
 #pragma unroll
       for (; d + 4 <= 4 + R; d += 4) {
         const float4 v = *reinterpret_cast<const float4*>(cr + d);
         win[d + R] = v.x; win[d + R + 1] = v.y; win[d + R + 2] = v.z; win[d + R + 3] = v.w;
       }
-      if (R % 4 == 2) {
+      if (d + 2 <= 4 + R) {
         const float2 v = *reinterpret_cast<const float2*>(cr + d);
         win[d + R] = v.x; win[d + R + 1] = v.y;
+        d += 2;
       }
+      if (d < 4 + R) win[d + R] = cr[d];
     }
 #pragma unroll
     for (int k = 1; k <= R; ++k) {
@@ -404,12 +416,12 @@ acoustic_wtb(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fused
   WtbLane<RY> L;
   L.init(a, work, ylo, zlo, in_tile);
   const int level = r1 ? 1 : 2;
-  L.src_init(a, work, tile * C::NTHR + (r1 ? t : C::NW1T + t), r1 ? x0 - C::H1 : x0, level);
+  L.src_init(a, work, tile * C::NTHR + (r1 ? t : C::NW1T + t), r1 ? x0 - (LV - 1) * R : x0, level);
   // CTA-uniform: does the level-1 region leave the grid?  Interior CTAs skip
   // the zero-halo masking.  (One level: nothing reads values outside the
   // grid, and they are never stored.)
-  const bool edge = LV == 2 && ((y0 - R < 0) || (y0 + TY + R > a.d.ny) || (z0 - C::HZ1 < 0) ||
-                                (z0 + TZ + C::HZ1 > a.d.nz));
+  const bool edge = LV == 2 && ((y0 - C::H1 < 0) || (y0 + TY + C::H1 > a.d.ny) ||
+                                (z0 - C::HZ1 < 0) || (z0 + TZ + C::HZ1 > a.d.nz));
 
   const int cnt = r1 ? N : N - 2 * R;
   const int noff = r1 ? 0 : 2 * R;
@@ -418,7 +430,8 @@ acoustic_wtb(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fused
   const int NS = r1 ? C::NS1 : C::NL;
   const int ES = r1 ? C::E0 : C::EL;
   const float* pring = r1 ? ring1 : lbuf;
-  const int offP = r1 ? (row + R) * W + 4 * g + (C::HZ0 - C::HZ1) : (row + R) * W + 4 * g + C::HZ1;
+  const int offP =
+      r1 ? (row + R) * W + 4 * g + (C::HZ0 - C::HZ1) : (row + C::H1) * W + 4 * g + C::HZ1;
   const int offA = r1 ? row * C::WZ1 + 4 * g : 2 * C::E1 + row * C::WZ1 + 4 * g + C::HZ1;
   const int invA = r1 ? C::E1 : C::ET;
   // this thread's (y, z) column in the output level; plane offsets added per store

@@ -231,7 +231,7 @@ def test_vs_oracle_random_medium_so8():
     assert_parity(res, ref.fields, ref.receivers, ref.checksum)
 
 
-@pytest.mark.parametrize("order", [4, 8])
+@pytest.mark.parametrize("order", [2, 4, 8])
 @pytest.mark.parametrize("k", [1, 2])
 def test_wavefront_kernel_multi_tile_dense_sources_vs_oracle(order, k):
     """Several y/z tiles with partial edge tiles (77 rows, 150 columns), a
