@@ -507,9 +507,9 @@ acoustic_wtb(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fused
             }
           }
           L.template epilogue<GUARD>(a, o, level, p, x0, x1, work);
-          if (p >= x0 && p < x1) L.store(a, dst, o, p);
           if (LV == 2 && r1) {
-            // hand the plane to level 2
+            // hand the plane to level 2 first (its warps wait on it), then
+            // the fire-and-forget HBM store
             if (c - 2 * R >= C::NL) STB_WTB_WAIT(&lempty[ls], (uint32_t)(lph ^ 1));
             if (work) {
               float* lb = lbuf + ls * C::EL + offW;
@@ -521,6 +521,7 @@ acoustic_wtb(const __grid_constant__ WtbMaps maps, const __grid_constant__ Fused
             mbar_arrive(&lfull[ls]);
             if (++ls == C::NL) { ls = 0; lph ^= 1; }
           }
+          if (p >= x0 && p < x1) L.store(a, dst, o, p);
         }
         if (!r1 && c >= R) {
           __syncwarp();
