@@ -527,8 +527,15 @@ class AcousticProp final : public stb_prop_s {
     STB_REQUIRE(k >= 0, STB_ERR_PLAN, "time_height must be >= 1");
     STB_REQUIRE(K_ == 0 || t0 + nsteps <= src_nt_, STB_ERR_ARG,
                 "run extends past the decomposed source series");
-    if (k == 0) autotune_k(t0);
-    const int kk = resolve_k(k);
+    // time_height = 0 and k not measured yet: time the first blocks of this
+    // very run (K = 1, 1, 2, 2 -- real steps, the second of each kind timed
+    // after its first-use costs) and continue with the faster; short runs
+    // use the separate idempotent trial (autotune_k)
+    bool trial = k == 0 && !tuned_k_ && path_ == Path::Fused && max_k_ >= 2 && nsteps >= 6 &&
+                 !std::getenv("STB_DEFAULT_K") &&
+                 !(std::getenv("STB_AUTOTUNE") && std::atoi(std::getenv("STB_AUTOTUNE")) == 0);
+    if (k == 0 && !trial) autotune_k(t0);
+    int kk = resolve_k(k);
     if (nrec_ && (int64_t)rec_dev_.n < nsteps * nrec_) rec_dev_.alloc(nsteps * nrec_);
     std::vector<int64_t> guard_steps;
     for (int64_t t = t0; t < t0 + nsteps; ++t)
@@ -544,8 +551,10 @@ class AcousticProp final : public stb_prop_s {
     std::vector<int64_t> chunk_end;           // exclusive step index (relative)
     size_t gi = 0;
     int64_t t = t0;
+    int64_t blk = 0;
     while (t < t0 + nsteps) {
-      const int kb = (int)std::min<int64_t>(path_ == Path::Fused ? kk : 1, t0 + nsteps - t);
+      const int want = trial ? (blk < 2 ? 1 : 2) : kk;
+      const int kb = (int)std::min<int64_t>(path_ == Path::Fused ? want : 1, t0 + nsteps - t);
       // guard steps inside this block
       int gmask = 0;
       int* gflag = nullptr;
@@ -624,6 +633,17 @@ class AcousticProp final : public stb_prop_s {
         }
       }
       t += kb;
+      if (trial && ++blk == 4) {
+        STB_CUDA(cudaEventSynchronize(events_[7]));
+        float m1 = 0.f, m2 = 0.f;
+        STB_CUDA(cudaEventElapsedTime(&m1, events_[2], events_[3]));   // block 1: K = 1
+        STB_CUDA(cudaEventElapsedTime(&m2, events_[6], events_[7]));   // block 3: K = 2
+        tune_ms_[0] = m1;
+        tune_ms_[1] = m2 / 2;
+        tuned_k_ = tune_ms_[1] < 0.95f * tune_ms_[0] ? 2 : 1;
+        kk = resolve_k(0);
+        trial = false;
+      }
     }
     if (nrec_) {                              // join the gather stream
       STB_CUDA(cudaEventRecord(sev_, gst_));
