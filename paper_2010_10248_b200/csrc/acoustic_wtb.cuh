@@ -1,42 +1,52 @@
-// Two-step wavefront temporal blocking with warp-specialised levels.
+// Wavefront temporal blocking with warp-specialised levels (LV = 2), and
+// the same machinery for a single level (LV = 1, measured slower than
+// acoustic_fused<R, 1>; kept behind STB_WTB1).
 //
 // The paper's wavefront schedule (Alg. 6, schedule.py:171-310) with
-// time-tile height 2, carried to one SM: a CTA owns a 16 x 64 (y, z) output
-// tile and an x chunk, sweeps x once, and produces u[t] and u[t+1] from one
-// read of u[t-1], u[t-2] and inv -- 20 B per point per two steps instead of
-// 2 x 16 B.  Level 2 lags level 1 by R planes (the skew of
-// schedule.py:139-168); level 1 is computed on the tile widened by R rows and
-// round_up4(R) columns (overlapped tiling: the halo is recomputed, never
-// exchanged).  Sources were turned by the inspector into per-thread entry
-// lists, so injection happens inside the sweep right after each level's
-// update -- the dependency that blocks temporal blocking with off-grid
-// sources is gone (precompute.py:209-252).
+// time-tile height 2, carried to one SM.  A CTA owns a TY x 64 (y, z) output
+// tile and an x chunk and sweeps x once.  It produces u[t] and u[t+1] from
+// one read of u[t-1], u[t-2] and inv: 20 B per point per two steps instead
+// of 2 x 16 B.  Level 2 lags level 1 by R planes (the skew of
+// schedule.py:139-168).  Level 1 is computed on the tile widened by H1 rows
+// (R rounded up to RY) and round_up4(R) columns: overlapped tiling, so the
+// halo is recomputed, never exchanged.  The inspector turned off-grid
+// sources into per-thread entry lists, so injection happens inside the sweep
+// right after each level's update.  That removes the dependency that blocks
+// temporal blocking with off-grid sources (precompute.py:209-252).
 //
-// Unlike the generic fused kernel (acoustic_fused.cuh), where the same
-// threads compute both levels and level 2 idles the halo threads behind a
-// CTA-wide barrier per plane, the levels run on separate warp groups:
+// Unlike acoustic_fused<R, 2>, where the same threads compute both levels
+// and level 2 idles the halo threads behind a CTA barrier per plane, the
+// levels run on separate warp groups:
 //
-//   producer warp : TMA of the u[t-1] plane (tile + 2R rows, OOB zero fill)
-//                   into an NS1-slot ring; per iteration the u[t-2]/inv boxes
-//                   of level 1 and the u[t-1]/inv boxes of level 2 into an
-//                   NSB-slot ring, all on one transaction mbarrier.
-//   level-1 warps : register queue of their own u[t-1] columns (x
-//                   neighbours), y/z neighbours from the staged plane; the
-//                   result goes to HBM (owned points) and to a shared ring
-//                   of NL level-1 planes (full/empty mbarriers per slot).
-//   level-2 warps : register queue of their level-1 columns read from that
-//                   ring, y/z neighbours from the ring; result to HBM.
+//   producer warp  TMA of the u[t-1] plane (level-1 region + R rows, OOB zero
+//                  fill) into an NS1-slot ring.  Per iteration it also loads
+//                  the u[t-2]/inv boxes of level 1 and the u[t-1]/inv boxes
+//                  of level 2 into an NSB-slot ring, all on one transaction
+//                  mbarrier.
+//   level-1 warps  Register queue of their own u[t-1] columns (x
+//                  neighbours), y/z neighbours from the staged plane.  Each
+//                  plane goes first to a shared ring of NL level-1 planes
+//                  (full/empty mbarriers per slot), then to HBM (owned
+//                  points).
+//   level-2 warps  Register queue of their level-1 columns read from that
+//                  ring, y/z neighbours from the ring; result to HBM.
+//                  (Letting only these warps release the producer's slots
+//                  -- their progress implies level 1's -- measured -2 %.)
 //
-// Each thread owns RY consecutive y rows x 4 consecutive z points, so the y
-// neighbours of its rows are loaded once (RY + 2R rows per RY x 4 points)
-// and the centre rows come from its queue: with RY = 2 a level update costs
-// 10 (level 1) / 9 (level 2) LDS.128 per 4 points, against 14 in the K = 1
-// kernel -- the shared-memory pipe, which bounds temporal blocking on B200
-// (DESIGN.md §6), carries fewer wavefronts per point-step than at K = 1.
+// Both groups run ONE role-parameterised code body.  Their rings share the
+// row stride, so shared addressing stays static.  Separate 9-way-unrolled
+// bodies (147 KB of SASS) stalled on instruction fetch.
+//
+// Each thread owns RY consecutive y rows x 4 consecutive z points.  The y
+// neighbours of its rows are loaded once (RY + 2R rows per RY x 4 points),
+// and the centre rows come from its queue.  With RY = 2 a level update
+// costs 10 (level 1) / 9 (level 2) LDS.128 per 4 points, against 14 in the
+// K = 1 kernel.
 //
 // Arithmetic: the reference's IEEE operation order (physics.py:199-213) on
-// packed fp32 pairs (sums FADD2, exact products FFMA2 with an opaque -0
-// addend; see f32x2.cuh); FAST contracts the Laplacian terms into FFMA2.
+// packed fp32 pairs: sums as FADD2, exact products as FFMA2 with an opaque
+// -0 addend (see f32x2.cuh).  FAST contracts the Laplacian terms into FFMA2.
+// Measured numbers and profile: DESIGN.md §6.
 #pragma once
 
 #include "acoustic_fused.cuh"
