@@ -17,7 +17,8 @@ import numpy as np
 from .errors import (ConfigError, DeviceError, InvalidPlanError, OutOfDomainError,
                      StabilityError)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libstb200.so")
+LIB_PATH = (os.environ.get("STB_LIB_PATH")      # A/B builds of the same sources
+            or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libstb200.so"))
 
 STB_OK, STB_ERR_ARG, STB_ERR_DOMAIN, STB_ERR_CUDA, STB_ERR_UNSTABLE, STB_ERR_PLAN, \
     STB_ERR_NOMEM, STB_ERR_CONFIG = range(8)
