@@ -217,6 +217,12 @@ int stb_prop_set_receivers(stb_prop_t p, const double* coords, int64_t nrec);
  * = the reference's: acoustic u, elastic txx (engine.py:327-332), TTI p.
  * Extension for BASELINE cfg5 (vx / vz receivers). */
 int stb_prop_set_receiver_field(stb_prop_t p, int32_t field);
+
+/* Sponge tables after creation (acoustic; replaces the desc's damp[]):
+ * _damp_factor's per-axis f64 tables (physics.py:66-115, engine.py:211-218),
+ * global x table as in the desc; NULL = no damping on that axis.  Lets the
+ * host compute v_max (the default decay needs it) while the model uploads. */
+int stb_prop_set_damping(stb_prop_t p, const double* fx, const double* fy, const double* fz);
 /* Advance steps [t0, t0 + nsteps), time_height steps fused per HBM pass
  * (schedule.py:171-207 semantics; 0 = library default).  rec_out, when not
  * NULL, receives the (nsteps, nrec) f64 traces.  On a non-finite field at a

@@ -31,6 +31,7 @@ EXPORTS = (
     "stb_support_decompose", "stb_support_destroy", "stb_acoustic_create",
     "stb_elastic_create", "stb_tti_create", "stb_prop_set_sources", "stb_prop_set_receivers", "stb_prop_run",
     "stb_prop_read_field", "stb_prop_level_ptr", "stb_prop_write_snapshot", "stb_prop_stream", "stb_prop_async_begin", "stb_prop_set_receiver_field",
+    "stb_prop_set_damping",
     "stb_prop_step_async", "stb_prop_gather_async", "stb_prop_async_finish", "stb_prop_reset", "stb_prop_stats",
     "stb_prop_describe",
     "stb_prop_destroy",
@@ -106,6 +107,7 @@ def _declare(lib):
         "stb_prop_write_snapshot": ([P, i32, i64, C.c_char_p], C.c_int),
         "stb_prop_stream": ([P, C.POINTER(P)], C.c_int),
         "stb_prop_set_receiver_field": ([P, i32], C.c_int),
+        "stb_prop_set_damping": ([P, pdbl, pdbl, pdbl], C.c_int),
         "stb_prop_async_begin": ([P, i64, i64], C.c_int),
         "stb_prop_step_async": ([P, i64, i32, i64, i64], C.c_int),
         "stb_prop_gather_async": ([P, i64, i32], C.c_int),

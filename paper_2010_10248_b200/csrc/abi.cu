@@ -225,6 +225,15 @@ STB_API int stb_prop_set_receiver_field(stb_prop_t p, int32_t field) {
   })
 }
 
+STB_API int stb_prop_set_damping(stb_prop_t p, const double* fx, const double* fy,
+                                 const double* fz) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr, STB_ERR_ARG, "NULL handle");
+    const double* t[3] = {fx, fy, fz};
+    p->set_damping(t);
+  })
+}
+
 STB_API int stb_prop_stream(stb_prop_t p, void** stream) {
   STB_GUARD({
     STB_REQUIRE(p != nullptr && stream != nullptr, STB_ERR_ARG, "NULL argument");

@@ -282,19 +282,22 @@ class AcousticProp final : public stb_prop_s {
     } else {
       inv_scalar_ = (T)desc.inv_scalar;
     }
-    has_fac_ = desc.damp[0] || desc.damp[1] || desc.damp[2];
+    set_damping(desc.damp);
+    choose_path();
+  }
+
+  void set_damping(const double* const* damp) override {
+    has_fac_ = damp[0] || damp[1] || damp[2];
     const int64_t n3[3] = {d_.nx, d_.ny, d_.nz};
     for (int a = 0; a < 3; ++a) {
-      fac_[a].alloc(n3[a]);
-      DevBuf<double> tmp(desc.damp[a] ? n3[a] : 0);
+      if (!fac_[a].p) fac_[a].alloc(n3[a]);
+      DevBuf<double> tmp(damp[a] ? n3[a] : 0);
       // the x table is global: take this slab's planes
-      if (desc.damp[a]) tmp.upload(desc.damp[a] + (a == 0 ? x_begin_ : 0), n3[a], st_);
-      table_kernel<T><<<g1(n3[a]), 256, 0, st_>>>(desc.damp[a] ? tmp.p : nullptr, n3[a],
-                                                  fac_[a].p);
+      if (damp[a]) tmp.upload(damp[a] + (a == 0 ? x_begin_ : 0), n3[a], st_);
+      table_kernel<T><<<g1(n3[a]), 256, 0, st_>>>(damp[a] ? tmp.p : nullptr, n3[a], fac_[a].p);
       STB_CHECK_LAUNCH();
       STB_CUDA(cudaStreamSynchronize(st_));
     }
-    choose_path();
   }
 
   ~AcousticProp() override {

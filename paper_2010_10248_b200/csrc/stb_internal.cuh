@@ -212,6 +212,7 @@ struct stb_prop_s {
   // host synchronisation; traces and guard flags stay on the device until
   // async_finish.  Default: unsupported.
   virtual void* stream() { return nullptr; }
+  virtual void set_damping(const double* const*) { throw_unsupported(); }
   virtual void async_begin(int64_t, int64_t) { throw_unsupported(); }
   virtual void step_async(int64_t, int, int64_t, int64_t) { throw_unsupported(); }
   virtual void gather_async(int64_t, int) { throw_unsupported(); }

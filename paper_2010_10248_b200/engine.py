@@ -331,6 +331,11 @@ class _Prop:
         _lib.check(_lib.lib().stb_prop_set_receivers(self.raw, _lib.dptr(c.reshape(-1)),
                                                      c.shape[0]))
 
+    def set_damping(self, tables):
+        t = [np.ascontiguousarray(a, dtype=np.float64) for a in tables] if tables else None
+        _lib.check(_lib.lib().stb_prop_set_damping(
+            self.raw, *((_lib.dptr(a) for a in t) if t else (_lib.dptr(None),) * 3)))
+
     def set_receiver_field(self, name):
         _lib.check(_lib.lib().stb_prop_set_receiver_field(self.raw, self.fields.index(name)))
 
@@ -407,17 +412,20 @@ def _as_f64_grid(values, grid: GridSpec, what: str):
     return arr
 
 
-def build_propagator(config: RunConfig, dt: float, v_max: float, x_begin: int = 0,
-                     nx_local: int = 0) -> _Prop:
+def build_propagator(config: RunConfig, dt: float, v_max: float | None, x_begin: int = 0,
+                     nx_local: int = 0, defer_damping: bool = False) -> _Prop:
     """Device model for a config (engine.py:235-255 + physics.py:124-278).
 
     ``x_begin``/``nx_local`` select an x slab (multi-GPU, see slabs.py): the
     geometry, sponge tables and sparse supports stay global; the medium is
     sliced to the slab's planes."""
     grid = config.grid
-    decay = (config.damping_decay if config.damping_decay is not None
-             else default_damping_decay(grid, v_max))
-    tables = damping_tables(grid, decay, dt)
+    if defer_damping:         # acoustic: tables follow via _Prop.set_damping
+        tables = None
+    else:
+        decay = (config.damping_decay if config.damping_decay is not None
+                 else default_damping_decay(grid, v_max))
+        tables = damping_tables(grid, decay, dt)
     keep = []
     if config.physics == "acoustic":
         d = _lib.AcousticDesc()
@@ -589,18 +597,11 @@ def _wavelets(config: RunConfig, dt: float, nt: int) -> np.ndarray:
     return np.repeat(base[:, None], spec.nsrc, axis=1)
 
 
-def run(config: RunConfig) -> RunResult:
-    """Execute a configured run on the GPU (engine.py:379-489 semantics)."""
-    _lib.require_device()
-    v_max = medium_velocity_bounds(config.physics, config.medium)
-    dt, nt = resolve_steps(config, v_max)
-    k = _gpu_time_height(config)
+def _host_sparse_prep(config: RunConfig, dt: float, nt: int):
+    """Host-only source/receiver checks and series (no device work)."""
     grid = config.grid
-    prop = build_propagator(config, dt, v_max)
-
-    t_pre0 = time.perf_counter()
-    nsrc = nrec = 0
     spec = config.sources
+    src = None
     if spec is not None and spec.nsrc > 0:
         validate_coords_in_extent(spec.coords, grid, what="source")
         wav = _wavelets(config, dt, nt)
@@ -610,6 +611,50 @@ def run(config: RunConfig) -> RunResult:
             scale = nearest_scales_from_velocity(spec.coords, grid, config.medium["vp"], dt)
         else:
             scale = np.full(spec.nsrc, dt)
+        src = (wav, scale)
+    if config.receiver_coords is not None and len(config.receiver_coords) > 0:
+        validate_coords_in_extent(config.receiver_coords, grid,
+                                  margin_points=grid.boundary_layers, what="receiver")
+    return src
+
+
+def run(config: RunConfig) -> RunResult:
+    """Execute a configured run on the GPU (engine.py:379-489 semantics)."""
+    _lib.require_device()
+    k = _gpu_time_height(config)
+    grid = config.grid
+    overlap = (config.physics == "acoustic" and config.dt is not None
+               and config.nt is not None and "velocity" in config.medium
+               and np.ndim(config.medium["velocity"]) > 0)
+    src_prep = None
+    if overlap:
+        # the model upload (inside the ctypes call, GIL released) overlaps the
+        # host's v_max (for the default sponge decay) and sparse-input checks;
+        # the sponge tables follow once v_max is known
+        from concurrent.futures import ThreadPoolExecutor
+        dt, nt = float(config.dt), int(config.nt)
+        with ThreadPoolExecutor(max_workers=1) as ex:
+            fut = ex.submit(build_propagator, config, dt, None, 0, 0, True)
+            try:
+                v_max = medium_velocity_bounds(config.physics, config.medium)
+                src_prep = _host_sparse_prep(config, dt, nt)
+            finally:
+                prop = fut.result()
+        decay = (config.damping_decay if config.damping_decay is not None
+                 else default_damping_decay(grid, v_max))
+        prop.set_damping(damping_tables(grid, decay, dt))
+    else:
+        v_max = medium_velocity_bounds(config.physics, config.medium)
+        dt, nt = resolve_steps(config, v_max)
+        prop = build_propagator(config, dt, v_max)
+
+    t_pre0 = time.perf_counter()
+    nsrc = nrec = 0
+    spec = config.sources
+    if not overlap:
+        src_prep = _host_sparse_prep(config, dt, nt)
+    if spec is not None and spec.nsrc > 0:
+        wav, scale = src_prep
         handle = _Handle.from_coords(spec.coords, grid, keep_zero=False)
         if nt > 0:
             prop.set_sources(handle, wav, scale, nt)
@@ -617,8 +662,6 @@ def run(config: RunConfig) -> RunResult:
     rec = None
     if config.receiver_coords is not None and len(config.receiver_coords) > 0:
         rc = config.receiver_coords
-        validate_coords_in_extent(rc, grid, margin_points=grid.boundary_layers,
-                                  what="receiver")
         prop.set_receivers(rc)
         if config.receiver_field is not None:
             prop.set_receiver_field(config.receiver_field)
