@@ -169,12 +169,40 @@ __device__ __forceinline__ void update4(const float (&xq)[Q][4], const int cs, c
     L01 = term2<FAST>(L01, pk(pp.x, pp.y), pk(mm.x, mm.y), cf.cy[r - 1], nz);
     L23 = term2<FAST>(L23, pk(pp.z, pp.w), pk(mm.z, mm.w), cf.cy[r - 1], nz);
   }
-  // z neighbours: window [z - RP, z + 4 + RP)
+  // z neighbours: window [z - RP, z + 4 + RP); only [z - R, z + 4 + R) is
+  // loaded (8-byte heads/tails where R is not a multiple of 4) and the
+  // centre comes from the queue
   float win[4 + 2 * RP];
+  {
+    int d = -R;
+    if (d & 1) {
+      win[RP + d] = cen[d];
+      d += 1;
+    }
+    if (((d % 4) + 4) % 4 == 2) {
+      const float2 v = *reinterpret_cast<const float2*>(cen + d);
+      win[RP + d] = v.x; win[RP + d + 1] = v.y;
+      d += 2;
+    }
 #pragma unroll
-  for (int w4 = 0; w4 < (4 + 2 * RP) / 4; ++w4) {
-    const float4 v = *reinterpret_cast<const float4*>(cen - RP + 4 * w4);
-    win[4 * w4] = v.x; win[4 * w4 + 1] = v.y; win[4 * w4 + 2] = v.z; win[4 * w4 + 3] = v.w;
+    for (; d < 0; d += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(cen + d);
+      win[RP + d] = v.x; win[RP + d + 1] = v.y; win[RP + d + 2] = v.z; win[RP + d + 3] = v.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) win[RP + i] = xq[cs][i];
+    d = 4;
+#pragma unroll
+    for (; d + 4 <= 4 + R; d += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(cen + d);
+      win[RP + d] = v.x; win[RP + d + 1] = v.y; win[RP + d + 2] = v.z; win[RP + d + 3] = v.w;
+    }
+    if (d + 2 <= 4 + R) {
+      const float2 v = *reinterpret_cast<const float2*>(cen + d);
+      win[RP + d] = v.x; win[RP + d + 1] = v.y;
+      d += 2;
+    }
+    if (d < 4 + R) win[RP + d] = cen[d];
   }
 #pragma unroll
   for (int r = 1; r <= R; ++r) {
