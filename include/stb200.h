@@ -197,6 +197,11 @@ typedef struct {
   int32_t arithmetic;        /* 0 = EXACT (the oracle's operation order,
                                 bitwise); 1 = FMA (contracted products, within
                                 1e-5 relative L2; fused f32 3-D kernel only)  */
+  int32_t raw_eps_delta;     /* 1: e2 / d2 carry epsilon / delta per point and
+                                the device forms 1 + 2 eps and
+                                sqrt(1 + 2 delta) in f64 (same IEEE ops)     */
+  const float* axis32[3];    /* precision 32: axis components already rounded
+                                to f32 on the host (overrides axis[a])      */
 } stb_tti_desc;
 
 int stb_acoustic_create(const stb_acoustic_desc* d, stb_prop_t* out);

@@ -70,7 +70,8 @@ class TTIDesc(C.Structure):
                 ("e2_scalar", C.c_double), ("d2", C.POINTER(C.c_double)),
                 ("d2_scalar", C.c_double), ("axis", C.POINTER(C.c_double) * 3),
                 ("axis_scalar", C.c_double * 3), ("damp", C.POINTER(C.c_double) * 3),
-                ("x_begin", C.c_int64), ("nx_local", C.c_int64), ("arithmetic", C.c_int32)]
+                ("x_begin", C.c_int64), ("nx_local", C.c_int64), ("arithmetic", C.c_int32),
+                ("raw_eps_delta", C.c_int32), ("axis32", C.POINTER(C.c_float) * 3)]
 
 
 _lock = threading.Lock()

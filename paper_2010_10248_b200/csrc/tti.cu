@@ -175,12 +175,31 @@ __global__ void tti_inv_kernel(const double* __restrict__ v, double dt2, PDims d
 }
 
 template <typename T>
-__global__ void tti_material_kernel(const double* __restrict__ src, PDims d, T* __restrict__ dst) {
+__global__ void tti_material_kernel(const double* __restrict__ src, PDims d, T* __restrict__ dst,
+                                    int mode) {
+  // mode 0: copy; 1: e2 = 1 + 2 eps; 2: d2 = sqrt(1 + 2 delta) -- the host's
+  // f64 NumPy expressions (physics.py tti_medium), each op correctly rounded
   const int64_t n = d.nx * d.ny * d.nz;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t z = i % d.nz, xy = i / d.nz;
-    dst[d.at(xy / d.ny, xy % d.ny, z)] = from_f64<T>(src[i]);
+    double v = src[i];
+    if (mode) {
+      v = __dadd_rn(1.0, __dmul_rn(2.0, v));
+      if (mode == 2) v = __dsqrt_rn(v);
+    }
+    dst[d.at(xy / d.ny, xy % d.ny, z)] = from_f64<T>(v);
+  }
+}
+
+// f32 axis components already rounded on the host (fp32 runs only)
+template <typename T>
+__global__ void tti_material32_kernel(const float* __restrict__ src, PDims d, T* __restrict__ dst) {
+  const int64_t n = d.nx * d.ny * d.nz;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = i % d.nz, xy = i / d.nz;
+    dst[d.at(xy / d.ny, xy % d.ny, z)] = (T)src[i];
   }
 }
 
@@ -243,7 +262,7 @@ class TtiProp final : public stb_prop_s {
       G_[ax].zero(st_);
     }
     const int64_t n = d_.nx * d_.ny * d_.nz;
-    auto material = [&](const double* h, double scalar, DevBuf<T>& dst, T& cf) {
+    auto material = [&](const double* h, double scalar, DevBuf<T>& dst, T& cf, int mode = 0) {
       if (!h) {
         cf = (T)scalar;
         return;
@@ -252,7 +271,16 @@ class TtiProp final : public stb_prop_s {
       tmp.upload(h, n, st_);
       dst.alloc(d_.total);
       dst.zero(st_);
-      tti_material_kernel<T><<<1184, 256, 0, st_>>>(tmp.p, d_, dst.p);
+      tti_material_kernel<T><<<1184, 256, 0, st_>>>(tmp.p, d_, dst.p, mode);
+      STB_CHECK_LAUNCH();
+      STB_CUDA(cudaStreamSynchronize(st_));
+    };
+    auto material32 = [&](const float* h, DevBuf<T>& dst) {
+      DevBuf<float> tmp(n);
+      tmp.upload(h, n, st_);
+      dst.alloc(d_.total);
+      dst.zero(st_);
+      tti_material32_kernel<T><<<1184, 256, 0, st_>>>(tmp.p, d_, dst.p);
       STB_CHECK_LAUNCH();
       STB_CUDA(cudaStreamSynchronize(st_));
     };
@@ -272,9 +300,17 @@ class TtiProp final : public stb_prop_s {
     } else {
       cf_.inv = (T)desc.inv_scalar;
     }
-    material(desc.e2, desc.e2_scalar, e2_, cf_.e2);
-    material(desc.d2, desc.d2_scalar, d2_, cf_.d2);
-    for (int ax = 0; ax < 3; ++ax) material(desc.axis[ax], desc.axis_scalar[ax], n_[ax], cf_.n[ax]);
+    // raw_eps_delta: the e2/d2 pointers carry epsilon/delta, formed here
+    material(desc.e2, desc.e2_scalar, e2_, cf_.e2, desc.raw_eps_delta ? 1 : 0);
+    material(desc.d2, desc.d2_scalar, d2_, cf_.d2, desc.raw_eps_delta ? 2 : 0);
+    for (int ax = 0; ax < 3; ++ax) {
+      if (desc.axis32[ax]) {
+        STB_REQUIRE(sizeof(T) == 4, STB_ERR_ARG, "f32 axis components need precision 32");
+        material32(desc.axis32[ax], n_[ax]);
+      } else {
+        material(desc.axis[ax], desc.axis_scalar[ax], n_[ax], cf_.n[ax]);
+      }
+    }
     has_fac_ = desc.damp[0] || desc.damp[1] || desc.damp[2];
     cx_ = 150;
     if (const char* e = std::getenv("STB_TTI_CX")) cx_ = std::max(1, std::atoi(e));

@@ -29,7 +29,7 @@ from . import _lib
 from .errors import ConfigError, InvalidPlanError
 from .grid import GridSpec, centered_first_weights, fd_weights, staggered_fd_weights
 from .physics import (_field_op, acoustic_coefficients, damping_tables, elastic_coefficients,
-                      par_max, par_max_of, ricker, tti_coefficients, tti_medium)
+                      par_max, par_max_of, ricker, tti_axis, tti_coefficients)
 from .precompute import _Handle
 from .sparse import nearest_scales_from_velocity, validate_coords_in_extent
 
@@ -510,7 +510,7 @@ def build_propagator(config: RunConfig, dt: float, v_max: float | None, x_begin:
 def _build_tti(config: RunConfig, dt: float, tables, x_begin: int, nx_local: int) -> _Prop:
     """TTI device model (csrc/tti.cu; repo-defined operator)."""
     grid = config.grid
-    med = tti_medium(config.medium, grid.shape)
+    mdict = config.medium
     d = _lib.TTIDesc()
     d.geom = _lib.geometry(grid)
     d.space_order, d.precision, d.dt, d.dt2 = config.space_order, config.precision, dt, dt ** 2
@@ -535,25 +535,45 @@ def _build_tti(config: RunConfig, dt: float, tables, x_begin: int, nx_local: int
         keep.append(a3)
         return _lib.dptr(a3.reshape(-1))
 
-    if np.ndim(med.vp):
-        d.velocity = local(med.vp, "vp")
+    vp = mdict["vp"]
+    if np.ndim(vp):
+        d.velocity = local(vp, "vp")
     else:
-        m = 1.0 / float(med.vp) ** 2
+        m = 1.0 / float(vp) ** 2
         if m <= 0.0:
             raise ValueError("m must be positive")
         d.inv_scalar = dt ** 2 / m
-    for name in ("e2", "d2"):
-        v = getattr(med, name)
-        if np.ndim(v):
-            setattr(d, name, local(v, name))
-        else:
-            setattr(d, f"{name}_scalar", float(v))
-    for a in range(3):
-        c = med.axis[a]
-        if np.ndim(c):
-            d.axis[a] = local(c, "axis")
-        else:
-            d.axis_scalar[a] = float(c)
+    # e2 = 1 + 2 eps and d2 = sqrt(1 + 2 delta) (physics.tti_medium): array
+    # fields go to the device raw and are formed there with the same f64 ops
+    d.raw_eps_delta = 1
+    eps, delta = mdict.get("epsilon", 0.0), mdict.get("delta", 0.0)
+    if np.ndim(eps):
+        d.e2 = local(eps, "epsilon")
+    else:
+        d.e2_scalar = 1.0 + 2.0 * float(eps)
+    if np.ndim(delta):
+        d.d2 = local(delta, "delta")
+    else:
+        d.d2_scalar = math.sqrt(1.0 + 2.0 * float(delta))
+    th, ph = mdict.get("theta", 0.0), mdict.get("phi", 0.0)
+    if np.ndim(th) == 0 and np.ndim(ph) == 0:
+        axis = tti_axis(th, ph)
+        for a in range(3):
+            d.axis_scalar[a] = float(axis[a])
+    elif config.precision == 32:
+        # rounded to f32 on the host (half the upload), bitwise the device's
+        # rounding of the f64 values
+        axis = tti_axis(th, ph, grid.shape, dtype=np.float32)
+        for a in range(3):
+            c = axis[a]
+            if nx_local:
+                c = np.ascontiguousarray(c[x_begin:x_begin + nx_local])
+            keep.append(c)
+            d.axis32[a] = c.ctypes.data_as(C.POINTER(C.c_float))
+    else:
+        axis = tti_axis(th, ph, grid.shape)
+        for a in range(3):
+            d.axis[a] = local(axis[a], "axis")
     if tables is not None:
         for a in range(3):
             keep.append(tables[a])

@@ -167,10 +167,12 @@ def _field_op(shape, fn, *inputs):
     return out
 
 
-def tti_axis(theta, phi, shape=None):
+def tti_axis(theta, phi, shape=None, dtype=np.float64):
     """Symmetry axis z-bar = (sin t cos p, sin t sin p, cos t) of the rotated
     frame of PAPER.md eq. 2 (x-bar = (cos t cos p, cos t sin p, -sin t)), f64.
-    With ``shape`` (grid shape) array inputs are evaluated on host threads."""
+    With ``shape`` (grid shape) array inputs are evaluated on host threads;
+    ``dtype=np.float32`` stores the f64 results rounded once to f32 (the
+    device's own rounding of the f64 values)."""
     th = np.asarray(theta, dtype=np.float64)
     ph = np.asarray(phi, dtype=np.float64)
     if shape is None or (th.ndim == 0 and ph.ndim == 0):
@@ -179,7 +181,7 @@ def tti_axis(theta, phi, shape=None):
     # calls on the same values as above, so the results are identical)
     tb = np.broadcast_to(th, shape)
     pb = np.broadcast_to(ph, shape)
-    out = tuple(np.empty(shape, dtype=np.float64) for _ in range(3))
+    out = tuple(np.empty(shape, dtype=dtype) for _ in range(3))
 
     def work(lo, hi):
         t, p = tb[lo:hi], pb[lo:hi]
