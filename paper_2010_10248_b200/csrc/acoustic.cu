@@ -846,7 +846,7 @@ class AcousticProp final : public stb_prop_s {
   // level-1 redundancy 1.31 instead of 1.41), 16 at R = 4 (160 registers x 12
   // warps).  One level: 32 (8 consumer warps of 2 rows x 4 z points).
   static constexpr int wtb_ty(int R, int LV = 2) {
-    return LV == 1 ? 32 : kWtbTYOverride ? kWtbTYOverride : (R <= 2 ? 24 : 16);
+    return LV == 1 ? (R == 6 ? 28 : 32) : kWtbTYOverride ? kWtbTYOverride : (R <= 2 ? 24 : 16);
   }
   // TMA prefetch depth: R = 6 stages 40% larger planes; PF = 2 keeps two
   // CTAs per SM resident (smem), PF = 3 elsewhere.
