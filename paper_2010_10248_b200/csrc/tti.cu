@@ -311,7 +311,6 @@ class TtiProp final : public stb_prop_s {
         material(desc.axis[ax], desc.axis_scalar[ax], n_[ax], cf_.n[ax]);
       }
     }
-    has_fac_ = desc.damp[0] || desc.damp[1] || desc.damp[2];
     cx_ = 150;
     if (const char* e = std::getenv("STB_TTI_CX")) cx_ = std::max(1, std::atoi(e));
     if (fused_) {
@@ -331,12 +330,18 @@ class TtiProp final : public stb_prop_s {
       STB_CUDA(cudaStreamSynchronize(st_));
       setup_fused();
     }
+    set_damping(desc.damp);
+  }
+
+  // sponge tables (also after creation: stb_prop_set_damping)
+  void set_damping(const double* const* damp) override {
+    has_fac_ = damp[0] || damp[1] || damp[2];
     const int64_t n3[3] = {d_.nx, d_.ny, d_.nz};
     for (int ax = 0; ax < 3; ++ax) {
-      fac_[ax].alloc(n3[ax]);
-      DevBuf<double> tmp(desc.damp[ax] ? n3[ax] : 0);
-      if (desc.damp[ax]) tmp.upload(desc.damp[ax] + (ax == 0 ? x_begin_ : 0), n3[ax], st_);
-      pad_table_kernel<T><<<g1t(n3[ax]), 256, 0, st_>>>(desc.damp[ax] ? tmp.p : nullptr, n3[ax],
+      if (!fac_[ax].p) fac_[ax].alloc(n3[ax]);
+      DevBuf<double> tmp(damp[ax] ? n3[ax] : 0);
+      if (damp[ax]) tmp.upload(damp[ax] + (ax == 0 ? x_begin_ : 0), n3[ax], st_);
+      pad_table_kernel<T><<<g1t(n3[ax]), 256, 0, st_>>>(damp[ax] ? tmp.p : nullptr, n3[ax],
                                                         fac_[ax].p);
       STB_CHECK_LAUNCH();
       STB_CUDA(cudaStreamSynchronize(st_));

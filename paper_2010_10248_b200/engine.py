@@ -413,7 +413,8 @@ def _as_f64_grid(values, grid: GridSpec, what: str):
 
 
 def build_propagator(config: RunConfig, dt: float, v_max: float | None, x_begin: int = 0,
-                     nx_local: int = 0, defer_damping: bool = False) -> _Prop:
+                     nx_local: int = 0, defer_damping: bool = False,
+                     host_done=None) -> _Prop:
     """Device model for a config (engine.py:235-255 + physics.py:124-278).
 
     ``x_begin``/``nx_local`` select an x slab (multi-GPU, see slabs.py): the
@@ -464,7 +465,7 @@ def build_propagator(config: RunConfig, dt: float, v_max: float | None, x_begin:
         _lib.check(_lib.lib().stb_acoustic_create(C.byref(d), C.byref(raw)))
         return _Prop(raw, config.dtype, ACOUSTIC_FIELDS)
     if config.physics == "tti":
-        return _build_tti(config, dt, tables, x_begin, nx_local)
+        return _build_tti(config, dt, tables, x_begin, nx_local, host_done)
     if getattr(config.schedule, "arithmetic", "exact") != "exact":
         raise ConfigError("schedule.arithmetic",
                           "elastic kernels run the reference's exact operation order only")
@@ -507,7 +508,8 @@ def build_propagator(config: RunConfig, dt: float, v_max: float | None, x_begin:
     return _Prop(raw, config.dtype, ELASTIC_FIELDS)
 
 
-def _build_tti(config: RunConfig, dt: float, tables, x_begin: int, nx_local: int) -> _Prop:
+def _build_tti(config: RunConfig, dt: float, tables, x_begin: int, nx_local: int,
+               host_done=None) -> _Prop:
     """TTI device model (csrc/tti.cu; repo-defined operator)."""
     grid = config.grid
     mdict = config.medium
@@ -578,6 +580,8 @@ def _build_tti(config: RunConfig, dt: float, tables, x_begin: int, nx_local: int
         for a in range(3):
             keep.append(tables[a])
             d.damp[a] = _lib.dptr(tables[a])
+    if host_done is not None:       # host-side model prep finished: the caller
+        host_done.set()             # may use the CPU while the model uploads
     raw = C.c_void_p()
     _lib.check(_lib.lib().stb_tti_create(C.byref(d), C.byref(raw)))
     return _Prop(raw, config.dtype, TTI_FIELDS)
@@ -643,19 +647,25 @@ def run(config: RunConfig) -> RunResult:
     _lib.require_device()
     k = _gpu_time_height(config)
     grid = config.grid
-    overlap = (config.physics == "acoustic" and config.dt is not None
-               and config.nt is not None and "velocity" in config.medium
-               and np.ndim(config.medium["velocity"]) > 0)
+    vkey = {"acoustic": "velocity", "tti": "vp"}.get(config.physics)
+    overlap = (vkey is not None and config.dt is not None and config.nt is not None
+               and vkey in config.medium and np.ndim(config.medium[vkey]) > 0)
     src_prep = None
     if overlap:
         # the model upload (inside the ctypes call, GIL released) overlaps the
         # host's v_max (for the default sponge decay) and sparse-input checks;
-        # the sponge tables follow once v_max is known
+        # the sponge tables follow once v_max is known.  TTI's own host prep
+        # (symmetry-axis trig) is CPU-bound: wait for it to finish first.
+        import threading
         from concurrent.futures import ThreadPoolExecutor
         dt, nt = float(config.dt), int(config.nt)
+        host_done = threading.Event()
         with ThreadPoolExecutor(max_workers=1) as ex:
-            fut = ex.submit(build_propagator, config, dt, None, 0, 0, True)
+            fut = ex.submit(build_propagator, config, dt, None, 0, 0, True, host_done)
             try:
+                if config.physics == "tti":
+                    while not host_done.wait(0.005) and not fut.done():
+                        pass
                 v_max = medium_velocity_bounds(config.physics, config.medium)
                 src_prep = _host_sparse_prep(config, dt, nt)
             finally:
