@@ -116,6 +116,55 @@ def test_repeat_determinism():
     assert a.report.checksum == b.report.checksum
 
 
+@pytest.mark.parametrize("physics", ["acoustic", "tti"])
+def test_overlapped_setup_matches_sequential(physics):
+    """run() with dt and nt given uploads the model while the host computes
+    v_max and checks the sparse inputs, and supplies the sponge tables
+    afterwards (stb_prop_set_damping).  The result must be bitwise that of
+    the sequential setup, which runs when dt comes from the CFL bound."""
+    rng = np.random.default_rng(41)
+    shape = (30, 34, 40)
+    grid = stb.GridSpec(shape, (10.0,) * 3, (0.0, 0.0, 0.0), boundary_layers=6)
+    v = 1800.0 + 900.0 * rng.random(shape)
+    if physics == "tti":
+        medium = {"vp": v, "epsilon": 0.2 * rng.random(shape), "delta": 0.05,
+                  "theta": 0.3 * rng.random(shape), "phi": 0.2}
+        so_ = 8
+    else:
+        medium = {"velocity": v}
+        so_ = 4
+    src = stb.SourceSpec(random_coords(rng, shape, grid.spacing, grid.origin, 3, margin=2),
+                         f0=20.0)
+    rec = random_coords(rng, shape, grid.spacing, grid.origin, 9, margin=6)
+    seq = stb.run(stb.RunConfig(physics=physics, grid=grid, space_order=so_, time_ms=30.0,
+                                medium=medium, sources=src, receiver_coords=rec))
+    ovl = stb.run(stb.RunConfig(physics=physics, grid=grid, space_order=so_, nt=seq.report.nt,
+                                dt=seq.report.dt, medium=medium, sources=src,
+                                receiver_coords=rec))
+    for k in seq.fields:
+        np.testing.assert_array_equal(ovl.fields[k], seq.fields[k])
+    np.testing.assert_array_equal(ovl.receivers, seq.receivers)
+
+
+def test_in_run_k_measurement_picks_blocking_at_so2():
+    """time_height=0 on a run of >= 6 steps measures K=1 and K=2 on its own
+    first blocks.  At so=2, where temporal blocking wins on B200, it keeps
+    K=2, and the fields are bitwise those of a pinned K=1 run."""
+    rng = np.random.default_rng(43)
+    shape = (192, 256, 256)
+    grid = stb.GridSpec(shape, (10.0,) * 3, (0.0, 0.0, 0.0), boundary_layers=8)
+    v = 2000.0 + 500.0 * rng.random(shape)
+    src = stb.SourceSpec(random_coords(rng, shape, grid.spacing, grid.origin, 20, margin=2),
+                         f0=20.0)
+    base = dict(physics="acoustic", grid=grid, space_order=2, nt=40, dt=1.0e-3,
+                medium={"velocity": v}, sources=src)
+    tuned = stb.run(stb.RunConfig(**base, schedule=stb.ScheduleSpec("gpu", time_height=0)))
+    pinned = stb.run(stb.RunConfig(**base, schedule=stb.ScheduleSpec("gpu", time_height=1)))
+    np.testing.assert_array_equal(tuned.fields["u"], pinned.fields["u"])
+    plan = tuned.report.schedule["device_plan"]
+    assert "autotuned" in plan and "k=2" in plan, plan
+
+
 # ------------------------------------------------------------------ inspector
 
 def test_interp_stencils_bitexact(golden_misc):
