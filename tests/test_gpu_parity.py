@@ -348,7 +348,7 @@ def test_cfg1_fma_mode_tolerance(golden_big):
 # ------------------------------------------------- x-slab device mechanics
 
 @pytest.mark.parametrize("kind,k", [("acoustic", 1), ("acoustic", 2), ("elastic", 1),
-                                    ("tti", 1)])
+                                    ("tti", 1), ("acoustic_so2", 2), ("acoustic_so4", 2)])
 def test_xslab_handles_emulated_two_ranks(kind, k):
     """Two x-slab handles on one GPU, ghost planes exchanged by device
     copies in the order slabs.SlabRunner uses (NCCL replaced by copies: two

@@ -22,7 +22,7 @@ def _free_port():
     return port
 
 
-def _case(k):
+def _case(k, so=8):
     import paper_2010_10248_b200 as stb
     rng = np.random.default_rng(5)
     shape = (36, 20, 24)
@@ -33,7 +33,7 @@ def _case(k):
     rec = random_coords(rng, shape, grid.spacing, grid.origin, 12, margin=5)
     rec[0] = [115.5, 100.0, 110.0]          # base plane 11, straddles x = 12
     rec[1] = [175.0, 100.0, 110.0]          # on plane 17.5 -> base 17
-    return stb.RunConfig(physics="acoustic", grid=grid, space_order=8, nt=14,
+    return stb.RunConfig(physics="acoustic", grid=grid, space_order=so, nt=14,
                          medium={"velocity": v}, sources=stb.SourceSpec(src, f0=25.0),
                          receiver_coords=rec,
                          schedule=stb.ScheduleSpec("gpu", time_height=k))
@@ -68,6 +68,8 @@ def _tti_case():
 
 
 def _make(kind, k):
+    if kind.startswith("acoustic_so"):            # acoustic at another space order
+        return _case(k, int(kind[len("acoustic_so"):]))
     if kind == "tti":
         return _tti_case()
     if kind == "elastic_vz":
