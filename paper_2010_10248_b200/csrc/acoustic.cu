@@ -8,10 +8,14 @@
 // with fac = min(fx[x], fy[y], fz[z]) == f(1/(1+dt*max_a profile_a)) bit for
 // bit (1-D tables), so the sponge costs no HBM stream.
 //
-// Three device paths, all bitwise equal in EXACT mode:
-//   fused      acoustic_fused<R,K,...>: K = time_height steps per HBM pass
-//              (fp32, 3-D grids, R in {2,4,6}); injection and receiver
-//              capture fused into the sweep.
+// Device paths, all bitwise equal in EXACT mode:
+//   fused      fp32, 3-D grids, R in {1, 2, 4, 6}; source injection fused
+//              into the sweep, receivers gathered on a second stream.
+//              K = 1: acoustic_fused<R,1> (the default; ~91 % of HBM at so=8).
+//              K = 2: acoustic_wtb<R,2> (acoustic_wtb.cuh), the two-level
+//              wavefront kernel with warp-specialised levels; the older
+//              acoustic_fused<R,2> stays behind STB_WTB=0.  time_height = 0
+//              measures K on the run's first blocks.
 //   tiled      acoustic_tiled_step: one step per launch (kept for A/B).
 //   reference  thread-per-point kernel for fp64 and degenerate grids.
 // Time level t lives in buffer t mod NB (NB = 6: distinct inputs/outputs
