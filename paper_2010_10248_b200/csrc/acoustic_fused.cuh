@@ -46,6 +46,7 @@ struct FusedCfg {
   static constexpr int hy(int j) { return (K - j) * R; }
   static constexpr int hz(int j) { return j >= K ? 0 : kRoundUp4(hz(j + 1) + R); }
   static constexpr int RP = kRoundUp4(R);
+  static constexpr int TY_ = TY;
   static constexpr int HY0 = TY + 2 * hy(0), WZ0 = TZ + 2 * hz(0);   // staged u[t-1]
   static constexpr int HY1 = TY + 2 * hy(1), WZ1 = TZ + 2 * hz(1);   // thread grid
   static constexpr int G1 = WZ1 / 4;
@@ -79,6 +80,9 @@ struct FusedCfg {
   static constexpr size_t BUFS = (size_t)NBUF * 2 * E1 * 4;
   static constexpr size_t BARS = (size_t)(2 * NSB) * 8;
   static constexpr size_t SMEM = RING1 + RING2 + BUFS + BARS;
+  // resident CTAs per SM the launch bounds ask for: two for the 9-warp
+  // K = 1 tiles (and the K = 2 R <= 2 kernel), one otherwise
+  static constexpr int MINB = K == 1 ? (NT <= 320 ? 2 : 1) : (R <= 2 ? 2 : 1);
 };
 
 struct FusedMaps {
@@ -235,7 +239,7 @@ __device__ __forceinline__ void update4(const float (&xq)[Q][4], const int cs, c
 }
 
 template <int R, int K, int TY, int TZ, int PF, bool FAST, bool GUARD>
-__global__ void __launch_bounds__(FusedCfg<R, K, TY, TZ, PF>::NT, (K == 1 || R <= 2 ? 2 : 1))
+__global__ void __launch_bounds__(FusedCfg<R, K, TY, TZ, PF>::NT, FusedCfg<R, K, TY, TZ, PF>::MINB)
 acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ FusedArgs a) {
   using C = FusedCfg<R, K, TY, TZ, PF>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
