@@ -238,6 +238,10 @@ constexpr int kWtbTYOverride = STB_WTB_TY;   // build-time A/B of the tile heigh
 #define STB_FUSED_TY6 32
 #endif
 constexpr int kFusedTY6 = STB_FUSED_TY6;     // acoustic_fused<6,1> tile height (0: 16)
+#ifndef STB_PF6
+#define STB_PF6 3
+#endif
+constexpr int kPF6 = STB_PF6;                // its TMA prefetch depth (one CTA per SM)
 
 }  // namespace
 
@@ -861,7 +865,9 @@ class AcousticProp final : public stb_prop_s {
   }
   // TMA prefetch depth: R = 6 stages 40% larger planes; PF = 2 keeps two
   // CTAs per SM resident (smem), PF = 3 elsewhere.
-  static constexpr int pf_for(int R, int K = 1) { return (R >= 6 || (R <= 2 && K > 1)) ? 2 : 3; }
+  static constexpr int pf_for(int R, int K = 1) {
+    return R >= 6 ? (fused_ty(R) == kTY ? 2 : kPF6) : ((R <= 2 && K > 1) ? 2 : 3);
+  }
 
   int slot(int64_t t) const { return (int)(((t % NB) + NB) % NB); }
 
