@@ -234,14 +234,10 @@ constexpr int kWtbRYOverride = STB_WTB_RY;   // build-time A/B of the rows per t
 #define STB_WTB_TY 0
 #endif
 constexpr int kWtbTYOverride = STB_WTB_TY;   // build-time A/B of the tile height
-#ifndef STB_FUSED_TY6
-#define STB_FUSED_TY6 32
+#ifndef STB_FUSED_TY1
+#define STB_FUSED_TY1 32
 #endif
-constexpr int kFusedTY6 = STB_FUSED_TY6;     // acoustic_fused<6,1> tile height (0: 16)
-#ifndef STB_PF6
-#define STB_PF6 3
-#endif
-constexpr int kPF6 = STB_PF6;                // its TMA prefetch depth (one CTA per SM)
+constexpr int kFusedTY1 = STB_FUSED_TY1;     // acoustic_fused<R,1> tile height (0: 16)
 
 }  // namespace
 
@@ -380,7 +376,7 @@ class AcousticProp final : public stb_prop_s {
     const int hy = (max_k_ - 1) * R_;
     int hz = 0;
     for (int j = 1; j < max_k_; ++j) hz = (hz + R_ + 3) / 4 * 4;
-    src_n_ = tile_lists(fused_ty(R_), kTZ, hy, hz, src_list_, src_tile_ptr_);
+    src_n_ = tile_lists(fused_ty(R_, 1), kTZ, hy, hz, src_list_, src_tile_ptr_);
     thr_.clear();
     wtb_thr_[0].reset();
     wtb_thr_[1].reset();
@@ -436,15 +432,31 @@ class AcousticProp final : public stb_prop_s {
     if (!K_ || src_n_ == 0) return nullptr;
     auto it = thr_.find(K);
     if (it != thr_.end()) return it->second.get();
-    using C = FusedCfg<R, K, fused_ty(R), kTZ, pf_for(R, K)>;
+    using C = FusedCfg<R, K, fused_ty(R, K), kTZ, pf_for(R, K)>;
     const int nty = (int)((d_.ny + C::TY_ - 1) / C::TY_), ntz = (int)((d_.nz + kTZ - 1) / kTZ);
     const int ntiles = nty * ntz;
-    const int64_t n = src_n_;
+    // the legacy K = 2 kernel tiles differently from the global lists
+    DevBuf<int4> own_list;
+    DevBuf<int> own_ptr;
+    const int4* tl = src_list_.p;
+    const int* tp = src_tile_ptr_.p;
+    int64_t n = src_n_;
+    if (C::TY_ != fused_ty(R, 1)) {
+      n = tile_lists(C::TY_, kTZ, C::hy(1), C::hz(1), own_list, own_ptr);
+      tl = own_list.p;
+      tp = own_ptr.p;
+    }
+    auto L = std::make_unique<ThrLists>();
+    if (n == 0) {
+      L->ptr.alloc(ntiles * C::NWORK + 1);
+      L->ptr.zero(st_);
+      STB_CUDA(cudaStreamSynchronize(st_));
+      return thr_.emplace(K, std::move(L)).first->second.get();
+    }
     DevBuf<int> key(n), key2(n);
     DevBuf<int2> val(n);
-    auto L = std::make_unique<ThrLists>();
     L->list.alloc(n);
-    thr_key_kernel<<<g1(n), 256, 0, st_>>>(src_list_.p, src_tile_ptr_.p, ntiles, n, ntz, C::TY_,
+    thr_key_kernel<<<g1(n), 256, 0, st_>>>(tl, tp, ntiles, n, ntz, C::TY_,
                                            kTZ, C::hy(1), C::hz(1), C::HY1, C::G1, key.p, val.p);
     STB_CHECK_LAUNCH();
     size_t tb = 0;
@@ -476,7 +488,7 @@ class AcousticProp final : public stb_prop_s {
     const int4* tl = src_list_.p;
     const int* tp = src_tile_ptr_.p;
     int64_t ne = src_n_;
-    if (C::TY != fused_ty(R) || C::H1 != (max_k_ - 1) * R || C::HZ1 != (max_k_ > 1 ? (R + 3) / 4 * 4 : 0)) {
+    if (C::TY != fused_ty(R, 1) || C::H1 != (max_k_ - 1) * R || C::HZ1 != (max_k_ > 1 ? (R + 3) / 4 * 4 : 0)) {
       ne = tile_lists(C::TY, kTZ, C::H1, C::HZ1, own_list, own_ptr);
       tl = own_list.p;
       tp = own_ptr.p;
@@ -833,7 +845,7 @@ class AcousticProp final : public stb_prop_s {
       if (k == 0 && tuned_k_ && tune_ms_[0] > 0.f)
         os << " autotuned(ms/step k1=" << tune_ms_[0] << " k2=" << tune_ms_[1] << ")";
     } else if (path_ == Path::Fused) {
-      os << "acoustic_fused<f32,R=" << R_ << ",TY=" << fused_ty(R_) << ",TZ=" << kTZ << ",PF=" << pf_for(R_, resolve_k(k))
+      os << "acoustic_fused<f32,R=" << R_ << ",TY=" << fused_ty(R_, kk) << ",TZ=" << kTZ << ",PF=" << pf_for(R_, resolve_k(k))
          << "," << (fast_ ? "fma" : "exact") << "> k=" << kk << " cx=" << cx_len_
          << " bytes_per_point=" << (kk == 1 ? 16 : 20);
       if (k == 0 && tuned_k_ && tune_ms_[0] > 0.f)
@@ -850,9 +862,13 @@ class AcousticProp final : public stb_prop_s {
  private:
   enum class Path { Reference, Tiled, Fused };
   static constexpr int kTY = 16, kTZ = 64;
-  // fused-kernel tile height: 32 at R = 6 (one CTA of 16 consumer warps,
-  // less y halo per staged plane), 16 elsewhere (two CTAs per SM)
-  static constexpr int fused_ty(int R) { return (R == 6 && kFusedTY6 > 0) ? kFusedTY6 : kTY; }
+  // fused-kernel tile height.  K = 1: 32 rows in one CTA of 16 consumer
+  // warps -- less y halo per staged plane and room for a deeper prefetch
+  // (measured +1 % at so=4/8 and +10 % at so=12 over two 16-row CTAs per
+  // SM); the legacy K = 2 kernel (STB_WTB=0) keeps 16-row tiles.
+  static constexpr int fused_ty(int, int K = 1) {
+    return K == 1 ? (kFusedTY1 > 0 ? kFusedTY1 : kTY) : kTY;
+  }
   static constexpr int kWtbPF = 3;                // two-level kernel: TMA prefetch depth
   // rows per thread: 2 (measured at R = 2: RY = 1 gives 21 warps instead of
   // 11 but doubles the per-plane bookkeeping per point, 274 vs 328 GPts/s)
@@ -863,10 +879,12 @@ class AcousticProp final : public stb_prop_s {
   static constexpr int wtb_ty(int R, int LV = 2) {
     return LV == 1 ? (R == 6 ? 28 : 32) : kWtbTYOverride ? kWtbTYOverride : (R <= 2 ? 24 : 16);
   }
-  // TMA prefetch depth: R = 6 stages 40% larger planes; PF = 2 keeps two
-  // CTAs per SM resident (smem), PF = 3 elsewhere.
+  // TMA prefetch depth.  One-CTA 32-row K = 1 tiles: 4 (R <= 4), 3 (R = 6,
+  // whose planes are 40 % larger; measured 4 > 3, 5 at so=8).  Two-CTA
+  // 16-row tiles: 3, and 2 at R = 6 or for the legacy K = 2 at R <= 2.
   static constexpr int pf_for(int R, int K = 1) {
-    return R >= 6 ? (fused_ty(R) == kTY ? 2 : kPF6) : ((R <= 2 && K > 1) ? 2 : 3);
+    if (K == 1 && fused_ty(R, 1) != kTY) return R >= 6 ? 3 : 4;
+    return (R >= 6 || (R <= 2 && K > 1)) ? 2 : 3;
   }
 
   int slot(int64_t t) const { return (int)(((t % NB) + NB) % NB); }
@@ -979,7 +997,7 @@ class AcousticProp final : public stb_prop_s {
 
   template <int R, int K>
   void fused_maps(FusedMaps& m, int s_l0, int s_lm1) {
-    using Cf = FusedCfg<R, K, fused_ty(R), kTZ, pf_for(R, K)>;
+    using Cf = FusedCfg<R, K, fused_ty(R, K), kTZ, pf_for(R, K)>;
     m.l0 = make_map3d_f32(reinterpret_cast<const float*>(lvl_[s_l0].p), d_, Cf::WZ0, Cf::HY0, 1);
     m.lm1 = make_map3d_f32(reinterpret_cast<const float*>(lvl_[s_lm1].p), d_, Cf::WZ1, Cf::HY1, 1);
     if (inv_.p) {
@@ -994,8 +1012,8 @@ class AcousticProp final : public stb_prop_s {
                        int cx = 0) {
     if (x_hi < 0) x_hi = (int)d_.nx;
     if (cx <= 0)
-      cx = chunk_len(x_hi - x_lo, K, FusedCfg<R, K, fused_ty(R), kTZ, pf_for(R, K)>::MINB,
-                     fused_ty(R));
+      cx = chunk_len(x_hi - x_lo, K, FusedCfg<R, K, fused_ty(R, K), kTZ, pf_for(R, K)>::MINB,
+                     fused_ty(R, K));
     // tensor maps are cached per (K, input slots)
     const int s_l0 = slot(t - 1), s_lm1 = slot(t - 2);
     const int key = (K * NB + s_l0) * NB + s_lm1;
@@ -1033,9 +1051,9 @@ class AcousticProp final : public stb_prop_s {
     a.guard_mask = gmask;
     const int nch = (x_hi - x_lo + cx - 1) / cx;
     if (fast_)
-      FusedLauncher<R, K, fused_ty(R), kTZ, pf_for(R, K), true>::launch(st_, it->second, a, nch);
+      FusedLauncher<R, K, fused_ty(R, K), kTZ, pf_for(R, K), true>::launch(st_, it->second, a, nch);
     else
-      FusedLauncher<R, K, fused_ty(R), kTZ, pf_for(R, K), false>::launch(st_, it->second, a, nch);
+      FusedLauncher<R, K, fused_ty(R, K), kTZ, pf_for(R, K), false>::launch(st_, it->second, a, nch);
   }
 
   // Wavefront kernel (acoustic_wtb.cuh): LV = 1 or 2 steps per pass.
