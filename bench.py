@@ -210,6 +210,80 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None}
 
 
+def host_cpu_info() -> dict:
+    """CPU model, logical and physical core counts of this host."""
+    model, phys = None, set()
+    try:
+        cur = {}
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if ":" not in line:
+                    if "physical id" in cur or "core id" in cur:
+                        phys.add((cur.get("physical id"), cur.get("core id")))
+                    cur = {}
+                    continue
+                k, v = (x.strip() for x in line.split(":", 1))
+                cur[k] = v
+                if k == "model name" and model is None:
+                    model = v
+        if "physical id" in cur or "core id" in cur:
+            phys.add((cur.get("physical id"), cur.get("core id")))
+    except OSError:
+        pass
+    n_phys = len(phys) or None
+    if n_phys is None:
+        try:
+            import psutil
+            n_phys = psutil.cpu_count(logical=False)
+        except Exception:
+            n_phys = None
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "physical_cores": n_phys}
+
+
+def self_launch(args) -> int | None:
+    """`bench.py --gpus N` outside torchrun: re-run this script under
+    torch.distributed.run with N ranks (one per GPU, rendezvous on
+    127.0.0.1); rank 0 prints the JSON line.  Returns the exit code, or None
+    when no launch is needed (N = 1 or already inside a launched job)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    log("launching", " ".join(cmd[3:6]))
+    return subprocess.run(cmd).returncode
+
+
+def launch_check(args) -> int:
+    """--launch-check: the multi-rank plumbing without a workload (the CPU
+    test of `--gpus N`): every rank joins the process group (NCCL with GPUs,
+    gloo without), all ranks sum their rank ids, rank 0 prints one line."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    gpu = torch.cuda.is_available()
+    if world > 1:
+        if gpu:
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl" if gpu else "gloo")
+    t = torch.tensor([float(rank)], device="cuda" if gpu else "cpu")
+    if world > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "requested": args.gpus,
+                          "rank_sum": float(t.item()),
+                          "backend": dist.get_backend() if world > 1 else None}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def dist_setup(n_gpus: int):
     import torch
     import torch.distributed as dist
@@ -286,6 +360,7 @@ def run_reference_arm(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD_TEXT[args.workload], "grid": list(SHAPE)},
         "cpu_baseline": {"value": gps, "unit": "GPts/s", "cores": threads, "kind": "port",
+                         **host_cpu_info(),
                          "sample": f"{steps} time steps of {args.workload} on its first "
                                    f"{nx} of 592 x planes ({nx} x 592 x 592 points per "
                                    f"step) through the oracle port (NumPy, {threads} "
@@ -311,7 +386,14 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg4"],
                     help="cfg2: acoustic headline (default); cfg4: TTI")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="multi-rank plumbing only (no workload); see launch_check()")
     args = ap.parse_args()
+    rc = self_launch(args)
+    if rc is not None:
+        return rc
+    if args.launch_check:
+        return launch_check(args)
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
         args.warmup = 3
@@ -334,7 +416,6 @@ def main():
 
     # ------------------------------------------------------------ value
     runner = slabs.SlabRunner(cfg, rank=rank, world=world)
-    k_used = runner.time_height
     runner.run(0, args.warmup)
     torch.cuda.synchronize()
     if world > 1:
@@ -350,6 +431,9 @@ def main():
     if world > 1:
         dist.barrier()
     st = runner.stats()
+    # k is resolved by the library during the warm-up blocks (time_height=0
+    # measures K=1 vs K=2 in-run); read it after the runs
+    k_used = runner.time_height
     # single device: the library's own events on its launching stream bracket
     # the whole run; multi-rank: torch events around kernels + halo exchanges
     region_ms = st["run_ms"] if world == 1 else ev0.elapsed_time(ev1)
@@ -433,7 +517,8 @@ def main():
         gps, el, n = cpu_baseline(args.cpu_steps, threads, wl)
         cpu = {"value": gps, "unit": "GPts/s", "cores": threads, "kind": "port",
                "sample": f"{n} time steps of {wl} (592^3) through the oracle port "
-                         f"(NumPy, {threads} threads), stepping only ({el:.1f} s)"}
+                         f"(NumPy, {threads} threads), stepping only ({el:.1f} s)",
+               **host_cpu_info()}
 
     if rank == 0:
         line = {

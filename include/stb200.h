@@ -272,6 +272,11 @@ int stb_prop_stats(stb_prop_t p, int64_t* launches, double* kernel_ms,
                    int64_t* updates, int64_t* all_launches, double* run_ms);
 /* Kernel configuration chosen for time_height k (name, bytes per point). */
 int stb_prop_describe(stb_prop_t p, int32_t time_height, char* buf, int64_t buflen);
+/* Deepest time_height one fused pass of this handle computes (acoustic fp32
+ * 3-D: 2 at so 2/4/8, 1 otherwise).  Longer wavefront heights
+ * (schedule.py:171-207) run as consecutive blocks of this depth; run()
+ * reports the depth used in RunReport.schedule["time_height"]. */
+int stb_prop_max_time_height(stb_prop_t p, int32_t* k);
 int stb_prop_destroy(stb_prop_t p);
 
 #ifdef __cplusplus

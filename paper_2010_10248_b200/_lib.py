@@ -34,6 +34,7 @@ EXPORTS = (
     "stb_prop_set_damping",
     "stb_prop_step_async", "stb_prop_gather_async", "stb_prop_async_finish", "stb_prop_reset", "stb_prop_stats",
     "stb_prop_describe",
+    "stb_prop_max_time_height",
     "stb_prop_destroy",
 )
 
@@ -116,6 +117,7 @@ def _declare(lib):
         "stb_prop_reset": ([P], C.c_int),
         "stb_prop_stats": ([P, pi64, pdbl, pi64, pi64, pdbl], C.c_int),
         "stb_prop_describe": ([P, i32, C.c_char_p, i64], C.c_int),
+        "stb_prop_max_time_height": ([P, C.POINTER(i32)], C.c_int),
         "stb_prop_destroy": ([P], C.c_int),
     }
     for name, (args, res) in sig.items():

@@ -362,6 +362,13 @@ STB_API int stb_prop_describe(stb_prop_t p, int32_t time_height, char* buf, int6
   })
 }
 
+STB_API int stb_prop_max_time_height(stb_prop_t p, int32_t* k) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr && k != nullptr, STB_ERR_ARG, "NULL argument");
+    *k = p->max_time_height();
+  })
+}
+
 STB_API int stb_prop_destroy(stb_prop_t p) {
   STB_GUARD({ delete p; })
 }

@@ -13,10 +13,8 @@
 //              into the sweep, receivers gathered on a second stream.
 //              K = 1: acoustic_fused<R,1> (the default; ~91 % of HBM at so=8).
 //              K = 2: acoustic_wtb<R,2> (acoustic_wtb.cuh), the two-level
-//              wavefront kernel with warp-specialised levels; the older
-//              acoustic_fused<R,2> stays behind STB_WTB=0.  time_height = 0
+//              wavefront kernel with warp-specialised levels.  time_height = 0
 //              measures K on the run's first blocks.
-//   tiled      acoustic_tiled_step: one step per launch (kept for A/B).
 //   reference  thread-per-point kernel for fp64 and degenerate grids.
 // Time level t lives in buffer t mod NB (NB = 6: distinct inputs/outputs
 // for every K <= 4).
@@ -30,7 +28,6 @@
 
 #include "acoustic_fused.cuh"
 #include "acoustic_kernels.cuh"
-#include "acoustic_tiled.cuh"
 #include "acoustic_wtb.cuh"
 #include "sparse_ops.cuh"
 
@@ -376,7 +373,7 @@ class AcousticProp final : public stb_prop_s {
     const int hy = (max_k_ - 1) * R_;
     int hz = 0;
     for (int j = 1; j < max_k_; ++j) hz = (hz + R_ + 3) / 4 * 4;
-    src_n_ = tile_lists(fused_ty(R_, 1), kTZ, hy, hz, src_list_, src_tile_ptr_);
+    src_n_ = tile_lists(fused_ty(R_), kTZ, hy, hz, src_list_, src_tile_ptr_);
     thr_.clear();
     wtb_thr_[0].reset();
     wtb_thr_[1].reset();
@@ -432,20 +429,13 @@ class AcousticProp final : public stb_prop_s {
     if (!K_ || src_n_ == 0) return nullptr;
     auto it = thr_.find(K);
     if (it != thr_.end()) return it->second.get();
-    using C = FusedCfg<R, K, fused_ty(R, K), kTZ, pf_for(R, K)>;
+    using C = FusedCfg<R, K, fused_ty(R), kTZ, pf_for(R)>;
     const int nty = (int)((d_.ny + C::TY_ - 1) / C::TY_), ntz = (int)((d_.nz + kTZ - 1) / kTZ);
     const int ntiles = nty * ntz;
-    // the legacy K = 2 kernel tiles differently from the global lists
-    DevBuf<int4> own_list;
-    DevBuf<int> own_ptr;
+    static_assert(K == 1, "acoustic_fused runs one step per pass; K = 2 is acoustic_wtb");
     const int4* tl = src_list_.p;
     const int* tp = src_tile_ptr_.p;
     int64_t n = src_n_;
-    if (C::TY_ != fused_ty(R, 1)) {
-      n = tile_lists(C::TY_, kTZ, C::hy(1), C::hz(1), own_list, own_ptr);
-      tl = own_list.p;
-      tp = own_ptr.p;
-    }
     auto L = std::make_unique<ThrLists>();
     if (n == 0) {
       L->ptr.alloc(ntiles * C::NWORK + 1);
@@ -488,7 +478,7 @@ class AcousticProp final : public stb_prop_s {
     const int4* tl = src_list_.p;
     const int* tp = src_tile_ptr_.p;
     int64_t ne = src_n_;
-    if (C::TY != fused_ty(R, 1) || C::H1 != (max_k_ - 1) * R || C::HZ1 != (max_k_ > 1 ? (R + 3) / 4 * 4 : 0)) {
+    if (C::TY != fused_ty(R) || C::H1 != (max_k_ - 1) * R || C::HZ1 != (max_k_ > 1 ? (R + 3) / 4 * 4 : 0)) {
       ne = tile_lists(C::TY, kTZ, C::H1, C::HZ1, own_list, own_ptr);
       tl = own_list.p;
       tp = own_ptr.p;
@@ -596,25 +586,8 @@ class AcousticProp final : public stb_prop_s {
       if (nrec_)
         for (int j = 0; j < kb; ++j) STB_CUDA(cudaStreamWaitEvent(st_, gev_[slot(t + j)], 0));
       STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
-      if (path_ == Path::Fused && kb == 2 && diag_cx_ > 0 && R_ == 4) {
-        // L2-streaming temporal blocking: step t on x-chunk c, then step t+1
-        // on chunk c-1 (its x-halo of step t was just written), so step t+1
-        // reads step t and the shared inputs while they are L2-resident.
-        const int cx = diag_cx_;
-        const int nc = (int)((d_.nx + cx - 1) / cx);
-        const int g0 = (gmask & 1) ? 1 : 0, g1 = (gmask & 2) ? 2 : 0;
-        for (int c = 0; c <= nc; ++c) {
-          if (c < nc)
-            launch_fused_rk<4, 1>(t, g0 ? gflag : nullptr, g0, c * cx,
-                                  (int)std::min<int64_t>((int64_t)(c + 1) * cx, d_.nx), cx);
-          if (c >= 1)
-            launch_fused_rk<4, 1>(t + 1, g1 ? gflag : nullptr, g1 ? 1 : 0, (c - 1) * cx,
-                                  (int)std::min<int64_t>((int64_t)c * cx, d_.nx), cx);
-        }
-      } else if (path_ == Path::Fused) {
-        launch_fused(t, kb, gflag, gmask);
-      } else if (path_ == Path::Tiled) {
-        launch_tiled(slot(t - 1), slot(t - 2), lvl_[slot(t)].p, gflag);
+      if (path_ == Path::Fused) {
+        launch_fused_range(t, kb, gflag, gmask, 0, (int)d_.nx);
       } else {
         launch_reference_step<T>(R_, st_, lvl_[slot(t - 1)].p, lvl_[slot(t - 2)].p,
                                  lvl_[slot(t)].p, inv_.p, inv_scalar_, fac_[0].p, fac_[1].p,
@@ -834,41 +807,35 @@ class AcousticProp final : public stb_prop_s {
   std::string describe(int k) override {
     std::ostringstream os;
     const int kk = resolve_k(k);
-    if (path_ == Path::Fused && kk == 1 && (wtb1_mask_ & (1 << R_))) {
-      os << "acoustic_wtb<f32,R=" << R_ << ",LV=1,TY=" << wtb_ty(R_, 1) << ",TZ=" << kTZ
-         << ",RY=" << wtb_ry(R_) << ",PF=" << kWtbPF << "," << (fast_ ? "fma" : "exact")
-         << "> k=1 bytes_per_point=16";
-    } else if (path_ == Path::Fused && kk == 2 && wtb_) {
+    const int L = (int)d_.nx;
+    if (path_ == Path::Fused && kk == 2) {
       os << "acoustic_wtb<f32,R=" << R_ << ",LV=2,TY=" << wtb_ty(R_) << ",TZ=" << kTZ
          << ",RY=" << wtb_ry(R_)
-         << ",PF=" << kWtbPF << "," << (fast_ ? "fma" : "exact") << "> k=2 bytes_per_point=20";
-      if (k == 0 && tuned_k_ && tune_ms_[0] > 0.f)
-        os << " autotuned(ms/step k1=" << tune_ms_[0] << " k2=" << tune_ms_[1] << ")";
+         << ",PF=" << kWtbPF << "," << (fast_ ? "fma" : "exact") << "> k=2 cx=" << wtb_cx(L)
+         << " bytes_per_point=20";
     } else if (path_ == Path::Fused) {
-      os << "acoustic_fused<f32,R=" << R_ << ",TY=" << fused_ty(R_, kk) << ",TZ=" << kTZ << ",PF=" << pf_for(R_, resolve_k(k))
-         << "," << (fast_ ? "fma" : "exact") << "> k=" << kk << " cx=" << cx_len_
-         << " bytes_per_point=" << (kk == 1 ? 16 : 20);
-      if (k == 0 && tuned_k_ && tune_ms_[0] > 0.f)
-        os << " autotuned(ms/step k1=" << tune_ms_[0] << " k2=" << tune_ms_[1] << ")";
-    } else if (path_ == Path::Tiled)
-      os << "acoustic_tiled_step<f32,R=" << R_ << ",TY=16,TZ=64,PF=2> k=1 cx=" << cx_len_
-         << " bytes_per_point=16";
-    else
+      os << "acoustic_fused<f32,R=" << R_ << ",TY=" << fused_ty(R_) << ",TZ=" << kTZ
+         << ",PF=" << pf_for(R_) << "," << (fast_ ? "fma" : "exact") << "> k=" << kk
+         << " cx=" << fused_cx(L) << " bytes_per_point=16";
+    } else {
       os << "acoustic_reference_step<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
          << "> k=1 bytes_per_point=" << 4 * sizeof(T);
+    }
+    if (path_ == Path::Fused && k == 0 && tuned_k_ && tune_ms_[0] > 0.f)
+      os << " autotuned(ms/step k1=" << tune_ms_[0] << " k2=" << tune_ms_[1] << ")";
     return os.str();
   }
 
+  int max_time_height() const override { return path_ == Path::Fused ? max_k_ : 1; }
+
  private:
-  enum class Path { Reference, Tiled, Fused };
+  enum class Path { Reference, Fused };
   static constexpr int kTY = 16, kTZ = 64;
   // fused-kernel tile height.  K = 1: 32 rows in one CTA of 16 consumer
   // warps -- less y halo per staged plane and room for a deeper prefetch
   // (measured +1 % at so=4/8 and +10 % at so=12 over two 16-row CTAs per
-  // SM); the legacy K = 2 kernel (STB_WTB=0) keeps 16-row tiles.
-  static constexpr int fused_ty(int, int K = 1) {
-    return K == 1 ? (kFusedTY1 > 0 ? kFusedTY1 : kTY) : kTY;
-  }
+  // SM).
+  static constexpr int fused_ty(int) { return kFusedTY1 > 0 ? kFusedTY1 : kTY; }
   static constexpr int kWtbPF = 3;                // two-level kernel: TMA prefetch depth
   // rows per thread: 2 (measured at R = 2: RY = 1 gives 21 warps instead of
   // 11 but doubles the per-plane bookkeeping per point, 274 vs 328 GPts/s)
@@ -879,12 +846,12 @@ class AcousticProp final : public stb_prop_s {
   static constexpr int wtb_ty(int R, int LV = 2) {
     return LV == 1 ? (R == 6 ? 28 : 32) : kWtbTYOverride ? kWtbTYOverride : (R <= 2 ? 24 : 16);
   }
-  // TMA prefetch depth.  One-CTA 32-row K = 1 tiles: 4 (R <= 4), 3 (R = 6,
-  // whose planes are 40 % larger; measured 4 > 3, 5 at so=8).  Two-CTA
-  // 16-row tiles: 3, and 2 at R = 6 or for the legacy K = 2 at R <= 2.
-  static constexpr int pf_for(int R, int K = 1) {
-    if (K == 1 && fused_ty(R, 1) != kTY) return R >= 6 ? 3 : 4;
-    return (R >= 6 || (R <= 2 && K > 1)) ? 2 : 3;
+  // TMA prefetch depth.  One-CTA 32-row tiles: 4 (R <= 4), 3 (R = 6, whose
+  // planes are 40 % larger; measured 4 > 3, 5 at so=8).  Two-CTA 16-row
+  // tiles: 3, and 2 at R = 6.
+  static constexpr int pf_for(int R) {
+    if (fused_ty(R) != kTY) return R >= 6 ? 3 : 4;
+    return R >= 6 ? 2 : 3;
   }
 
   int slot(int64_t t) const { return (int)(((t % NB) + NB) % NB); }
@@ -943,6 +910,37 @@ class AcousticProp final : public stb_prop_s {
     return (L + best_c - 1) / best_c;
   }
 
+  // x-chunk lengths the launches use (describe() reports the same)
+  template <int R>
+  int fused_cx_r(int L) {
+    using C = FusedCfg<R, 1, fused_ty(R), kTZ, pf_for(R)>;
+    return chunk_len(L, 1, C::MINB, fused_ty(R));
+  }
+  template <int R>
+  int wtb_cx_r(int L) {
+    using C = WtbCfg<R, 2, wtb_ry(R), kWtbPF, wtb_ty(R, 2)>;
+    int cx = chunk_len(L, 2, 1, C::TY);
+    if (cx + 4 * R > C::MAXN) cx = C::MAXN - 4 * R;   // per-CTA damping table
+    return cx;
+  }
+  int fused_cx(int L) {
+    switch (R_) {
+      case 1: return fused_cx_r<1>(L);
+      case 2: return fused_cx_r<2>(L);
+      case 4: return fused_cx_r<4>(L);
+      case 6: return fused_cx_r<6>(L);
+      default: return L;
+    }
+  }
+  int wtb_cx(int L) {
+    switch (R_) {
+      case 1: return wtb_cx_r<1>(L);
+      case 2: return wtb_cx_r<2>(L);
+      case 4: return wtb_cx_r<4>(L);
+      default: return L;
+    }
+  }
+
   int resolve_k(int k) const {
     if (path_ != Path::Fused) return 1;
     int kk = k < 1 ? (tuned_k_ ? tuned_k_ : default_k_) : k;
@@ -970,101 +968,62 @@ class AcousticProp final : public stb_prop_s {
       if (const char* c = std::getenv("STB_NCHUNK")) nch = std::atoi(c);
       if (nch < 1) nch = 1;
       cx_len_ = (int)((d_.nx + nch - 1) / nch);
-      nchunks_ = (int)((d_.nx + cx_len_ - 1) / cx_len_);
       fast_ = arithmetic_ == 1;
-      if (const char* f = std::getenv("STB_FMA")) fast_ = f[0] == '1';
-      if (e && std::strcmp(e, "tiled") == 0) {
-        const int hz = (R_ + 3) / 4 * 4;
-        for (int l = 0; l < NB; ++l) {
-          map_ext_[l] = make_map3d_f32(lvl_[l].p, d_, 64 + 2 * hz, 16 + 2 * R_, 1);
-          map_tile_[l] = make_map3d_f32(lvl_[l].p, d_, 64, 16, 1);
-        }
-        if (inv_.p) map_inv_ = make_map3d_f32(inv_.p, d_, 64, 16, 1);
-        path_ = Path::Tiled;
-        return;
-      }
       max_k_ = (R_ == 4 || R_ == 2 || R_ == 1) ? 2 : 1;
       default_k_ = 1;
       if (const char* kd = std::getenv("STB_DEFAULT_K")) default_k_ = std::atoi(kd);
-      if (const char* dc = std::getenv("STB_DIAG_CX")) diag_cx_ = std::atoi(dc);
-      if (const char* w = std::getenv("STB_WTB")) wtb_ = w[0] != '0';
-      if (const char* w = std::getenv("STB_WTB1")) wtb1_mask_ = std::atoi(w);
       if (default_k_ < 1) default_k_ = 1;
       if (default_k_ > max_k_) default_k_ = max_k_;
       path_ = Path::Fused;
     }
   }
 
-  template <int R, int K>
+  template <int R>
   void fused_maps(FusedMaps& m, int s_l0, int s_lm1) {
-    using Cf = FusedCfg<R, K, fused_ty(R, K), kTZ, pf_for(R, K)>;
+    using Cf = FusedCfg<R, 1, fused_ty(R), kTZ, pf_for(R)>;
     m.l0 = make_map3d_f32(reinterpret_cast<const float*>(lvl_[s_l0].p), d_, Cf::WZ0, Cf::HY0, 1);
     m.lm1 = make_map3d_f32(reinterpret_cast<const float*>(lvl_[s_lm1].p), d_, Cf::WZ1, Cf::HY1, 1);
-    if (inv_.p) {
-      for (int j = 1; j <= K; ++j)
-        m.inv[j - 1] = make_map3d_f32(reinterpret_cast<const float*>(inv_.p), d_,
-                                      kTZ + 2 * Cf::hz(j), Cf::TY_ + 2 * Cf::hy(j), 1);
-    }
+    if (inv_.p)
+      m.inv[0] = make_map3d_f32(reinterpret_cast<const float*>(inv_.p), d_, kTZ + 2 * Cf::hz(1),
+                                Cf::TY_ + 2 * Cf::hy(1), 1);
   }
 
-  template <int R, int K>
-  void launch_fused_rk(int64_t t, int* gflag, int gmask, int x_lo = 0, int x_hi = -1,
-                       int cx = 0) {
-    if (x_hi < 0) x_hi = (int)d_.nx;
-    if (cx <= 0)
-      cx = chunk_len(x_hi - x_lo, K, FusedCfg<R, K, fused_ty(R, K), kTZ, pf_for(R, K)>::MINB,
-                     fused_ty(R, K));
-    // tensor maps are cached per (K, input slots)
+  // One step per pass: acoustic_fused<R, 1> (acoustic_fused.cuh).
+  template <int R>
+  void launch_fused_rk(int64_t t, int* gflag, int gmask, int x_lo, int x_hi) {
+    constexpr int TY = fused_ty(R), PF = pf_for(R);
+    const int cx = fused_cx_r<R>(x_hi - x_lo);
+    // tensor maps are cached per input slots
     const int s_l0 = slot(t - 1), s_lm1 = slot(t - 2);
-    const int key = (K * NB + s_l0) * NB + s_lm1;
+    const int key = (NB + s_l0) * NB + s_lm1;
     auto it = fmaps_.find(key);
     if (it == fmaps_.end()) {
       FusedMaps m{};
-      fused_maps<R, K>(m, s_l0, s_lm1);
+      fused_maps<R>(m, s_l0, s_lm1);
       it = fmaps_.emplace(key, m).first;
     }
-    FusedArgs a{};
-    a.out_km1 = K >= 2 ? reinterpret_cast<float*>(lvl_[slot(t + K - 2)].p) : nullptr;
-    a.out_k = reinterpret_cast<float*>(lvl_[slot(t + K - 1)].p);
-    a.fx = reinterpret_cast<const float*>(fac_[0].p);
-    a.fy = reinterpret_cast<const float*>(fac_[1].p);
-    a.fz = reinterpret_cast<const float*>(fac_[2].p);
-    a.inv_scalar = (float)inv_scalar_;
-    a.use_inv = inv_.p ? 1 : 0;
-    a.cf = tcf_;
-    a.d = d_;
-    a.cx_len = cx;
-    a.x_lo = x_lo;
-    a.x_hi = x_hi;
-    a.ntz = (int)((d_.nz + kTZ - 1) / kTZ);
-    a.zero_lo = zero_lo_ ? 1 : 0;
-    a.zero_hi = zero_hi_ ? 1 : 0;
-    a.t0 = (int)t;
+    FusedArgs a = common_args(t, x_lo, x_hi, cx, gflag, gmask);
+    a.out_km1 = nullptr;
+    a.out_k = reinterpret_cast<float*>(lvl_[slot(t)].p);
     if (K_) {
-      const ThrLists* tl = thr_lists<R, K>();
+      const ThrLists* tl = thr_lists<R, 1>();
       a.thr_ptr = tl ? tl->ptr.p : nullptr;
       a.thr_list = tl ? tl->list.p : nullptr;
-      a.series = reinterpret_cast<const float*>(series_.p);
-      a.n_src = (int)K_;
     }
-    a.nonfinite = gflag;
-    a.guard_mask = gmask;
     const int nch = (x_hi - x_lo + cx - 1) / cx;
     if (fast_)
-      FusedLauncher<R, K, fused_ty(R, K), kTZ, pf_for(R, K), true>::launch(st_, it->second, a, nch);
+      FusedLauncher<R, 1, TY, kTZ, PF, true>::launch(st_, it->second, a, nch);
     else
-      FusedLauncher<R, K, fused_ty(R, K), kTZ, pf_for(R, K), false>::launch(st_, it->second, a, nch);
+      FusedLauncher<R, 1, TY, kTZ, PF, false>::launch(st_, it->second, a, nch);
   }
 
-  // Wavefront kernel (acoustic_wtb.cuh): LV = 1 or 2 steps per pass.
-  template <int R, int LV>
-  void launch_wtb_rk(int64_t t, int* gflag, int gmask, int x_lo = 0, int x_hi = -1) {
-    using C = WtbCfg<R, LV, wtb_ry(R), kWtbPF, wtb_ty(R, LV)>;
-    if (x_hi < 0) x_hi = (int)d_.nx;
-    int cx = chunk_len(x_hi - x_lo, LV, 1, C::TY);
-    if (cx + 2 * LV * R > C::MAXN) cx = C::MAXN - 2 * LV * R;   // per-CTA damping table
+  // Two steps per pass: the two-level wavefront kernel (acoustic_wtb.cuh).
+  template <int R>
+  void launch_wtb_rk(int64_t t, int* gflag, int gmask, int x_lo, int x_hi) {
+    using C = WtbCfg<R, 2, wtb_ry(R), kWtbPF, wtb_ty(R, 2)>;
+    const int cx = wtb_cx_r<R>(x_hi - x_lo);
     const int s_l0 = slot(t - 1), s_lm1 = slot(t - 2);
-    const int key = (LV * NB + s_l0) * NB + s_lm1;
+    const int key = (2 * NB + s_l0) * NB + s_lm1;
     auto it = wmaps_.find(key);
     if (it == wmaps_.end()) {
       WtbMaps m{};
@@ -1072,17 +1031,31 @@ class AcousticProp final : public stb_prop_s {
       m.l0 = make_map3d_f32(l0, d_, C::WZ0, C::HY0, 1);
       m.lm1 = make_map3d_f32(reinterpret_cast<const float*>(lvl_[s_lm1].p), d_, C::WZ1, C::HY1,
                              1);
-      if (LV == 2) m.c1 = make_map3d_f32(l0, d_, C::WZ1, C::TY, 1);
+      m.c1 = make_map3d_f32(l0, d_, C::WZ1, C::TY, 1);
       if (inv_.p) {
         const float* iv = reinterpret_cast<const float*>(inv_.p);
         m.inv1 = make_map3d_f32(iv, d_, C::WZ1, C::HY1, 1);
-        if (LV == 2) m.inv2 = make_map3d_f32(iv, d_, C::WZ1, C::TY, 1);
+        m.inv2 = make_map3d_f32(iv, d_, C::WZ1, C::TY, 1);
       }
       it = wmaps_.emplace(key, m).first;
     }
-    FusedArgs a{};
+    FusedArgs a = common_args(t, x_lo, x_hi, cx, gflag, gmask);
     a.out_km1 = reinterpret_cast<float*>(lvl_[slot(t)].p);
-    a.out_k = reinterpret_cast<float*>(lvl_[slot(t + LV - 1)].p);
+    a.out_k = reinterpret_cast<float*>(lvl_[slot(t + 1)].p);
+    if (K_) {
+      const ThrLists* tl = wtb_thr_lists<R, 2>();
+      a.thr_ptr = tl ? tl->ptr.p : nullptr;
+      a.thr_list = tl ? tl->list.p : nullptr;
+    }
+    const int nch = (x_hi - x_lo + cx - 1) / cx;
+    if (fast_)
+      WtbLauncher<R, 2, wtb_ry(R), kWtbPF, wtb_ty(R, 2), true>::launch(st_, it->second, a, nch);
+    else
+      WtbLauncher<R, 2, wtb_ry(R), kWtbPF, wtb_ty(R, 2), false>::launch(st_, it->second, a, nch);
+  }
+
+  FusedArgs common_args(int64_t t, int x_lo, int x_hi, int cx, int* gflag, int gmask) {
+    FusedArgs a{};
     a.fx = reinterpret_cast<const float*>(fac_[0].p);
     a.fy = reinterpret_cast<const float*>(fac_[1].p);
     a.fz = reinterpret_cast<const float*>(fac_[2].p);
@@ -1098,84 +1071,34 @@ class AcousticProp final : public stb_prop_s {
     a.zero_hi = zero_hi_ ? 1 : 0;
     a.t0 = (int)t;
     if (K_) {
-      const ThrLists* tl = wtb_thr_lists<R, LV>();
-      a.thr_ptr = tl ? tl->ptr.p : nullptr;
-      a.thr_list = tl ? tl->list.p : nullptr;
       a.series = reinterpret_cast<const float*>(series_.p);
       a.n_src = (int)K_;
     }
     a.nonfinite = gflag;
     a.guard_mask = gmask;
-    const int nch = (x_hi - x_lo + cx - 1) / cx;
-    if (fast_)
-      WtbLauncher<R, LV, wtb_ry(R), kWtbPF, wtb_ty(R, LV), true>::launch(st_, it->second, a, nch);
-    else
-      WtbLauncher<R, LV, wtb_ry(R), kWtbPF, wtb_ty(R, LV), false>::launch(st_, it->second, a,
-                                                                          nch);
+    return a;
   }
 
-  // K = 1 launches: the one-level wavefront kernel where it was measured
-  // faster (bit k of wtb1_mask_ set for R = k), else acoustic_fused<R, 1>
-  template <int R>
-  void launch_k1(int64_t t, int* gflag, int gmask, int x_lo = 0, int x_hi = -1) {
-    if (wtb1_mask_ & (1 << R)) return launch_wtb_rk<R, 1>(t, gflag, gmask, x_lo, x_hi);
-    launch_fused_rk<R, 1>(t, gflag, gmask, x_lo, x_hi);
-  }
-
+  // kb (1 or 2) fused steps from t over local planes [x_lo, x_hi)
   void launch_fused_range(int64_t t, int kb, int* gflag, int gmask, int x_lo, int x_hi) {
     if constexpr (sizeof(T) == 4) {
-      if (R_ == 4 && kb == 2)
-        return wtb_ ? launch_wtb_rk<4, 2>(t, gflag, gmask, x_lo, x_hi)
-                    : launch_fused_rk<4, 2>(t, gflag, gmask, x_lo, x_hi);
-      if (R_ == 4) return launch_k1<4>(t, gflag, gmask, x_lo, x_hi);
-      if (R_ == 2 && kb == 2)
-        return wtb_ ? launch_wtb_rk<2, 2>(t, gflag, gmask, x_lo, x_hi)
-                    : launch_fused_rk<2, 2>(t, gflag, gmask, x_lo, x_hi);
-      if (R_ == 2) return launch_k1<2>(t, gflag, gmask, x_lo, x_hi);
-      if (R_ == 1 && kb == 2)
-        return wtb_ ? launch_wtb_rk<1, 2>(t, gflag, gmask, x_lo, x_hi)
-                    : launch_fused_rk<1, 2>(t, gflag, gmask, x_lo, x_hi);
-      if (R_ == 1) return launch_fused_rk<1, 1>(t, gflag, gmask, x_lo, x_hi);
-      if (R_ == 6) return launch_k1<6>(t, gflag, gmask, x_lo, x_hi);
-      throw Error(STB_ERR_ARG, "no fused kernel for this space order");
+      STB_REQUIRE(kb >= 1 && kb <= max_k_, STB_ERR_PLAN,
+                  "time_height exceeds the fused kernel's depth");
+      switch (R_) {
+        case 1: return kb == 2 ? launch_wtb_rk<1>(t, gflag, gmask, x_lo, x_hi)
+                               : launch_fused_rk<1>(t, gflag, gmask, x_lo, x_hi);
+        case 2: return kb == 2 ? launch_wtb_rk<2>(t, gflag, gmask, x_lo, x_hi)
+                               : launch_fused_rk<2>(t, gflag, gmask, x_lo, x_hi);
+        case 4: return kb == 2 ? launch_wtb_rk<4>(t, gflag, gmask, x_lo, x_hi)
+                               : launch_fused_rk<4>(t, gflag, gmask, x_lo, x_hi);
+        case 6: return launch_fused_rk<6>(t, gflag, gmask, x_lo, x_hi);
+        default: throw Error(STB_ERR_ARG, "no fused kernel for this space order");
+      }
     }
   }
 
   void launch_fused(int64_t t, int kb, int* gflag, int gmask) {
-    if constexpr (sizeof(T) == 4) {
-      if (R_ == 4 && kb == 2)
-        return wtb_ ? launch_wtb_rk<4, 2>(t, gflag, gmask) : launch_fused_rk<4, 2>(t, gflag, gmask);
-      if (R_ == 4) return launch_k1<4>(t, gflag, gmask);
-      if (R_ == 2 && kb == 2)
-        return wtb_ ? launch_wtb_rk<2, 2>(t, gflag, gmask) : launch_fused_rk<2, 2>(t, gflag, gmask);
-      if (R_ == 2) return launch_k1<2>(t, gflag, gmask);
-      if (R_ == 1 && kb == 2)
-        return wtb_ ? launch_wtb_rk<1, 2>(t, gflag, gmask) : launch_fused_rk<1, 2>(t, gflag, gmask);
-      if (R_ == 1) return launch_fused_rk<1, 1>(t, gflag, gmask);
-      if (R_ == 6) return launch_k1<6>(t, gflag, gmask);
-      throw Error(STB_ERR_ARG, "no fused kernel for this space order");
-    }
-  }
-
-  void launch_tiled(int s1, int s0, T* dst, int* nonfinite) {
-    if constexpr (sizeof(T) == 4) {
-      const CUtensorMap& mi = inv_.p ? map_inv_ : map_tile_[s0];
-#define STB_TILED_CASE(RR)                                                                   \
-  case RR:                                                                                   \
-    TiledAcousticLauncher<RR, 16, 64, 2>::launch(st_, map_ext_[s1], map_tile_[s0], mi, dst,  \
-                                                 fac_[0].p, fac_[1].p, fac_[2].p, has_fac_,  \
-                                                 inv_.p != nullptr, inv_scalar_, tcf_, d_,   \
-                                                 cx_len_, nonfinite);                        \
-    break;
-      switch (R_) {
-        STB_TILED_CASE(2)
-        STB_TILED_CASE(4)
-        STB_TILED_CASE(6)
-        default:
-          throw Error(STB_ERR_ARG, "no tiled kernel for this space order");
-      }
-#undef STB_TILED_CASE
-    }
+    launch_fused_range(t, kb, gflag, gmask, 0, (int)d_.nx);
   }
 
   void check_same_geometry(const Support& s) {
@@ -1224,15 +1147,11 @@ class AcousticProp final : public stb_prop_s {
   cudaStream_t cst_ = nullptr;                   // trace copies
   std::vector<cudaEvent_t> cev_;
   float tune_ms_[2] = {0.f, 0.f};   // measured ms per step at K = 1, 2
-  int cx_len_ = 0, nchunks_ = 1;
+  int cx_len_ = 0;                  // STB_NCHUNK override of the x-chunk length
   int sm_count_ = 0;
-  int diag_cx_ = 0;                 // >0: K=2 blocks run as diagonal K=1 sweeps
   TiledCoefs tcf_{};
-  CUtensorMap map_ext_[NB]{}, map_tile_[NB]{}, map_inv_{};
   std::unordered_map<int, FusedMaps> fmaps_;
   std::unordered_map<int, WtbMaps> wmaps_;
-  bool wtb_ = true;                 // K = 2 runs the two-level wavefront kernel
-  int wtb1_mask_ = 0;               // bit R: K = 1 runs the one-level wavefront kernel
   // sources
   int64_t K_ = 0, src_nt_ = 0;
   DevBuf<T> series_;

@@ -32,7 +32,7 @@
 // rounding per term instead of two); tests bound it at 1e-5 relative L2.
 #pragma once
 
-#include "acoustic_tiled.cuh"
+#include "acoustic_kernels.cuh"
 #include "f32x2.cuh"
 #include "fp_exact.cuh"
 #include "tma.cuh"
@@ -40,6 +40,14 @@
 namespace stb {
 
 constexpr int kRoundUp4(int v) { return (v + 3) / 4 * 4; }
+
+// Stencil coefficients of the fp32 sweep kernels, rounded once to fp32 as
+// NumPy's weak-scalar rule rounds the Python floats (physics.py:158-164).
+struct TiledCoefs {
+  float c0;
+  float cx[8], cy[8], cz[8];
+  float nz;     // -0.0f, a runtime value on purpose (see xmul2 in f32x2.cuh)
+};
 
 template <int R, int K, int TY, int TZ, int PF>
 struct FusedCfg {

@@ -206,6 +206,9 @@ struct stb_prop_s {
   virtual void stats(int64_t* launches, double* ms, int64_t* updates, int64_t* all_launches,
                      double* run_ms) = 0;
   virtual std::string describe(int k) = 0;
+  // deepest time_height one fused pass supports (requests above it are
+  // split into blocks of this depth; schedule.py:171-207 accepts any T)
+  virtual int max_time_height() const { return 1; }
   // local field shape (x slab) and element size, for host-side copies
   virtual void field_info(int64_t shape[3], int* elem_bytes) = 0;
   // asynchronous stepping (multi-GPU x slabs): enqueue on stream() without

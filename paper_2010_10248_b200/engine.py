@@ -18,6 +18,7 @@ import ctypes as C
 import hashlib
 import math
 import os
+import re
 import platform
 import struct
 import time
@@ -276,6 +277,17 @@ def arithmetic_intensity(physics: str, space_order: int, precision: int) -> floa
     return (18 * (3 * r - 1) + 45) / (22 * item)
 
 
+def device_max_time_height(config: RunConfig) -> int:
+    """Deepest time_height one device pass fuses for this configuration
+    (the library's rule, checked against stb_prop_max_time_height by the
+    x-slab runner): fp32 acoustic on a 3-D grid at so 2, 4, 8 -> 2; else 1."""
+    active = all(n > 1 for n in config.grid.shape)
+    if (config.physics == "acoustic" and config.precision == 32 and active
+            and config.space_order in (2, 4, 8)):
+        return 2
+    return 1
+
+
 def _gpu_time_height(config: RunConfig) -> int:
     """Map the reference schedule onto the device plan; mirror its legality
     errors (engine.py:293-305, schedule.py:181-199)."""
@@ -387,6 +399,11 @@ class _Prop:
                                              C.byref(al), C.byref(rm)))
         return {"stencil_launches": n.value, "stencil_ms": ms.value, "updates": up.value,
                 "launches": al.value, "run_ms": rm.value}
+
+    def max_time_height(self) -> int:
+        k = C.c_int32(1)
+        _lib.check(_lib.lib().stb_prop_max_time_height(self.raw, C.byref(k)))
+        return int(k.value)
 
     def describe(self, k):
         buf = C.create_string_buffer(512)
@@ -699,8 +716,13 @@ def run(config: RunConfig) -> RunResult:
         rec = np.zeros((nt, nrec), dtype=np.float64)
     precompute_s = time.perf_counter() - t_pre0
 
+    # the device fuses at most max_time_height() steps per pass; deeper
+    # wavefront heights run as consecutive blocks of that depth (reported)
+    k_max = prop.max_time_height()
     if config.validate and nt > 0:
-        _validate_device_plan(config, prop, k, nt, handle if nsrc else None)
+        # every depth the run may use (time_height = 0 measures k in-run)
+        for kk in ([min(k, k_max)] if k > 0 else range(1, k_max + 1)):
+            _validate_device_plan(config, prop, kk, nt, handle if nsrc else None)
 
     t0 = time.perf_counter()
     if nt > 0:
@@ -716,12 +738,17 @@ def run(config: RunConfig) -> RunResult:
     nf = len(names)
     gpoints = grid.npoints * nt * nf / elapsed / 1e9 if nt > 0 and elapsed > 0 else 0.0
     s = config.schedule
+    plan_text = prop.describe(k)
+    m = re.search(r"\bk=(\d+)", plan_text)
+    k_used = int(m.group(1)) if m else 1
     report = RunReport(
         physics=config.physics, grid_shape=grid.shape, space_order=config.space_order,
         precision=config.precision, threads=config.threads,
         schedule={"kind": s.kind, "block_shape": s.block_shape, "tile_shape": s.tile_shape,
-                  "time_height": s.time_height, "arithmetic": getattr(s, "arithmetic", "exact"),
-                  "device_plan": prop.describe(k)},
+                  "time_height": k_used, "time_height_requested": s.time_height,
+                  "max_time_height": k_max,
+                  "arithmetic": getattr(s, "arithmetic", "exact"),
+                  "device_plan": plan_text},
         nt=nt, dt=dt, elapsed_s=elapsed, precompute_s=precompute_s, gpoints_per_s=gpoints,
         arithmetic_intensity=arithmetic_intensity(config.physics, config.space_order,
                                                   config.precision),

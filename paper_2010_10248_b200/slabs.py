@@ -35,7 +35,7 @@ import numpy as np
 
 from . import _lib
 from .engine import (FIELDS, _gpu_time_height, _Handle, _Prop, _wavelets, build_propagator,
-                     medium_velocity_bounds, resolve_steps)
+                     device_max_time_height, medium_velocity_bounds, resolve_steps)
 from .sparse import nearest_scales_from_velocity, stencils, validate_coords_in_extent
 
 DEFAULT_TIME_HEIGHT = 1
@@ -96,6 +96,9 @@ class DeviceSlab:
 
     def run(self, t0, n, k, rec_out=None):
         self.prop.run(t0, n, k, rec_out)
+
+    def max_time_height(self) -> int:
+        return self.prop.max_time_height()
 
     # asynchronous stepping (fused acoustic path): see SlabRunner._run_async
     def supports_async(self) -> bool:
@@ -162,6 +165,10 @@ class SlabRunner:
         self.dt, self.nt = resolve_steps(config)
         k = _gpu_time_height(config)
         self.time_height = 1 if self.single_step else (k if k > 0 else DEFAULT_TIME_HEIGHT)
+        # the device fuses at most k_max steps per pass; deeper heights run as
+        # blocks of that depth, so the ghost depth follows the clamped k
+        self.k_max = device_max_time_height(config)
+        self.time_height = min(self.time_height, self.k_max)
         # one rank: time_height 0 lets the library measure k on this grid
         # (AcousticProp::autotune_k); several ranks share the ghost depth of
         # an explicit k
@@ -184,6 +191,10 @@ class SlabRunner:
             _lib.require_device()
             backend_factory = DeviceSlab
         self.dev = backend_factory(config, self.dt, v_max, self.lo, self.nl)
+        dev_max = getattr(self.dev, "max_time_height", None)
+        if dev_max is not None and dev_max() != self.k_max:
+            raise RuntimeError(f"library fuses {dev_max()} steps per pass, host rule says "
+                               f"{self.k_max}")
         # sources: the global inspector support, restricted on the device
         spec = config.sources
         if spec is not None and spec.nsrc and self.nt > 0:

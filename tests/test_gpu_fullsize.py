@@ -72,6 +72,73 @@ def test_cfg2_fused_vs_reference_kernel_and_k2(cfg2_inputs):
     assert np.abs(a.fields["u"]).max() > 0
 
 
+NEAR_SOURCE_Z = 105.0      # tests/golden/make_big_runs.py (cfg2_near)
+
+
+def _golden_big_runs():
+    import json
+    path = os.path.join(os.path.dirname(__file__), "golden", "big_runs.json")
+    return json.load(open(path))
+
+
+def _sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _assert_golden(res, g):
+    """The device run reproduces the REAL reference's full-size run bit for
+    bit: sha256 checksum (engine.py:450-455), field and trace digests."""
+    assert _sha(res.fields["u"]) == g["field_sha"]
+    assert _sha(res.receivers) == g["receivers_sha"]
+    assert res.report.checksum == g["checksum"]
+
+
+@pytest.mark.parametrize("k", [1, 2])
+@pytest.mark.parametrize("variant", ["cfg2", "cfg2_near"])
+def test_cfg2_checksum_equals_reference_full_size(cfg2_inputs, variant, k):
+    """cfg2 at full size (592^3, so=8, 262,144 receivers, nt=16) against
+    digests of stencil_tb.run on the same seeded arrays
+    (tests/golden/make_big_runs.py).  cfg2_near moves the source 105 m deep
+    so the traces are non-zero within 16 steps."""
+    g = _golden_big_runs()[variant]
+    v, src, rec = cfg2_inputs
+    if variant == "cfg2_near":
+        src = src.copy()
+        src[:, 2] = NEAR_SOURCE_Z
+    res = stb.run(bench.make_config(stb, v, src, rec, g["nt"], k))
+    assert res.report.schedule["time_height"] == k
+    _assert_golden(res, g)
+    if variant == "cfg2_near":
+        assert np.count_nonzero(res.receivers) > 0
+
+
+@pytest.mark.parametrize("so", [4, 8, 12])
+def test_cfg3_checksum_equals_reference_full_size(cfg2_inputs, so):
+    """cfg3 at full size (4096 sources with per-source wavelets, 10^4
+    receivers, nt=8) against stencil_tb.run digests, at k = 1 and (so 4/8)
+    k = 2."""
+    g = _golden_big_runs()[f"cfg3_so{so}"]
+    nt = g["nt"]
+    v, _, _ = cfg2_inputs
+    rng = np.random.default_rng(3)
+    src = rng.uniform(0.0, 5110.0, size=(4096, 3))
+    rec = rng.uniform(0.0, 5110.0, size=(10000, 3))
+    f0 = rng.uniform(8.0, 20.0, size=4096)
+    t0 = 1.0 / f0 + rng.uniform(0.0, 0.05, size=4096)
+    wav = np.stack([stb.ricker(f, t, 0.8e-3, nt).samples for f, t in zip(f0, t0)],
+                   axis=1)
+    grid = stb.GridSpec(bench.SHAPE, (10.0,) * 3, (-400.0,) * 3, boundary_layers=40)
+    for k in ([1, 2] if so in (4, 8) else [1]):
+        cfg = stb.RunConfig(physics="acoustic", grid=grid, space_order=so, nt=nt,
+                            dt=0.8e-3, medium={"velocity": v},
+                            sources=stb.SourceSpec(src, wavelets=wav), receiver_coords=rec,
+                            schedule=stb.ScheduleSpec("gpu", time_height=k))
+        res = stb.run(cfg)
+        assert res.report.schedule["time_height"] == k
+        _assert_golden(res, g)
+
+
 def test_cfg2_xslab_two_handles_full_size(cfg2_inputs):
     """x-slab decomposition (two slab handles, device ghost copies in the
     order of the multi-rank loop) equals the single-device run at 592^3."""

@@ -49,12 +49,20 @@ def test_run_bitexact_vs_reference(name, golden_runs):
 
 @pytest.mark.parametrize("name", ["ac_so4_24", "ac_so8_het_32", "ac_so12_28", "ac_aniso_so8",
                                   "ac_dense_src"])
-@pytest.mark.parametrize("k", [2, 3, 4])
-def test_temporal_blocking_is_bitwise_invariant(name, k, golden_runs):
-    """Fusing k steps per HBM pass must not change a single bit."""
+@pytest.mark.parametrize("k_requested", [2, 3, 4])
+def test_time_height_request_is_bitwise_invariant(name, k_requested, golden_runs):
+    """A wavefront height k must not change a single bit.  The device fuses
+    min(k, max_time_height) steps per HBM pass (2 at so 2/4/8, 1 at so=12)
+    and runs deeper heights as consecutive blocks of that depth (k = 3: 2+1
+    blocks); the report states the depth actually fused."""
     arrays, meta = golden_runs
     case = build_case(name)
-    res = stb.run(to_config(case, stb, schedule=stb.ScheduleSpec("gpu", time_height=k)))
+    res = stb.run(to_config(case, stb, schedule=stb.ScheduleSpec("gpu", time_height=k_requested)))
+    sch = res.report.schedule
+    assert sch["time_height_requested"] == k_requested
+    assert sch["time_height"] == min(k_requested, sch["max_time_height"])
+    if case["so"] in (4, 8) and case.get("precision", 32) == 32:
+        assert sch["time_height"] == 2 and "acoustic_wtb" in sch["device_plan"]
     fields = {kk: arrays[f"{name}/field/{kk}"] for kk in meta[name]["fields"]}
     assert_parity(res, fields, arrays[f"{name}/receivers"], meta[name]["checksum"])
 
