@@ -279,6 +279,61 @@ int stb_prop_describe(stb_prop_t p, int32_t time_height, char* buf, int64_t bufl
 int stb_prop_max_time_height(stb_prop_t p, int32_t* k);
 int stb_prop_destroy(stb_prop_t p);
 
+/* ------------------------------------------------------------------------
+ * Step-level operators (stepping.cu) on the reference's halo-padded level
+ * layout: TimeBufferedField.level(t) (grid.py:173-218) is a C-order
+ * (nx+2h, ny+2h, nz+2h) array with a zero halo.  All pointers below are
+ * DEVICE pointers in that layout (caller-owned, e.g. torch CUDA tensors);
+ * work is enqueued on `stream` (a cudaStream_t, NULL = legacy default) and
+ * not synchronised.  Boxes are half-open interior index ranges
+ * (grid.py:228-262).  Materials (inv, buoy, lam, mu, mu2) and the sponge
+ * factor are padded arrays of the same layout or NULL (scalar / no sponge),
+ * exactly as the reference models store them (physics.py:90-115).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int64_t padded[3];   /* nx + 2h, ny + 2h, nz + 2h */
+  int32_t halo;        /* h */
+  int32_t precision;   /* 32 or 64 */
+} stb_layout;
+
+typedef struct {
+  int64_t lo[3], hi[3];
+} stb_box;
+
+/* acoustic_update (physics.py:181-213).  active[3]: axes with > 1 point;
+ * weights[a*8 + r-1] = w_r / h_a^2, center = sum_a w_0 / h_a^2 (Python
+ * floats, rounded to the field dtype like NumPy's weak scalars). */
+int stb_box_acoustic_update(const stb_layout* L, void* dst, const void* u1, const void* u0,
+                            int32_t radius, const int32_t* active, double center,
+                            const double* weights, const void* inv, double inv_scalar,
+                            const void* dampfac, const stb_box* box, void* stream);
+/* elastic_update_v (physics.py:334-368): v_out/v_prev = vx vy vz at t / t-1,
+ * tau_prev = txx tyy tzz txy txz tyz at t-1; d1[a*8 + j-1] = c_j / h_a. */
+int stb_box_elastic_v(const stb_layout* L, void* const* v_out, const void* const* v_prev,
+                      const void* const* tau_prev, int32_t radius, const int32_t* active,
+                      const double* d1, const void* buoy, double buoy_scalar,
+                      const void* dampfac, const stb_box* box, void* stream);
+/* elastic_update_tau (physics.py:371-429): v_cur = vx vy vz at t. */
+int stb_box_elastic_tau(const stb_layout* L, void* const* tau_out, const void* const* tau_prev,
+                        const void* const* v_cur, int32_t radius, const int32_t* active,
+                        const double* d1, const void* lam, double lam_scalar, const void* mu,
+                        double mu_scalar, const void* mu2, double mu2_scalar,
+                        const void* dampfac, const stb_box* box, void* stream);
+/* scatter_box / fused_inject_row / inject_direct (precompute.py:209-252,
+ * sparse.py:176-194): dst[p_k] += T(values[k]) for the K support points
+ * (points K*3 int64, lexicographic, each once) that lie in the box. */
+int stb_box_scatter(const stb_layout* L, void* dst, const int64_t* points,
+                    const double* values, int64_t K, const stb_box* box, void* stream);
+/* gather_box (precompute.py:287-308): contrib[m] = w[m] * level[p_m] (f64)
+ * and in_box[m] = 1 for entries in the box, 0 (contrib 0) otherwise. */
+int stb_box_gather(const stb_layout* L, const void* src, const int64_t* points,
+                   const double* weights, int64_t M, const stb_box* box, double* contrib,
+                   uint8_t* in_box, void* stream);
+/* record_receivers (sparse.py:197-207): out[r] = sum of the 8 corner
+ * products w * level[corner] in NumPy's pairwise order; idx n*8*3, w n*8. */
+int stb_record_receivers(const stb_layout* L, const void* src, const int64_t* idx,
+                         const double* w, int64_t n, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,8 @@ EXPORTS = (
     "stb_prop_describe",
     "stb_prop_max_time_height",
     "stb_prop_destroy",
+    "stb_box_acoustic_update", "stb_box_elastic_v", "stb_box_elastic_tau", "stb_box_scatter",
+    "stb_box_gather", "stb_record_receivers",
 )
 
 
@@ -61,6 +63,15 @@ class ElasticDesc(C.Structure):
                 ("mu_scalar", C.c_double), ("rho_scalar", C.c_double),
                 ("damp", C.POINTER(C.c_double) * 3), ("x_begin", C.c_int64),
                 ("nx_local", C.c_int64)]
+
+
+class Layout(C.Structure):
+    """stb_layout: the halo-padded level layout of TimeBufferedField."""
+    _fields_ = [("padded", C.c_int64 * 3), ("halo", C.c_int32), ("precision", C.c_int32)]
+
+
+class Box(C.Structure):
+    _fields_ = [("lo", C.c_int64 * 3), ("hi", C.c_int64 * 3)]
 
 
 class TTIDesc(C.Structure):
@@ -119,6 +130,16 @@ def _declare(lib):
         "stb_prop_describe": ([P, i32, C.c_char_p, i64], C.c_int),
         "stb_prop_max_time_height": ([P, C.POINTER(i32)], C.c_int),
         "stb_prop_destroy": ([P], C.c_int),
+        "stb_box_acoustic_update": ([C.POINTER(Layout), P, P, P, i32, pi32, dbl, pdbl, P, dbl,
+                                     P, C.POINTER(Box), P], C.c_int),
+        "stb_box_elastic_v": ([C.POINTER(Layout), C.POINTER(P), C.POINTER(P), C.POINTER(P), i32,
+                               pi32, pdbl, P, dbl, P, C.POINTER(Box), P], C.c_int),
+        "stb_box_elastic_tau": ([C.POINTER(Layout), C.POINTER(P), C.POINTER(P), C.POINTER(P),
+                                 i32, pi32, pdbl, P, dbl, P, dbl, P, dbl, P, C.POINTER(Box), P],
+                                C.c_int),
+        "stb_box_scatter": ([C.POINTER(Layout), P, P, P, i64, C.POINTER(Box), P], C.c_int),
+        "stb_box_gather": ([C.POINTER(Layout), P, P, P, i64, C.POINTER(Box), P, P, P], C.c_int),
+        "stb_record_receivers": ([C.POINTER(Layout), P, P, P, i64, P, P], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

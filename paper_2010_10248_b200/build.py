@@ -51,6 +51,13 @@ def build(verbose: bool = False, force: bool = False, extra: list[str] | None = 
     """Compile and link; returns the library path."""
     extra = extra or []
     os.makedirs(OBJ, exist_ok=True)
+    # objects built with other flags (A/B -D switches) are stale: the flag set
+    # is stamped next to them and a change forces a full rebuild
+    stamp = os.path.join(OBJ, "flags.stamp")
+    flags = " ".join(NVCC_FLAGS + list(extra))
+    old = open(stamp).read() if os.path.exists(stamp) else None
+    if old != flags:
+        force = True
     sources = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
     hdr = _newest_header()
     jobs = []
@@ -77,6 +84,9 @@ def build(verbose: bool = False, force: bool = False, extra: list[str] | None = 
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")
         os.replace(tmp, LIB)
+    if old != flags:
+        with open(stamp, "w") as fh:
+            fh.write(flags)
     return LIB
 
 

@@ -226,3 +226,16 @@ def tti_medium(medium: dict, shape=None) -> TTIMedium:
     if np.ndim(th) == 0 and np.ndim(ph) == 0:
         axis = tuple(float(c) for c in axis)
     return TTIMedium(vp, e2, d2, axis)
+
+
+_STEP_API = ('AcousticModel', 'ElasticModel', 'acoustic_update', 'elastic_update_v', 'elastic_update_tau')
+
+
+def __getattr__(name):
+    """The step-level (device-resident) operators of this reference module
+    live in stepping.py; they are reachable under the reference's module
+    path too (e.g. ``precompute.apply_gather``)."""
+    if name in _STEP_API:
+        from . import stepping
+        return getattr(stepping, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

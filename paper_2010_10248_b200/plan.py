@@ -57,24 +57,29 @@ class DependenceSpec:
         return [f for g in self.groups for f in g]
 
 
+def _shape(grid_or_shape) -> tuple:
+    """A GridSpec (the reference's argument) or a plain shape tuple."""
+    return tuple(getattr(grid_or_shape, "shape", grid_or_shape))
+
+
 def _radius(r: int, shape) -> tuple:
+    shape = _shape(shape)
     return tuple(r if shape[a] > 1 else 0 for a in range(3))
 
 
-def acoustic_deps(radius: int, shape) -> DependenceSpec:
-    """u <- u(t-1, R), u(t-2, 0) (schedule.py:76-82)."""
-    return DependenceSpec([["u"]], {"u": [Dep("u", -1, _radius(radius, shape)),
-                                          Dep("u", -2, (0, 0, 0))]},
-                          inject_fields=("u",), gather_field="u")
+def acoustic_deps(radius: int, grid) -> DependenceSpec:
+    """u <- u(t-1, R), u(t-2, 0) (schedule.py:76-82).  Sparse fields are
+    left unset, as in the reference (the engine assigns them)."""
+    return DependenceSpec([["u"]], {"u": [Dep("u", -1, _radius(radius, grid)),
+                                          Dep("u", -2, (0, 0, 0))]})
 
 
-def elastic_deps(radius: int, shape) -> DependenceSpec:
+def elastic_deps(radius: int, grid) -> DependenceSpec:
     """v <- tau(t-1, R), v(t-1, 0); tau <- v(t, R), tau(t-1, 0) (schedule.py:85-95)."""
-    r = _radius(radius, shape)
+    r = _radius(radius, grid)
     return DependenceSpec([["v"], ["tau"]],
                           {"v": [Dep("tau", -1, r), Dep("v", -1, (0, 0, 0))],
-                           "tau": [Dep("v", 0, r), Dep("tau", -1, (0, 0, 0))]},
-                          inject_fields=("tau",), gather_field="tau")
+                           "tau": [Dep("v", 0, r), Dep("tau", -1, (0, 0, 0))]})
 
 
 def tti_deps(radius: int, shape) -> DependenceSpec:
@@ -87,12 +92,17 @@ def tti_deps(radius: int, shape) -> DependenceSpec:
 
 
 def deps_for(physics: str, space_order: int, shape) -> DependenceSpec:
+    """Dependences with the engine's sparse-operator fields (engine.py:390-392)."""
     R = space_order // 2
     if physics == "elastic":
-        return elastic_deps(R, shape)
+        d = elastic_deps(R, shape)
+        d.inject_fields, d.gather_field = ("tau",), "tau"
+        return d
     if physics == "tti":
         return tti_deps(R, shape)
-    return acoustic_deps(R, shape)
+    d = acoustic_deps(R, shape)
+    d.inject_fields, d.gather_field = ("u",), "u"
+    return d
 
 
 @dataclass(frozen=True)
@@ -120,6 +130,201 @@ class Violation:
                 f"{self.count} point(s), e.g. {self.example}")
 
 
+# --------------------------------------------------------------- host plans
+#
+# The reference's loop-nest plans (schedule.py:98-310), for callers that
+# drive the step-level operators (acoustic_update, scatter_box, gather_box,
+# ...) themselves.  run() never enumerates them: on the device every plan
+# maps to the fused sweep (DevicePlan below); these objects keep their
+# legality rules and the exact command stream the reference produces.
+
+PLANE_AXES = (0, 1)   # x, y are tiled; z stays the inner full sweep
+
+
+@dataclass
+class SpacePlan:
+    """Time-outermost plan: ``naive`` (direct sparse ops after each sweep)
+    or ``space`` ((x, y) blocks with fused sparse ops) (schedule.py:112-126)."""
+
+    deps: DependenceSpec
+    kind: str = "naive"
+    block_shape: tuple | None = None
+
+    def __post_init__(self):
+        if self.kind not in ("naive", "space"):
+            raise InvalidPlanError(f"unknown space plan kind {self.kind!r}")
+        if self.block_shape is not None and min(self.block_shape) < 1:
+            raise InvalidPlanError(f"block shape must be >= 1, got {self.block_shape}")
+
+
+@dataclass
+class WavefrontPlan:
+    """Skewed temporal blocking over (x, y) (schedule.py:129-138)."""
+
+    deps: DependenceSpec
+    tile_shape: tuple
+    time_height: int
+    block_shape: tuple
+    skew: tuple
+    offsets: dict
+    kind: str = "wavefront"
+
+
+def stage_offsets(deps: DependenceSpec) -> tuple[dict, tuple]:
+    """Per-field footprint offsets and the per-step skew (schedule.py:139-168).
+
+    A field read at the same step by a later field shifts that field's
+    footprint by the read radius (offset[f] >= offset[g] + r); a read of an
+    earlier step dt < 0 needs skew >= ceil((r + offset[g] - offset[f]) / |dt|).
+    """
+    offs: dict = {}
+    for group in deps.groups:
+        for f in group:
+            o = [0, 0]
+            for d in deps.deps.get(f, []):
+                if d.dt != 0:
+                    continue
+                if d.field not in offs:
+                    raise InvalidPlanError(f"{f} reads {d.field} at the same step but "
+                                           f"{d.field} is not updated earlier in the step")
+                o = [max(o[a], offs[d.field][a] + d.radius[a]) for a in PLANE_AXES]
+            offs[f] = tuple(o)
+    skew = [0, 0]
+    for f, reads in deps.deps.items():
+        for d in reads:
+            if d.dt < 0:
+                for a in PLANE_AXES:
+                    skew[a] = max(skew[a], -(-(d.radius[a] + offs[d.field][a] - offs[f][a])
+                                             // -d.dt))
+    return offs, tuple(skew)
+
+
+def make_wavefront_plan(grid, deps: DependenceSpec, time_height: int, tile_shape,
+                        block_shape=None, force_skew=None) -> WavefrontPlan:
+    """schedule.py:171-207: derive skew/offsets, check tile > skew * T on
+    every non-degenerate tiled axis.  ``force_skew`` overrides the skew
+    (mutation tests), never the shape checks."""
+    if time_height < 1:
+        raise InvalidPlanError(f"time_height must be >= 1, got {time_height}")
+    tile = (int(tile_shape[0]), int(tile_shape[1]))
+    if min(tile) < 1:
+        raise InvalidPlanError(f"tile shape must be >= 1, got {tile}")
+    offs, skew = stage_offsets(deps)
+    if force_skew is not None:
+        skew = (int(force_skew[0]), int(force_skew[1]))
+    shape = _shape(grid)
+    for a in PLANE_AXES:
+        if shape[a] > 1 and tile[a] <= skew[a] * time_height:
+            raise InvalidPlanError(f"tile extent {tile[a]} on axis {a} must exceed "
+                                   f"skew*time_height = {skew[a] * time_height}")
+    block = tile if block_shape is None else (int(block_shape[0]), int(block_shape[1]))
+    if min(block) < 1:
+        raise InvalidPlanError(f"block shape must be >= 1, got {block}")
+    return WavefrontPlan(deps=deps, tile_shape=tile, time_height=int(time_height),
+                         block_shape=block, skew=skew, offsets=offs)
+
+
+def naive_plan(deps: DependenceSpec) -> SpacePlan:
+    return SpacePlan(deps=deps, kind="naive")
+
+
+def space_plan(deps: DependenceSpec, block_shape=None) -> SpacePlan:
+    return SpacePlan(deps=deps, kind="space", block_shape=block_shape)
+
+
+def _split_xy(box: Box, block) -> list:
+    """(x, y) blocks of a box, x-major, z whole (schedule.py:210-218)."""
+    if block is None:
+        return [box]
+    (x0, x1), (y0, y1), zr = box
+    return [((xa, min(xa + block[0], x1)), (ya, min(ya + block[1], y1)), zr)
+            for xa in range(x0, x1, block[0]) for ya in range(y0, y1, block[1])]
+
+
+def _task(f: str, t: int, box: Box, deps: DependenceSpec) -> tuple:
+    """stencil, then fused inject / gather of the same box (schedule.py:221-236)."""
+    cmds = [Cmd("stencil", f, t, box)]
+    if f in deps.inject_fields:
+        cmds.append(Cmd("inject", f, t, box))
+    if f == deps.gather_field:
+        cmds.append(Cmd("gather", f, t, box))
+    return tuple(cmds)
+
+
+def enumerate_updates(plan, grid, nt: int):
+    """Block sets (lists of tasks; tasks of a set write disjoint boxes and may
+    run concurrently, sets are separated by barriers) realising the plan
+    over nt steps (schedule.py:239-310).  The multiset of stencil updates is
+    the naive schedule's."""
+    shape = _shape(grid)
+    if isinstance(plan, SpacePlan):
+        return _space_sets(plan, shape, nt)
+    if isinstance(plan, WavefrontPlan):
+        return _wavefront_sets(plan, shape, nt)
+    raise InvalidPlanError(f"unknown plan type {type(plan).__name__}")
+
+
+def _space_sets(plan: SpacePlan, shape, nt: int):
+    deps = plan.deps
+    full = tuple((0, n) for n in shape)
+    for t in range(nt):
+        for group in deps.groups:
+            if plan.kind == "naive":
+                yield [(Cmd("stencil", f, t, full),) for f in group]
+            else:
+                yield [_task(f, t, b, deps) for f in group
+                       for b in _split_xy(full, plan.block_shape)]
+        if plan.kind != "naive":
+            continue
+        if deps.inject_fields and deps.inject_points is not None:
+            yield [tuple(Cmd("inject_direct", f, t, full) for f in deps.inject_fields)]
+        if deps.gather_field is not None and deps.gather_points is not None:
+            yield [(Cmd("record", deps.gather_field, t, full),)]
+
+
+def _wavefront_sets(plan: WavefrontPlan, shape, nt: int):
+    deps = plan.deps
+    nx, ny, nz = shape
+    sk = plan.skew
+    tile = plan.tile_shape
+    reach = [max(o[a] for o in plan.offsets.values()) for a in PLANE_AXES]
+    for t0 in range(0, nt, plan.time_height):
+        height = min(plan.time_height, nt - t0)
+        # enough tiles that the last one, shifted back by the skew, still
+        # covers the far face at the deepest step
+        n_tiles = [max(1, math.ceil((shape[a] + sk[a] * (height - 1) + reach[a]) / tile[a]))
+                   for a in PLANE_AXES]
+        for ix in range(n_tiles[0]):
+            for iy in range(n_tiles[1]):
+                for j in range(height):
+                    for group in deps.groups:
+                        tasks = []
+                        for f in group:
+                            lo = [(ix, iy)[a] * tile[a] - sk[a] * j - plan.offsets[f][a]
+                                  for a in PLANE_AXES]
+                            box = ((max(lo[0], 0), min(lo[0] + tile[0], nx)),
+                                   (max(lo[1], 0), min(lo[1] + tile[1], ny)), (0, nz))
+                            if box[0][0] >= box[0][1] or box[1][0] >= box[1][1]:
+                                continue
+                            tasks.extend(_task(f, t0 + j, b, deps)
+                                         for b in _split_xy(box, plan.block_shape))
+                        if tasks:
+                            yield tasks
+
+
+def describe_plan(plan) -> str:
+    """One property per line (schedule.py:423-436)."""
+    out = [f"kind: {plan.kind}"]
+    if isinstance(plan, SpacePlan):
+        out.append(f"block_shape: {plan.block_shape}")
+    else:
+        out += [f"tile_shape: {plan.tile_shape}", f"time_height: {plan.time_height}",
+                f"block_shape: {plan.block_shape}", f"skew: {plan.skew}"]
+        out += [f"offset[{f}]: {plan.offsets[f]}" for f in plan.deps.fields]
+    out.append(f"fields: {','.join(plan.deps.fields)}")
+    return "\n".join(out) + "\n"
+
+
 # --------------------------------------------------------------- validator
 
 def _inside(pts: np.ndarray, box: Box) -> np.ndarray:
@@ -129,7 +334,7 @@ def _inside(pts: np.ndarray, box: Box) -> np.ndarray:
     return m
 
 
-def validate_schedule(stream, deps: DependenceSpec, shape, max_violations: int = 1000):
+def validate_schedule(stream, deps: DependenceSpec, grid, max_violations: int = 1000):
     """Replay ``stream`` (iterable of block sets = lists of tasks = tuples
     of Cmd) against last-written-time state; report every read of a value
     that does not exist yet and every injection before its point's update
@@ -140,7 +345,7 @@ def validate_schedule(stream, deps: DependenceSpec, shape, max_violations: int =
     CTA (visible to the task only), ``store`` commits a task-computed box to
     memory; commits keep the newest level per point (the device keeps a ring
     of levels, so writing an older level never hides a newer one)."""
-    shape = tuple(shape)
+    shape = _shape(grid)
     last = {f: np.full(shape, -1, dtype=np.int32) for f in deps.fields}
     out: list[Violation] = []
 
@@ -193,9 +398,9 @@ def validate_schedule(stream, deps: DependenceSpec, shape, max_violations: int =
                         commits.append((cmd.field, cmd.box, cmd.t))
                 elif cmd.op == "store":
                     commits.append((cmd.field, cmd.box, cmd.t))
-                elif cmd.op == "inject":
+                elif cmd.op in ("inject", "inject_direct"):
                     sparse_check(cmd, deps.inject_points, "inject-before-stencil", local)
-                elif cmd.op == "gather":
+                elif cmd.op in ("gather", "record"):
                     sparse_check(cmd, deps.gather_points, "read-before-write", local)
                 else:
                     raise InvalidPlanError(f"unknown command op {cmd.op!r}")

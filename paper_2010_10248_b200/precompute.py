@@ -265,3 +265,16 @@ def _in_box(pts: np.ndarray, box: Box) -> np.ndarray:
     (x0, x1), (y0, y1), (z0, z1) = box
     return ((pts[:, 0] >= x0) & (pts[:, 0] < x1) & (pts[:, 1] >= y0) & (pts[:, 1] < y1)
             & (pts[:, 2] >= z0) & (pts[:, 2] < z1))
+
+
+_STEP_API = ('fused_inject_row', 'scatter_box', 'scatter_all', 'gather_box', 'apply_gather')
+
+
+def __getattr__(name):
+    """The step-level (device-resident) operators of this reference module
+    live in stepping.py; they are reachable under the reference's module
+    path too (e.g. ``precompute.apply_gather``)."""
+    if name in _STEP_API:
+        from . import stepping
+        return getattr(stepping, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -168,3 +168,16 @@ def validate_coords_in_extent(coords, grid: GridSpec, margin_points: int = 0,
             raise OutOfDomainError(
                 f"{what} {tuple(c[i])} outside allowed region on axis {a}: "
                 f"index {frac[i, a]:.6g} not in [{lo}, {hi}]")
+
+
+_STEP_API = ('inject_direct', 'record_receivers')
+
+
+def __getattr__(name):
+    """The step-level (device-resident) operators of this reference module
+    live in stepping.py; they are reachable under the reference's module
+    path too (e.g. ``precompute.apply_gather``)."""
+    if name in _STEP_API:
+        from . import stepping
+        return getattr(stepping, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -110,3 +110,27 @@ def test_bad_plans_rejected():
     text = plan.describe_device_plan(plan.DevicePlan(k=2, tile=(150, 16, 64), skew=4),
                                      (592, 592, 592))
     assert "halo_per_level: [4, 0]" in text
+
+
+def test_host_plans_match_reference_streams():
+    """naive/space/wavefront plans, enumerate_updates, describe_plan and
+    validate_schedule reproduce the reference's command streams exactly
+    (tests/golden/plans.json, made by running stencil_tb)."""
+    import json
+    import os
+
+    from golden import make_plan_golden as mk
+    import paper_2010_10248_b200 as stb
+    golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "plans.json")))
+    cases = mk.cases()
+    assert len(golden) == len(cases)
+    for c, g in zip(cases, golden):
+        assert mk.run_case(stb, c) == g, c
+
+
+def test_host_plan_api_exported():
+    import paper_2010_10248_b200 as stb
+    for name in ("Cmd", "Dep", "DependenceSpec", "SpacePlan", "Violation", "WavefrontPlan",
+                 "acoustic_deps", "describe_plan", "elastic_deps", "enumerate_updates",
+                 "make_wavefront_plan", "naive_plan", "space_plan", "validate_schedule"):
+        assert hasattr(stb, name), name
