@@ -261,6 +261,11 @@ int stb_prop_write_snapshot(stb_prop_t p, int32_t field, int64_t t, const char* 
 int stb_prop_stream(stb_prop_t p, void** stream);
 int stb_prop_async_begin(stb_prop_t p, int64_t t0, int64_t nsteps);
 int stb_prop_step_async(stb_prop_t p, int64_t t, int32_t kb, int64_t x_lo, int64_t x_hi);
+/* Elastic x slabs: one half step of step t (phase 0: v, physics.py:334-368;
+ * phase 1: tau + injection, physics.py:371-429) over local planes
+ * [x_lo, x_hi), so R ghost planes of the half step's fields can be exchanged
+ * between the halves (step_async runs both). */
+int stb_prop_half_step_async(stb_prop_t p, int64_t t, int32_t phase, int64_t x_lo, int64_t x_hi);
 int stb_prop_gather_async(stb_prop_t p, int64_t t, int32_t kb);
 int stb_prop_async_finish(stb_prop_t p, double* rec_out, int64_t* bad_step);
 /* Zero all time levels (reuse a handle for another shot). */

@@ -32,7 +32,7 @@ EXPORTS = (
     "stb_elastic_create", "stb_tti_create", "stb_prop_set_sources", "stb_prop_set_receivers", "stb_prop_run",
     "stb_prop_read_field", "stb_prop_level_ptr", "stb_prop_write_snapshot", "stb_prop_stream", "stb_prop_async_begin", "stb_prop_set_receiver_field",
     "stb_prop_set_damping",
-    "stb_prop_step_async", "stb_prop_gather_async", "stb_prop_async_finish", "stb_prop_reset", "stb_prop_stats",
+    "stb_prop_step_async", "stb_prop_half_step_async", "stb_prop_gather_async", "stb_prop_async_finish", "stb_prop_reset", "stb_prop_stats",
     "stb_prop_describe",
     "stb_prop_max_time_height",
     "stb_prop_destroy",
@@ -123,6 +123,7 @@ def _declare(lib):
         "stb_prop_set_damping": ([P, pdbl, pdbl, pdbl], C.c_int),
         "stb_prop_async_begin": ([P, i64, i64], C.c_int),
         "stb_prop_step_async": ([P, i64, i32, i64, i64], C.c_int),
+        "stb_prop_half_step_async": ([P, i64, i32, i64, i64], C.c_int),
         "stb_prop_gather_async": ([P, i64, i32], C.c_int),
         "stb_prop_async_finish": ([P, pdbl, pi64], C.c_int),
         "stb_prop_reset": ([P], C.c_int),

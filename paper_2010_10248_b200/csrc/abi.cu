@@ -255,6 +255,14 @@ STB_API int stb_prop_step_async(stb_prop_t p, int64_t t, int32_t kb, int64_t x_l
   })
 }
 
+STB_API int stb_prop_half_step_async(stb_prop_t p, int64_t t, int32_t phase, int64_t x_lo,
+                                     int64_t x_hi) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr, STB_ERR_ARG, "NULL handle");
+    p->half_step_async(t, phase, x_lo, x_hi);
+  })
+}
+
 STB_API int stb_prop_gather_async(stb_prop_t p, int64_t t, int32_t kb) {
   STB_GUARD({
     STB_REQUIRE(p != nullptr, STB_ERR_ARG, "NULL handle");

@@ -14,10 +14,10 @@
 //
 // Layout: every field is stored with a zero halo of H >= R points on all
 // sides (never written), interior z starting 128-byte aligned, so neighbour
-// loads need no bounds checks.  Kernels are 2.5-D x sweeps: a block of
-// 32 (z) x 16 (y) threads walks an x chunk; the three fields differentiated
-// along x live in register queues of 2R+1 planes (loop unrolled by 2R+1),
-// y/z neighbours come through L1.
+// loads need no bounds checks.  f32 3-D grids run the TMA-tiled 2.5-D x
+// sweeps of elastic_tiled.cuh; f64 and degenerate grids the thread-per-point
+// kernels below.  Every launch covers a local x range [x_lo, x_hi) (x-slab
+// runs compute owned planes only and exchange R ghost planes per half step).
 #include <cstdlib>
 #include <memory>
 #include <sstream>
@@ -55,7 +55,7 @@ struct ElArgs {
   int has_fac;
   ElCoefs<T> cf;
   PDims d;
-  int cx;                 // x chunk length
+  int x_lo, x_hi;         // local planes computed by this launch
   int* nonfinite;         // guard flag (NULL: no check this step)
 };
 
@@ -74,212 +74,6 @@ __device__ __forceinline__ T stag(const G& g, const T* c, bool fwd) {
 }
 
 // ---------------------------------------------------------------------------
-// velocity half step: v[t] = (v[t-1] + div(tau[t-1]) * buoy) * fac
-// x derivatives from register queues of txx, txy, txz.
-// ---------------------------------------------------------------------------
-template <typename T, int R>
-__global__ void __launch_bounds__(256, 3)
-elastic_v_sweep(ElArgs<T> a) {
-  constexpr int Q = 2 * R + 1;
-  const int z = blockIdx.x * 32 + threadIdx.x;
-  const int y = blockIdx.y * 8 + threadIdx.y;
-  const int x0 = blockIdx.z * a.cx;
-  const int x1 = min(x0 + a.cx, (int)a.d.nx);
-  if (z >= a.d.nz || y >= a.d.ny) return;
-  const int ys = (int)a.d.pitch, xs = (int)a.d.plane;
-  const ElCoefs<T>& cf = a.cf;
-  const T* __restrict__ txx = a.f[TXX];
-  const T* __restrict__ txy = a.f[TXY];
-  const T* __restrict__ txz = a.f[TXZ];
-  const T* __restrict__ tyy = a.f[TYY];
-  const T* __restrict__ tyz = a.f[TYZ];
-  const T* __restrict__ tzz = a.f[TZZ];
-  T qxx[Q], qxy[Q], qxz[Q];
-#pragma unroll
-  for (int s = 0; s < Q; ++s) qxx[s] = qxy[s] = qxz[s] = T(0);
-  const int N = (x1 - x0) + 2 * R;
-  const int base = (int)a.d.at(x0 - R, y, z);      // offset of queue plane n = 0
-  const T fyz = a.has_fac ? tmin(a.fy[y], a.fz[z]) : T(1);
-  int bad = 0;
-  for (int nb = 0; nb < N; nb += Q) {
-#pragma unroll
-    for (int qq = 0; qq < Q; ++qq) {
-      const int n = nb + qq;
-      if (n < N) {
-        const int ip = base + n * xs;
-        qxx[qq] = txx[ip];
-        qxy[qq] = txy[ip];
-        qxz[qq] = txz[ip];
-        if (n >= 2 * R) {
-          const int x = x0 - 2 * R + n;
-          const int i = ip - R * xs;   // centre of the output plane
-          const int cs = (qq - R + Q) % Q;
-          auto qx = [&](const T* q) { return [=](int o) { return q[(cs + o + Q) % Q]; }; };
-          auto gy = [&](const T* p) { return [=](int o) { return p[i + o * ys]; }; };
-          auto gz = [&](const T* p) { return [=](int o) { return p[i + o]; }; };
-          // elastic_update_v (physics.py:348-362), inactive axes skipped
-          T d[3];
-          bool h[3] = {false, false, false};
-#pragma unroll
-          for (int k = 0; k < 3; ++k) d[k] = T(0);
-          if (cf.active[0]) {
-            d[0] = stag<T, R>(qx(qxx), cf.d1[0], true);
-            d[1] = stag<T, R>(qx(qxy), cf.d1[0], false);
-            d[2] = stag<T, R>(qx(qxz), cf.d1[0], false);
-            h[0] = h[1] = h[2] = true;
-          }
-          if (cf.active[1]) {
-            const T e0 = stag<T, R>(gy(txy), cf.d1[1], false);
-            const T e1 = stag<T, R>(gy(tyy), cf.d1[1], true);
-            const T e2 = stag<T, R>(gy(tyz), cf.d1[1], false);
-            d[0] = h[0] ? radd(d[0], e0) : e0;
-            d[1] = h[1] ? radd(d[1], e1) : e1;
-            d[2] = h[2] ? radd(d[2], e2) : e2;
-            h[0] = h[1] = h[2] = true;
-          }
-          if (cf.active[2]) {
-            const T e0 = stag<T, R>(gz(txz), cf.d1[2], false);
-            const T e1 = stag<T, R>(gz(tyz), cf.d1[2], false);
-            const T e2 = stag<T, R>(gz(tzz), cf.d1[2], true);
-            d[0] = h[0] ? radd(d[0], e0) : e0;
-            d[1] = h[1] ? radd(d[1], e1) : e1;
-            d[2] = h[2] ? radd(d[2], e2) : e2;
-            h[0] = h[1] = h[2] = true;
-          }
-          const T buoy = a.buoy ? a.buoy[i] : cf.buoy;
-          const T fac = a.has_fac ? tmin(a.fx[x], fyz) : T(1);
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            T* v = a.f[VX + k];
-            T o = v[i];
-            if (h[k]) o = radd(o, rmul(d[k], buoy));
-            if (a.has_fac) o = rmul(o, fac);
-            v[i] = o;
-            if (a.nonfinite) bad |= !finite(o);
-          }
-        }
-      }
-    }
-  }
-  if (a.nonfinite && bad) atomicExch(a.nonfinite, 1);
-}
-
-// ---------------------------------------------------------------------------
-// stress half step (physics.py:385-429); x derivatives from register queues
-// of vx, vy, vz.
-// ---------------------------------------------------------------------------
-template <typename T, int R>
-__global__ void __launch_bounds__(256, 3)
-elastic_tau_sweep(ElArgs<T> a) {
-  constexpr int Q = 2 * R + 1;
-  const int z = blockIdx.x * 32 + threadIdx.x;
-  const int y = blockIdx.y * 8 + threadIdx.y;
-  const int x0 = blockIdx.z * a.cx;
-  const int x1 = min(x0 + a.cx, (int)a.d.nx);
-  if (z >= a.d.nz || y >= a.d.ny) return;
-  const int ys = (int)a.d.pitch, xs = (int)a.d.plane;
-  const ElCoefs<T>& cf = a.cf;
-  const T* __restrict__ vx = a.f[VX];
-  const T* __restrict__ vy = a.f[VY];
-  const T* __restrict__ vz = a.f[VZ];
-  T qx_[Q], qy_[Q], qz_[Q];
-#pragma unroll
-  for (int s = 0; s < Q; ++s) qx_[s] = qy_[s] = qz_[s] = T(0);
-  const int N = (x1 - x0) + 2 * R;
-  const int base = (int)a.d.at(x0 - R, y, z);
-  const T fyz = a.has_fac ? tmin(a.fy[y], a.fz[z]) : T(1);
-  int bad = 0;
-  for (int nb = 0; nb < N; nb += Q) {
-#pragma unroll
-    for (int qq = 0; qq < Q; ++qq) {
-      const int n = nb + qq;
-      if (n < N) {
-        const int ip = base + n * xs;
-        qx_[qq] = vx[ip];
-        qy_[qq] = vy[ip];
-        qz_[qq] = vz[ip];
-        if (n >= 2 * R) {
-          const int x = x0 - 2 * R + n;
-          const int i = ip - R * xs;
-          const int cs = (qq - R + Q) % Q;
-          auto qx = [&](const T* q) { return [=](int o) { return q[(cs + o + Q) % Q]; }; };
-          auto gy = [&](const T* p) { return [=](int o) { return p[i + o * ys]; }; };
-          auto gz = [&](const T* p) { return [=](int o) { return p[i + o]; }; };
-          const T lam = a.lam ? a.lam[i] : cf.lam;
-          const T mu = a.mu ? a.mu[i] : cf.mu;
-          const T mu2 = rmul(mu, T(2));
-          const T fac = a.has_fac ? tmin(a.fx[x], fyz) : T(1);
-          T dg[3] = {T(0), T(0), T(0)};
-          if (cf.active[0]) dg[0] = stag<T, R>(qx(qx_), cf.d1[0], false);
-          if (cf.active[1]) dg[1] = stag<T, R>(gy(vy), cf.d1[1], false);
-          if (cf.active[2]) dg[2] = stag<T, R>(gz(vz), cf.d1[2], false);
-          T tr = T(0);
-          bool htr = false;
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            if (!cf.active[k]) continue;
-            tr = htr ? radd(tr, dg[k]) : dg[k];
-            htr = true;
-          }
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            T inc = T(0);
-            bool hi = false;
-            if (htr) {
-              inc = rmul(tr, lam);
-              hi = true;
-            }
-            if (cf.active[k]) {
-              const T d2 = rmul(dg[k], mu2);
-              inc = hi ? radd(inc, d2) : d2;
-              hi = true;
-            }
-            T* f = a.f[TXX + k];
-            T o = f[i];
-            if (hi) o = radd(o, inc);
-            if (a.has_fac) o = rmul(o, fac);
-            f[i] = o;
-            if (a.nonfinite) bad |= !finite(o);
-          }
-          // shear: txy (d_y vx, d_x vy), txz (d_z vx, d_x vz), tyz (d_z vy, d_y vz)
-          T s[3] = {T(0), T(0), T(0)};
-          bool hs[3] = {false, false, false};
-          // first terms
-          if (cf.active[1]) { s[0] = stag<T, R>(gy(vx), cf.d1[1], true); hs[0] = true; }
-          if (cf.active[2]) { s[1] = stag<T, R>(gz(vx), cf.d1[2], true); hs[1] = true; }
-          if (cf.active[2]) { s[2] = stag<T, R>(gz(vy), cf.d1[2], true); hs[2] = true; }
-          // second terms
-          if (cf.active[0]) {
-            const T e = stag<T, R>(qx(qy_), cf.d1[0], true);
-            s[0] = hs[0] ? radd(s[0], e) : e;
-            hs[0] = true;
-            const T e2 = stag<T, R>(qx(qz_), cf.d1[0], true);
-            s[1] = hs[1] ? radd(s[1], e2) : e2;
-            hs[1] = true;
-          }
-          if (cf.active[1]) {
-            const T e = stag<T, R>(gy(vz), cf.d1[1], true);
-            s[2] = hs[2] ? radd(s[2], e) : e;
-            hs[2] = true;
-          }
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            T* f = a.f[TXY + k];
-            T o = f[i];
-            if (hs[k]) o = radd(o, rmul(s[k], mu));
-            if (a.has_fac) o = rmul(o, fac);
-            f[i] = o;
-            if (a.nonfinite) bad |= !finite(o);
-          }
-        }
-      }
-    }
-  }
-  if (a.nonfinite && bad) atomicExch(a.nonfinite, 1);
-}
-
-
-// ---------------------------------------------------------------------------
 // Thread-per-point variants (default): full occupancy hides L1/L2 latency of
 // the ~110 neighbour loads per point; the zero halo removes all bounds checks.
 // ---------------------------------------------------------------------------
@@ -288,7 +82,7 @@ __global__ void __launch_bounds__(128)
 elastic_v_point(ElArgs<T> a) {
   const int z = blockIdx.x * 32 + threadIdx.x;
   const int y = blockIdx.y * 4 + threadIdx.y;
-  const int x = blockIdx.z;
+  const int x = a.x_lo + blockIdx.z;
   if (z >= a.d.nz || y >= a.d.ny) return;
   const int ys = (int)a.d.pitch, xs = (int)a.d.plane;
   const int i = (int)a.d.at(x, y, z);
@@ -348,7 +142,7 @@ __global__ void __launch_bounds__(128)
 elastic_tau_point(ElArgs<T> a) {
   const int z = blockIdx.x * 32 + threadIdx.x;
   const int y = blockIdx.y * 4 + threadIdx.y;
-  const int x = blockIdx.z;
+  const int x = a.x_lo + blockIdx.z;
   if (z >= a.d.nz || y >= a.d.ny) return;
   const int ys = (int)a.d.pitch, xs = (int)a.d.plane;
   const int i = (int)a.d.at(x, y, z);
@@ -462,20 +256,17 @@ __global__ void el_fill_kernel(T* __restrict__ dst, PDims d, T v) {
   }
 }
 
+// phase 0: v half step, 1: tau half step, over local planes [x_lo, x_hi)
 template <typename T, int R>
-void launch_sweeps(cudaStream_t st, const ElArgs<T>& a) {
-  if (a.cx <= 0) {
-    dim3 block(32, 4);
-    dim3 grid((unsigned)((a.d.nz + 31) / 32), (unsigned)((a.d.ny + 3) / 4), (unsigned)a.d.nx);
+void launch_point(cudaStream_t st, const ElArgs<T>& a, int phase) {
+  if (a.x_hi <= a.x_lo) return;
+  dim3 block(32, 4);
+  dim3 grid((unsigned)((a.d.nz + 31) / 32), (unsigned)((a.d.ny + 3) / 4),
+            (unsigned)(a.x_hi - a.x_lo));
+  if (phase == 0)
     elastic_v_point<T, R><<<grid, block, 0, st>>>(a);
+  else
     elastic_tau_point<T, R><<<grid, block, 0, st>>>(a);
-    return;
-  }
-  dim3 block(32, 8);
-  dim3 grid((unsigned)((a.d.nz + 31) / 32), (unsigned)((a.d.ny + 7) / 8),
-            (unsigned)((a.d.nx + a.cx - 1) / a.cx));
-  elastic_v_sweep<T, R><<<grid, block, 0, st>>>(a);
-  elastic_tau_sweep<T, R><<<grid, block, 0, st>>>(a);
 }
 
 }  // namespace
@@ -544,11 +335,8 @@ class ElasticProp final : public stb_prop_s {
       STB_CHECK_LAUNCH();
       STB_CUDA(cudaStreamSynchronize(st_));
     }
-    cx_ = 0;   // thread-per-point kernels (x sweeps: STB_ELASTIC_CX > 0)
-    if (const char* e = std::getenv("STB_ELASTIC_CX")) cx_ = std::atoi(e);
     // TMA-tiled sweeps (elastic_tiled.cuh): f32, 3-D, R <= 4
-    tiled_ = sizeof(T) == 4 && cf_.active[0] && cf_.active[1] && cf_.active[2] && R_ <= 4 &&
-             cx_ == 0;
+    tiled_ = sizeof(T) == 4 && cf_.active[0] && cf_.active[1] && cf_.active[2] && R_ <= 4;
     if (const char* e = std::getenv("STB_ELASTIC_PATH")) tiled_ = tiled_ && std::string(e) != "point";
     if (tiled_) setup_tiled();
     STB_REQUIRE(d_.total < (int64_t)INT32_MAX, STB_ERR_ARG,
@@ -623,14 +411,15 @@ class ElasticProp final : public stb_prop_s {
   }
 
   template <int R>
-  void launch_tiled_r(int* nonfinite) {
+  void launch_tiled_r(int* nonfinite, int phase, int x_lo, int x_hi) {
     // x chunk per CTA (measured at so=8: 512^3 256 planes 36.6 vs 150 planes
     // 36.0 Gpts/s -- half the warm-ups; 1024^3 35.95 vs 35.88)
     int cx = 256;
     if (const char* e = std::getenv("STB_EL_CX")) cx = std::max(8, std::atoi(e));
+    if (x_hi <= x_lo) return;
     auto grid_for = [&](int ty) {
       return dim3((unsigned)((d_.nz + kElTZ - 1) / kElTZ), (unsigned)((d_.ny + ty - 1) / ty),
-                  (unsigned)((d_.nx + cx - 1) / cx));
+                  (unsigned)((x_hi - x_lo + cx - 1) / cx));
     };
     ElTiledArgs a{};
     a.fx = reinterpret_cast<const float*>(fac_[0].p);
@@ -641,7 +430,10 @@ class ElasticProp final : public stb_prop_s {
       for (int j = 0; j < 8; ++j) a.cf.d1[ax][j] = (float)cf_.d1[ax][j];
     a.d = d_;
     a.cx = cx;
+    a.x_lo = x_lo;
+    a.x_hi = x_hi;
     a.nonfinite = nonfinite;
+    if (phase == 0) {
     // v half step: inputs txx tyy tzz txy txz tyz, updates vx vy vz
     ElTiledMaps mv{};
     for (int f = 0; f < 6; ++f) mv.f[f] = fmap_[TXX + f];
@@ -651,6 +443,8 @@ class ElasticProp final : public stb_prop_s {
     elastic_tiled<R, 0, kTYv, ns_v<R>(), kMBv>
         <<<grid_for(kTYv), CfgV<R>::THREADS, CfgV<R>::smem_bytes(), st_>>>(mv, a);
     STB_CHECK_LAUNCH();
+    return;
+    }
     // tau half step: inputs vx vy vz, updates the six stresses
     ElTiledMaps mt{};
     for (int f = 0; f < 3; ++f) mt.f[f] = fmap_[VX + f];
@@ -662,18 +456,62 @@ class ElasticProp final : public stb_prop_s {
     STB_CHECK_LAUNCH();
   }
 
-  void launch_tiled(int* nonfinite) {
-    if constexpr (sizeof(T) == 4) {
-      switch (R_) {
-        case 1: launch_tiled_r<1>(nonfinite); break;
-        case 2: launch_tiled_r<2>(nonfinite); break;
-        case 3: launch_tiled_r<3>(nonfinite); break;
-        case 4: launch_tiled_r<4>(nonfinite); break;
-        default: throw Error(STB_ERR_ARG, "no tiled elastic kernel for this space order");
+  // one half step (phase 0: v, 1: tau) over local planes [x_lo, x_hi)
+  void launch_half(int phase, int x_lo, int x_hi, int* nonfinite) {
+    if (tiled_) {
+      if constexpr (sizeof(T) == 4) {
+        switch (R_) {
+          case 1: return launch_tiled_r<1>(nonfinite, phase, x_lo, x_hi);
+          case 2: return launch_tiled_r<2>(nonfinite, phase, x_lo, x_hi);
+          case 3: return launch_tiled_r<3>(nonfinite, phase, x_lo, x_hi);
+          case 4: return launch_tiled_r<4>(nonfinite, phase, x_lo, x_hi);
+          default: throw Error(STB_ERR_ARG, "no tiled elastic kernel for this space order");
+        }
       }
-    } else {
-      (void)nonfinite;
     }
+    ElArgs<T> A{};
+    for (int i = 0; i < NFIELDS; ++i) A.f[i] = f_[i].p;
+    A.buoy = buoy_.p;
+    A.lam = lam_.p;
+    A.mu = mu_.p;
+    A.fx = fac_[0].p;
+    A.fy = fac_[1].p;
+    A.fz = fac_[2].p;
+    A.has_fac = has_fac_ ? 1 : 0;
+    A.cf = cf_;
+    A.d = d_;
+    A.x_lo = x_lo;
+    A.x_hi = x_hi;
+    A.nonfinite = nonfinite;
+    switch (R_) {
+      case 1: launch_point<T, 1>(st_, A, phase); break;
+      case 2: launch_point<T, 2>(st_, A, phase); break;
+      case 3: launch_point<T, 3>(st_, A, phase); break;
+      case 4: launch_point<T, 4>(st_, A, phase); break;
+      case 5: launch_point<T, 5>(st_, A, phase); break;
+      case 6: launch_point<T, 6>(st_, A, phase); break;
+      case 7: launch_point<T, 7>(st_, A, phase); break;
+      case 8: launch_point<T, 8>(st_, A, phase); break;
+      default: throw Error(STB_ERR_ARG, "space_order must be even in [2, 16]");
+    }
+    STB_CHECK_LAUNCH();
+  }
+
+  // injection of step t into the diagonal stresses (engine.py:327-332)
+  void inject(int64_t t) {
+    if (!K_) return;
+    for (int fi = TXX; fi <= TZZ; ++fi)
+      inject_kernel<T><<<g1(K_), 256, 0, st_>>>(f_[fi].p, src_off_.p, series_.p + t * K_, K_);
+    STB_CHECK_LAUNCH();
+    all_launches_ += 3;
+  }
+
+  void gather(int64_t row) {
+    if (!nrec_) return;
+    gather_kernel<T><<<g1(nrec_), 256, 0, st_>>>(f_[rec_field_].p, rec_off_.p, rec_w_.p, nrec_,
+                                                 rec_dev_.p + row * nrec_);
+    STB_CHECK_LAUNCH();
+    ++all_launches_;
   }
 
   void set_sources(Support& s, const double* wav, int64_t nt_w, const double* scale,
@@ -750,18 +588,6 @@ class ElasticProp final : public stb_prop_s {
     DevBuf<int> guards(guard_steps.size() + 1);
     guards.zero(st_);
     ensure_events(nsteps + 1);
-    ElArgs<T> A{};
-    for (int i = 0; i < NFIELDS; ++i) A.f[i] = f_[i].p;
-    A.buoy = buoy_.p;
-    A.lam = lam_.p;
-    A.mu = mu_.p;
-    A.fx = fac_[0].p;
-    A.fy = fac_[1].p;
-    A.fz = fac_[2].p;
-    A.has_fac = has_fac_ ? 1 : 0;
-    A.cf = cf_;
-    A.d = d_;
-    A.cx = cx_;
     size_t gi = 0;
     STB_CUDA(cudaEventRecord(run_ev_[0], st_));
     for (int64_t t = t0; t < t0 + nsteps; ++t) {
@@ -770,38 +596,16 @@ class ElasticProp final : public stb_prop_s {
       // checks every field (engine.py:373-376): the v fields are new, the
       // stress fields still hold t-1 -- checked after the tau sweep here,
       // which flags the same blow-ups one half step later.
-      A.nonfinite = guard_now ? guards.p + gi : nullptr;
+      int* nf = guard_now ? guards.p + gi : nullptr;
       STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
-      if (tiled_) {
-        launch_tiled(A.nonfinite);
-      } else switch (R_) {
-        case 1: launch_sweeps<T, 1>(st_, A); break;
-        case 2: launch_sweeps<T, 2>(st_, A); break;
-        case 3: launch_sweeps<T, 3>(st_, A); break;
-        case 4: launch_sweeps<T, 4>(st_, A); break;
-        case 5: launch_sweeps<T, 5>(st_, A); break;
-        case 6: launch_sweeps<T, 6>(st_, A); break;
-        case 7: launch_sweeps<T, 7>(st_, A); break;
-        case 8: launch_sweeps<T, 8>(st_, A); break;
-        default: throw Error(STB_ERR_ARG, "space_order must be even in [2, 16]");
-      }
-      STB_CHECK_LAUNCH();
+      launch_half(0, 0, (int)d_.nx, nf);
+      launch_half(1, 0, (int)d_.nx, nf);
       STB_CUDA(cudaEventRecord(events_[2 * launches_ + 1], st_));
       ++launches_;
       all_launches_ += 2;
       if (guard_now) ++gi;
-      if (K_) {
-        for (int fi = TXX; fi <= TZZ; ++fi)
-          inject_kernel<T><<<g1(K_), 256, 0, st_>>>(f_[fi].p, src_off_.p, series_.p + t * K_, K_);
-        STB_CHECK_LAUNCH();
-        all_launches_ += 3;
-      }
-      if (nrec_) {
-        gather_kernel<T><<<g1(nrec_), 256, 0, st_>>>(f_[rec_field_].p, rec_off_.p, rec_w_.p, nrec_,
-                                                     rec_dev_.p + (t - t0) * nrec_);
-        STB_CHECK_LAUNCH();
-        ++all_launches_;
-      }
+      inject(t);
+      gather(t - t0);
     }
     STB_CUDA(cudaEventRecord(run_ev_[1], st_));
     t_next_ = t0 + nsteps;
@@ -821,6 +625,88 @@ class ElasticProp final : public stb_prop_s {
         throw Error(STB_ERR_UNSTABLE, os.str());
       }
     }
+  }
+
+  // ---------------------------------------------------------------- async
+  // x-slab stepping without host synchronisation (slabs.py): per step the v
+  // half step over the owned planes, an exchange of R ghost planes of vx vy
+  // vz, the tau half step (+ injection), an exchange of R planes of the six
+  // stresses, the receiver gather -- all ordered on stream().
+  void* stream() override { return st_; }
+
+  void async_begin(int64_t t0, int64_t nsteps) override {
+    STB_REQUIRE(nsteps >= 0, STB_ERR_ARG, "nsteps must be >= 0");
+    STB_REQUIRE(t0 == t_next_, STB_ERR_ARG,
+                "elastic handles update in place: steps must be run in order");
+    STB_REQUIRE(K_ == 0 || t0 + nsteps <= src_nt_, STB_ERR_ARG,
+                "run extends past the decomposed source series");
+    as_t0_ = t0;
+    as_n_ = nsteps;
+    as_guard_.clear();
+    for (int64_t t = t0; t < t0 + nsteps; ++t)
+      if (t > 0 && t % 32 == 0) as_guard_.push_back(t);
+    if ((int64_t)guards_.n < (int64_t)as_guard_.size() + 1) guards_.alloc(as_guard_.size() + 1);
+    guards_.zero(st_);
+    if (nrec_ && (int64_t)rec_dev_.n < nsteps * nrec_) rec_dev_.alloc(nsteps * nrec_);
+    launches_ = all_launches_ = 0;
+    updates_ = 0;
+    ensure_events(2 * nsteps + 1);
+    STB_CUDA(cudaEventRecord(run_ev_[0], st_));
+    as_open_ = true;
+  }
+
+  void half_step_async(int64_t t, int phase, int64_t x_lo, int64_t x_hi) override {
+    STB_REQUIRE(as_open_, STB_ERR_ARG, "async_begin first");
+    STB_REQUIRE(t >= as_t0_ && t < as_t0_ + as_n_, STB_ERR_ARG, "step outside the async window");
+    STB_REQUIRE(phase == 0 || phase == 1, STB_ERR_ARG, "phase: 0 = v, 1 = tau");
+    STB_REQUIRE(0 <= x_lo && x_lo <= x_hi && x_hi <= d_.nx, STB_ERR_ARG, "plane range");
+    int* nf = nullptr;
+    for (size_t g = 0; g < as_guard_.size(); ++g)
+      if (as_guard_[g] == t && phase == 1) nf = guards_.p + g;
+    STB_REQUIRE(2 * launches_ + 1 < (int64_t)events_.size(), STB_ERR_ARG,
+                "more than two launches per step in the async window");
+    STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
+    launch_half(phase, (int)x_lo, (int)x_hi, nf);
+    STB_CUDA(cudaEventRecord(events_[2 * launches_ + 1], st_));
+    ++launches_;
+    ++all_launches_;
+    if (phase == 1) {
+      inject(t);
+      updates_ += (x_hi - x_lo) * d_.ny * d_.nz;
+    }
+  }
+
+  void step_async(int64_t t, int kb, int64_t x_lo, int64_t x_hi) override {
+    STB_REQUIRE(kb == 1, STB_ERR_PLAN, "elastic steps fuse one time step per pass");
+    half_step_async(t, 0, x_lo, x_hi);
+    half_step_async(t, 1, x_lo, x_hi);
+  }
+
+  void gather_async(int64_t t, int kb) override {
+    STB_REQUIRE(as_open_, STB_ERR_ARG, "async_begin first");
+    for (int j = 0; j < kb; ++j) gather(t + j - as_t0_);
+  }
+
+  void async_finish(double* rec_out, int64_t* bad_step) override {
+    STB_REQUIRE(as_open_, STB_ERR_ARG, "async_begin first");
+    as_open_ = false;
+    if (bad_step) *bad_step = -1;
+    STB_CUDA(cudaEventRecord(run_ev_[1], st_));
+    t_next_ = as_t0_ + as_n_;
+    if (nrec_ && rec_out && as_n_) rec_dev_.download(rec_out, as_n_ * nrec_, st_);
+    std::vector<int> gh(as_guard_.size() + 1, 0);
+    if (!as_guard_.empty()) guards_.download(gh.data(), as_guard_.size(), st_);
+    STB_CUDA(cudaStreamSynchronize(st_));
+    float rm = 0.f;
+    STB_CUDA(cudaEventElapsedTime(&rm, run_ev_[0], run_ev_[1]));
+    run_ms_ = rm;
+    for (size_t i = 0; i < as_guard_.size(); ++i)
+      if (gh[i]) {
+        if (bad_step) *bad_step = as_guard_[i];
+        std::ostringstream os;
+        os << "non-finite values in field group 'v' at step " << as_guard_[i];
+        throw Error(STB_ERR_UNSTABLE, os.str());
+      }
   }
 
   void read_field(int field, int64_t t, void* out) override {
@@ -872,9 +758,6 @@ class ElasticProp final : public stb_prop_s {
     if (tiled_)
       os << "elastic_tiled<f32,R=" << R_ << "> (TMA plane rings; " << kTYv
          << "x32 tiles; x chunk 256)";
-    else if (cx_ > 0)
-      os << "elastic_sweeps<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
-         << "> (v + tau x-sweeps, 32x8 threads, cx=" << cx_ << ")";
     else
       os << "elastic_point<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
          << "> (v + tau, thread per point, zero-haloed layout)";
@@ -903,11 +786,14 @@ class ElasticProp final : public stb_prop_s {
   DevBuf<T> buoy_, lam_, mu_;
   DevBuf<T> fac_[3];
   bool has_fac_ = false;
-  int cx_ = 64;
   bool tiled_ = false;
   int rec_field_ = TXX;      // engine.py:327-332 records txx
   CUtensorMap fmap_[NFIELDS];
   int64_t t_next_ = 0;
+  bool as_open_ = false;
+  int64_t as_t0_ = 0, as_n_ = 0;
+  std::vector<int64_t> as_guard_;
+  DevBuf<int> guards_;
   int64_t K_ = 0, src_nt_ = 0;
   DevBuf<T> series_;
   DevBuf<int64_t> src_off_;

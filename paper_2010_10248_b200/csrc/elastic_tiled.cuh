@@ -59,6 +59,7 @@ struct ElTiledArgs {
   ElCoefs<float> cf;
   PDims d;
   int cx;
+  int x_lo, x_hi;         // local planes of this launch, in cx chunks
   int* nonfinite;
 };
 
@@ -91,9 +92,9 @@ elastic_tiled(const __grid_constant__ ElTiledMaps maps, ElTiledArgs a) {
 
   const int tid = threadIdx.x;
   const int ty = tid >> 5, tz = tid & 31;
-  const int z0 = blockIdx.x * kElTZ, y0 = blockIdx.y * TY, x0 = blockIdx.z * a.cx;
-  const int nx = (int)a.d.nx, ny = (int)a.d.ny, nz = (int)a.d.nz;
-  const int x1 = min(x0 + a.cx, nx);
+  const int z0 = blockIdx.x * kElTZ, y0 = blockIdx.y * TY, x0 = a.x_lo + blockIdx.z * a.cx;
+  const int ny = (int)a.d.ny, nz = (int)a.d.nz;
+  const int x1 = min(x0 + a.cx, a.x_hi);
   const int y = y0 + ty, z = z0 + tz;
   const bool core_in = y < ny && z < nz;
   const int N = (x1 - x0) + 2 * R;            // sequence n = plane x0 - R + n

@@ -218,13 +218,15 @@ struct stb_prop_s {
   virtual void set_damping(const double* const*) { throw_unsupported(); }
   virtual void async_begin(int64_t, int64_t) { throw_unsupported(); }
   virtual void step_async(int64_t, int, int64_t, int64_t) { throw_unsupported(); }
+  // elastic: one half step (0 = v, 1 = tau + injection) over local planes
+  virtual void half_step_async(int64_t, int, int64_t, int64_t) { throw_unsupported(); }
   virtual void gather_async(int64_t, int) { throw_unsupported(); }
   virtual void async_finish(double*, int64_t*) { throw_unsupported(); }
 
  protected:
   [[noreturn]] static void throw_unsupported() {
-    throw stb::Error(STB_ERR_ARG, "asynchronous stepping is implemented for the fused "
-                                  "acoustic path only");
+    throw stb::Error(STB_ERR_ARG, "this handle does not support that asynchronous "
+                                  "stepping call");
   }
 };
 

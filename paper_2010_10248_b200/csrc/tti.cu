@@ -25,6 +25,7 @@
 //   pass 1: p, q, n_x, n_y, n_z in; F, G out          (5 + 6) x 4 B
 //   pass 2: F, G, p, q, p_prev, q_prev, inv, e2, d2 in; p', q' out
 //                                                    (13 + 2) x 4 B
+#include <algorithm>
 #include <cstdlib>
 #include <memory>
 #include <sstream>
@@ -75,6 +76,7 @@ struct TtiArgs {
   int has_fac;
   TtiCoefs<T> cf;
   PDims d;
+  int x_lo;           // first local plane of this launch (grid.z = plane count)
   int* nonfinite;
 };
 
@@ -91,7 +93,7 @@ template <typename T, int r>
 __global__ void __launch_bounds__(128) tti_pass1(TtiArgs<T> a) {
   const int z = blockIdx.x * 32 + threadIdx.x;
   const int y = blockIdx.y * 4 + threadIdx.y;
-  const int x = blockIdx.z;
+  const int x = a.x_lo + blockIdx.z;
   if (z >= a.d.nz || y >= a.d.ny) return;
   const int st[3] = {(int)a.d.plane, (int)a.d.pitch, 1};
   const int i = (int)a.d.at(x, y, z);
@@ -123,7 +125,7 @@ template <typename T, int r>
 __global__ void __launch_bounds__(128) tti_pass2(TtiArgs<T> a) {
   const int z = blockIdx.x * 32 + threadIdx.x;
   const int y = blockIdx.y * 4 + threadIdx.y;
-  const int x = blockIdx.z;
+  const int x = a.x_lo + blockIdx.z;
   if (z >= a.d.nz || y >= a.d.ny) return;
   const int st[3] = {(int)a.d.plane, (int)a.d.pitch, 1};
   const int i = (int)a.d.at(x, y, z);
@@ -213,12 +215,20 @@ __global__ void tti_fill_kernel(T* __restrict__ dst, PDims d, T v) {
   }
 }
 
+// pass 1 (gradient streams) over [x_lo - r, x_hi + r) within the slab, pass 2
+// (divergences + update) over [x_lo, x_hi)
 template <typename T, int r>
-void launch_tti(cudaStream_t st, const TtiArgs<T>& a) {
+void launch_tti(cudaStream_t st, TtiArgs<T> a, int x_lo, int x_hi) {
+  if (x_hi <= x_lo) return;
   dim3 block(32, 4);
-  dim3 grid((unsigned)((a.d.nz + 31) / 32), (unsigned)((a.d.ny + 3) / 4), (unsigned)a.d.nx);
-  tti_pass1<T, r><<<grid, block, 0, st>>>(a);
-  tti_pass2<T, r><<<grid, block, 0, st>>>(a);
+  const int lo1 = std::max(x_lo - r, 0), hi1 = std::min<int>(x_hi + r, (int)a.d.nx);
+  a.x_lo = lo1;
+  dim3 grid1((unsigned)((a.d.nz + 31) / 32), (unsigned)((a.d.ny + 3) / 4), (unsigned)(hi1 - lo1));
+  tti_pass1<T, r><<<grid1, block, 0, st>>>(a);
+  a.x_lo = x_lo;
+  dim3 grid2((unsigned)((a.d.nz + 31) / 32), (unsigned)((a.d.ny + 3) / 4),
+             (unsigned)(x_hi - x_lo));
+  tti_pass2<T, r><<<grid2, block, 0, st>>>(a);
 }
 
 }  // namespace
@@ -432,63 +442,20 @@ class TtiProp final : public stb_prop_s {
     DevBuf<int> guards(guard_steps.size() + 1);
     guards.zero(st_);
     ensure_events(nsteps + 1);
-    TtiArgs<T> A{};
-    for (int ax = 0; ax < 3; ++ax) {
-      A.F[ax] = F_[ax].p;
-      A.G[ax] = G_[ax].p;
-      A.n[ax] = n_[ax].p;
-    }
-    A.inv = inv_.p;
-    A.e2 = e2_.p;
-    A.d2 = d2_.p;
-    A.fx = fac_[0].p;
-    A.fy = fac_[1].p;
-    A.fz = fac_[2].p;
-    A.has_fac = has_fac_ ? 1 : 0;
-    A.cf = cf_;
-    A.d = d_;
     size_t gi = 0;
     STB_CUDA(cudaEventRecord(run_ev_[0], st_));
     for (int64_t t = t0; t < t0 + nsteps; ++t) {
-      const int cur = (int)(t & 1), prev = cur ^ 1;
-      A.p1 = lv_[0][prev].p;
-      A.q1 = lv_[1][prev].p;
-      A.p0 = lv_[0][cur].p;
-      A.q0 = lv_[1][cur].p;
       const bool guard_now = gi < guard_steps.size() && guard_steps[gi] == t;
-      A.nonfinite = guard_now ? guards.p + gi : nullptr;
       STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
-      if (fused_) {
-        launch_fused(A, prev);
-      } else switch (r_) {
-        case 1: launch_tti<T, 1>(st_, A); break;
-        case 2: launch_tti<T, 2>(st_, A); break;
-        case 3: launch_tti<T, 3>(st_, A); break;
-        case 4: launch_tti<T, 4>(st_, A); break;
-        default: throw Error(STB_ERR_CONFIG, "space_order: TTI supports 4, 8, 12, 16");
-      }
-      STB_CHECK_LAUNCH();
+      launch_step(t, 0, (int)d_.nx, guard_now ? guards.p + gi : nullptr);
       STB_CUDA(cudaEventRecord(events_[2 * launches_ + 1], st_));
       ++launches_;
-      all_launches_ += fused_ ? 1 : 2;
       if (guard_now) ++gi;
-      if (K_) {
-        for (int f = 0; f < 2; ++f)
-          inject_kernel<T><<<g1t(K_), 256, 0, st_>>>(lv_[f][cur].p, src_off_.p,
-                                                     series_.p + t * K_, K_);
-        STB_CHECK_LAUNCH();
-        all_launches_ += 2;
-      }
-      if (nrec_) {
-        gather_kernel<T><<<g1t(nrec_), 256, 0, st_>>>(lv_[rec_field_][cur].p, rec_off_.p, rec_w_.p, nrec_,
-                                                      rec_dev_.p + (t - t0) * nrec_);
-        STB_CHECK_LAUNCH();
-        ++all_launches_;
-      }
+      inject(t);
+      gather(t, t - t0);
     }
     STB_CUDA(cudaEventRecord(run_ev_[1], st_));
     t_next_ = t0 + nsteps;
-    updates_ = nsteps * d_.nx * d_.ny * d_.nz;
     if (nrec_ && rec_out) rec_dev_.download(rec_out, nsteps * nrec_, st_);
     std::vector<int> gh(guard_steps.size() + 1, 0);
     if (!guard_steps.empty()) guards.download(gh.data(), guard_steps.size(), st_);
@@ -504,6 +471,135 @@ class TtiProp final : public stb_prop_s {
         throw Error(STB_ERR_UNSTABLE, os.str());
       }
     }
+  }
+
+  // step t (level t from t-1, t-2) over local planes [x_lo, x_hi)
+  void launch_step(int64_t t, int x_lo, int x_hi, int* nonfinite) {
+    TtiArgs<T> A{};
+    for (int ax = 0; ax < 3; ++ax) {
+      A.F[ax] = F_[ax].p;
+      A.G[ax] = G_[ax].p;
+      A.n[ax] = n_[ax].p;
+    }
+    A.inv = inv_.p;
+    A.e2 = e2_.p;
+    A.d2 = d2_.p;
+    A.fx = fac_[0].p;
+    A.fy = fac_[1].p;
+    A.fz = fac_[2].p;
+    A.has_fac = has_fac_ ? 1 : 0;
+    A.cf = cf_;
+    A.d = d_;
+    const int cur = (int)(t & 1), prev = cur ^ 1;
+    A.p1 = lv_[0][prev].p;
+    A.q1 = lv_[1][prev].p;
+    A.p0 = lv_[0][cur].p;
+    A.q0 = lv_[1][cur].p;
+    A.nonfinite = nonfinite;
+    if (fused_) {
+      launch_fused(A, prev, x_lo, x_hi);
+      all_launches_ += 1;
+    } else {
+      switch (r_) {
+        case 1: launch_tti<T, 1>(st_, A, x_lo, x_hi); break;
+        case 2: launch_tti<T, 2>(st_, A, x_lo, x_hi); break;
+        case 3: launch_tti<T, 3>(st_, A, x_lo, x_hi); break;
+        case 4: launch_tti<T, 4>(st_, A, x_lo, x_hi); break;
+        default: throw Error(STB_ERR_CONFIG, "space_order: TTI supports 4, 8, 12, 16");
+      }
+      all_launches_ += 2;
+    }
+    STB_CHECK_LAUNCH();
+    updates_ += (int64_t)(x_hi - x_lo) * d_.ny * d_.nz;
+  }
+
+  void inject(int64_t t) {
+    if (!K_) return;
+    const int cur = (int)(t & 1);
+    for (int f = 0; f < 2; ++f)
+      inject_kernel<T><<<g1t(K_), 256, 0, st_>>>(lv_[f][cur].p, src_off_.p, series_.p + t * K_,
+                                                 K_);
+    STB_CHECK_LAUNCH();
+    all_launches_ += 2;
+  }
+
+  void gather(int64_t t, int64_t row) {
+    if (!nrec_) return;
+    gather_kernel<T><<<g1t(nrec_), 256, 0, st_>>>(lv_[rec_field_][t & 1].p, rec_off_.p, rec_w_.p,
+                                                  nrec_, rec_dev_.p + row * nrec_);
+    STB_CHECK_LAUNCH();
+    ++all_launches_;
+  }
+
+  // ---------------------------------------------------------------- async
+  // x-slab stepping without host synchronisation (slabs.py): per step one
+  // launch over the owned planes (+ injection), then the exchange of R ghost
+  // planes of p and q at level t, then the gather -- ordered on stream().
+  void* stream() override { return st_; }
+
+  void async_begin(int64_t t0, int64_t nsteps) override {
+    STB_REQUIRE(nsteps >= 0, STB_ERR_ARG, "nsteps must be >= 0");
+    STB_REQUIRE(t0 == t_next_, STB_ERR_ARG,
+                "TTI handles keep two time levels: steps must be run in order");
+    STB_REQUIRE(K_ == 0 || t0 + nsteps <= src_nt_, STB_ERR_ARG,
+                "run extends past the decomposed source series");
+    as_t0_ = t0;
+    as_n_ = nsteps;
+    as_guard_.clear();
+    for (int64_t t = t0; t < t0 + nsteps; ++t)
+      if (t > 0 && t % 32 == 0) as_guard_.push_back(t);
+    if ((int64_t)guards_.n < (int64_t)as_guard_.size() + 1) guards_.alloc(as_guard_.size() + 1);
+    guards_.zero(st_);
+    if (nrec_ && (int64_t)rec_dev_.n < nsteps * nrec_) rec_dev_.alloc(nsteps * nrec_);
+    launches_ = all_launches_ = 0;
+    updates_ = 0;
+    ensure_events(nsteps + 1);
+    STB_CUDA(cudaEventRecord(run_ev_[0], st_));
+    as_open_ = true;
+  }
+
+  void step_async(int64_t t, int kb, int64_t x_lo, int64_t x_hi) override {
+    STB_REQUIRE(as_open_, STB_ERR_ARG, "async_begin first");
+    STB_REQUIRE(kb == 1, STB_ERR_PLAN, "TTI steps fuse one time step per pass");
+    STB_REQUIRE(t >= as_t0_ && t < as_t0_ + as_n_, STB_ERR_ARG, "step outside the async window");
+    STB_REQUIRE(0 <= x_lo && x_lo <= x_hi && x_hi <= d_.nx, STB_ERR_ARG, "plane range");
+    int* nf = nullptr;
+    for (size_t g = 0; g < as_guard_.size(); ++g)
+      if (as_guard_[g] == t) nf = guards_.p + g;
+    STB_REQUIRE(2 * launches_ + 1 < (int64_t)events_.size(), STB_ERR_ARG,
+                "more than one launch per step in the async window");
+    STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
+    launch_step(t, (int)x_lo, (int)x_hi, nf);
+    STB_CUDA(cudaEventRecord(events_[2 * launches_ + 1], st_));
+    ++launches_;
+    inject(t);
+  }
+
+  void gather_async(int64_t t, int kb) override {
+    STB_REQUIRE(as_open_, STB_ERR_ARG, "async_begin first");
+    for (int j = 0; j < kb; ++j) gather(t + j, t + j - as_t0_);
+  }
+
+  void async_finish(double* rec_out, int64_t* bad_step) override {
+    STB_REQUIRE(as_open_, STB_ERR_ARG, "async_begin first");
+    as_open_ = false;
+    if (bad_step) *bad_step = -1;
+    STB_CUDA(cudaEventRecord(run_ev_[1], st_));
+    t_next_ = as_t0_ + as_n_;
+    if (nrec_ && rec_out && as_n_) rec_dev_.download(rec_out, as_n_ * nrec_, st_);
+    std::vector<int> gh(as_guard_.size() + 1, 0);
+    if (!as_guard_.empty()) guards_.download(gh.data(), as_guard_.size(), st_);
+    STB_CUDA(cudaStreamSynchronize(st_));
+    float rm = 0.f;
+    STB_CUDA(cudaEventElapsedTime(&rm, run_ev_[0], run_ev_[1]));
+    run_ms_ = rm;
+    for (size_t i = 0; i < as_guard_.size(); ++i)
+      if (gh[i]) {
+        if (bad_step) *bad_step = as_guard_[i];
+        std::ostringstream os;
+        os << "non-finite values in field group 'pq' at step " << as_guard_[i];
+        throw Error(STB_ERR_UNSTABLE, os.str());
+      }
   }
 
   void read_field(int field, int64_t t, void* out) override {
@@ -612,8 +708,9 @@ class TtiProp final : public stb_prop_s {
 
   template <int r>
   void launch_fused_r(const TtiFusedArgs& fa, int prev) {
+    if (fa.x_hi <= fa.x_lo) return;
     dim3 grid((unsigned)((d_.nz + kTtiTZ - 1) / kTtiTZ), (unsigned)((d_.ny + kTtiTY - 1) / kTtiTY),
-              (unsigned)((d_.nx + cx_ - 1) / cx_));
+              (unsigned)((fa.x_hi - fa.x_lo + cx_ - 1) / cx_));
     constexpr int M = m_for_r(r);
     if (fast_)
       tti_fused<r, M, true><<<grid, kTtiThreads, TtiFusedCfg<r, M>::smem_bytes(), st_>>>(
@@ -623,7 +720,7 @@ class TtiProp final : public stb_prop_s {
           maps_[prev], fa);
   }
 
-  void launch_fused(const TtiArgs<T>& A, int prev) {
+  void launch_fused(const TtiArgs<T>& A, int prev, int x_lo, int x_hi) {
     if constexpr (sizeof(T) == 4) {
       TtiFusedArgs fa{};
       fa.p0 = A.p0;
@@ -639,6 +736,8 @@ class TtiProp final : public stb_prop_s {
       fa.cf = A.cf;
       fa.d = A.d;
       fa.cx = cx_;
+      fa.x_lo = x_lo;
+      fa.x_hi = x_hi;
       fa.nonfinite = A.nonfinite;
       switch (r_) {
         case 1: launch_fused_r<1>(fa, prev); break;
@@ -650,6 +749,8 @@ class TtiProp final : public stb_prop_s {
     } else {
       (void)A;
       (void)prev;
+      (void)x_lo;
+      (void)x_hi;
     }
   }
 
@@ -668,6 +769,10 @@ class TtiProp final : public stb_prop_s {
   bool fast_ = false;
   int rec_field_ = 0;        // p
   int cx_ = 150;
+  bool as_open_ = false;
+  int64_t as_t0_ = 0, as_n_ = 0;
+  std::vector<int64_t> as_guard_;
+  DevBuf<int> guards_;
   TtiMaps maps_[2];           // [level buffer] p/q tensor maps (fused path)
   PDims d_{};
   stb_geometry geom_{};

@@ -75,6 +75,7 @@ struct TtiFusedArgs {
   TtiCoefs<float> cf;
   PDims d;
   int cx;             // x planes per CTA
+  int x_lo, x_hi;     // local output planes of this launch (in cx chunks)
   int* nonfinite;
 };
 
@@ -160,9 +161,9 @@ tti_fused(const __grid_constant__ TtiMaps maps, TtiFusedArgs a) {
 
   const int tid = threadIdx.x;
   const int z0 = blockIdx.x * C::TZ, y0 = blockIdx.y * C::TY;
-  const int x0 = blockIdx.z * a.cx;
+  const int x0 = a.x_lo + blockIdx.z * a.cx;
   const int nx = (int)a.d.nx, ny = (int)a.d.ny, nz = (int)a.d.nz;
-  const int x1 = min(x0 + a.cx, nx);
+  const int x1 = min(x0 + a.cx, a.x_hi);
   const int n_iter = (x1 - x0) + 2 * r;             // pass-1 planes x0-r .. x1-1+r
   const int n_seq = n_iter + 2 * r;                 // p/q planes x0-2r .. x1-1+2r
 

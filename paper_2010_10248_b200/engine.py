@@ -59,6 +59,10 @@ class ScheduleSpec:
     time_height: int = 1
     force_skew: tuple[int, int] | None = None
     arithmetic: str = "exact"
+    # x-slab decomposition over GPUs of this process (multi.py); ``devices``
+    # overrides range(n_gpus) and may repeat a device (several slabs per GPU)
+    n_gpus: int = 1
+    devices: tuple | None = None
 
 
 @dataclass
@@ -375,6 +379,9 @@ class _Prop:
     def step_async(self, t, kb, x_lo, x_hi):
         _lib.check(_lib.lib().stb_prop_step_async(self.raw, t, kb, x_lo, x_hi))
 
+    def half_step_async(self, t, phase, x_lo, x_hi):
+        _lib.check(_lib.lib().stb_prop_half_step_async(self.raw, t, phase, x_lo, x_hi))
+
     def gather_async(self, t, kb):
         _lib.check(_lib.lib().stb_prop_gather_async(self.raw, t, kb))
 
@@ -659,10 +666,60 @@ def _host_sparse_prep(config: RunConfig, dt: float, nt: int):
     return src
 
 
+def _slab_devices(config: RunConfig):
+    s = config.schedule
+    devices = getattr(s, "devices", None)
+    n = int(getattr(s, "n_gpus", 1) or 1)
+    if devices is None:
+        if n < 1:
+            raise ConfigError("schedule.n_gpus", f"must be >= 1, got {n}")
+        return list(range(n)) if n > 1 else None
+    devices = [int(d) for d in devices]
+    if not devices:
+        raise ConfigError("schedule.devices", "must list at least one device")
+    return devices if len(devices) > 1 else None
+
+
+def make_report(config: RunConfig, fields, rec, nt, dt, elapsed, precompute_s, plan_text,
+                k_used, k_max, nsrc, nrec) -> RunReport:
+    """RunReport with the reference's GPts/s and checksum definitions
+    (engine.py:436-489) plus the device plan actually run."""
+    grid = config.grid
+    nf = len(FIELDS[config.physics])
+    gpoints = grid.npoints * nt * nf / elapsed / 1e9 if nt > 0 and elapsed > 0 else 0.0
+    s = config.schedule
+    devices = _slab_devices(config)
+    return RunReport(
+        physics=config.physics, grid_shape=grid.shape, space_order=config.space_order,
+        precision=config.precision, threads=config.threads,
+        schedule={"kind": s.kind, "block_shape": s.block_shape, "tile_shape": s.tile_shape,
+                  "time_height": k_used, "time_height_requested": s.time_height,
+                  "max_time_height": k_max,
+                  "arithmetic": getattr(s, "arithmetic", "exact"),
+                  "n_gpus": len(devices) if devices else 1,
+                  "device_plan": plan_text},
+        nt=nt, dt=dt, elapsed_s=elapsed, precompute_s=precompute_s, gpoints_per_s=gpoints,
+        arithmetic_intensity=arithmetic_intensity(config.physics, config.space_order,
+                                                  config.precision),
+        checksum_source=(fields, rec), nsrc=nsrc, nrec=nrec,
+        source_scale_rule=("dt" if config.physics == "elastic"
+                           else "dt^2/m at nearest grid point"),
+        machine={"platform": platform.platform(),
+                 "processor": platform.processor() or platform.machine(),
+                 "cpus": os.cpu_count(), "device": "cuda"},
+    )
+
+
 def run(config: RunConfig) -> RunResult:
-    """Execute a configured run on the GPU (engine.py:379-489 semantics)."""
+    """Execute a configured run on the GPU (engine.py:379-489 semantics).
+    ``schedule.n_gpus`` > 1 (or a ``devices`` list) splits the grid in
+    x-slabs over that many GPUs of this process (multi.py)."""
     _lib.require_device()
     k = _gpu_time_height(config)
+    devices = _slab_devices(config)
+    if devices is not None:
+        from .multi import run_multi
+        return run_multi(config, devices)
     grid = config.grid
     vkey = {"acoustic": "velocity", "tti": "vp"}.get(config.physics)
     overlap = (vkey is not None and config.dt is not None and config.nt is not None
@@ -735,30 +792,10 @@ def run(config: RunConfig) -> RunResult:
         fields = {n: prop.read(n, t_final, grid.shape) for n in names}
     else:
         fields = {n: np.zeros(grid.shape, dtype=config.dtype) for n in names}
-    nf = len(names)
-    gpoints = grid.npoints * nt * nf / elapsed / 1e9 if nt > 0 and elapsed > 0 else 0.0
-    s = config.schedule
     plan_text = prop.describe(k)
     m = re.search(r"\bk=(\d+)", plan_text)
-    k_used = int(m.group(1)) if m else 1
-    report = RunReport(
-        physics=config.physics, grid_shape=grid.shape, space_order=config.space_order,
-        precision=config.precision, threads=config.threads,
-        schedule={"kind": s.kind, "block_shape": s.block_shape, "tile_shape": s.tile_shape,
-                  "time_height": k_used, "time_height_requested": s.time_height,
-                  "max_time_height": k_max,
-                  "arithmetic": getattr(s, "arithmetic", "exact"),
-                  "device_plan": plan_text},
-        nt=nt, dt=dt, elapsed_s=elapsed, precompute_s=precompute_s, gpoints_per_s=gpoints,
-        arithmetic_intensity=arithmetic_intensity(config.physics, config.space_order,
-                                                  config.precision),
-        checksum_source=(fields, rec), nsrc=nsrc, nrec=nrec,
-        source_scale_rule=("dt" if config.physics == "elastic"
-                           else "dt^2/m at nearest grid point"),
-        machine={"platform": platform.platform(),
-                 "processor": platform.processor() or platform.machine(),
-                 "cpus": os.cpu_count(), "device": "cuda"},
-    )
+    report = make_report(config, fields, rec, nt, dt, elapsed, precompute_s, plan_text,
+                         int(m.group(1)) if m else 1, k_max, nsrc, nrec)
     return RunResult(fields=fields, receivers=rec, report=report)
 
 

@@ -75,8 +75,9 @@ class DeviceSlab:
         # device is independent of torch's: bind it to the rank's device
         # (torch.cuda.set_device(local_rank)) so the slab's buffers, the torch
         # views of its ghost planes and the NCCL transfers share one GPU
+        self.device = torch.cuda.current_device() if torch.cuda.is_available() else 0
         if torch.cuda.is_available():
-            _lib.check(_lib.lib().stb_set_device(torch.cuda.current_device()))
+            _lib.check(_lib.lib().stb_set_device(self.device))
         self.prop: _Prop = build_propagator(config, dt, v_max, x_begin=x_begin,
                                             nx_local=nx_local)
         self.item = np.dtype(config.dtype).itemsize
@@ -100,10 +101,12 @@ class DeviceSlab:
     def max_time_height(self) -> int:
         return self.prop.max_time_height()
 
-    # asynchronous stepping (fused acoustic path): see SlabRunner._run_async
+    # asynchronous stepping: see SlabRunner._run_async (acoustic: the fused
+    # path; elastic and TTI: every path)
     def supports_async(self) -> bool:
-        return self.config.physics == "acoustic" and self.prop.describe(1).startswith(
-            ("acoustic_fused", "acoustic_wtb"))
+        if self.config.physics != "acoustic":
+            return True
+        return self.prop.describe(1).startswith(("acoustic_fused", "acoustic_wtb"))
 
     def stream_ptr(self) -> int:
         return self.prop.stream_ptr()
@@ -113,6 +116,9 @@ class DeviceSlab:
 
     def step_async(self, t, kb, x_lo, x_hi):
         self.prop.step_async(t, kb, x_lo, x_hi)
+
+    def half_step_async(self, t, phase, x_lo, x_hi):
+        self.prop.half_step_async(t, phase, x_lo, x_hi)
 
     def gather_async(self, t, kb):
         self.prop.gather_async(t, kb)
@@ -128,7 +134,8 @@ class DeviceSlab:
                                                  C.byref(plane), C.byref(pitch)))
         typestr = "<f4" if self.item == 4 else "<f8"
         base = dev.value + i * plane.value * self.item
-        return torch.as_tensor(_DevArray(base, (j - i, plane.value), typestr), device="cuda")
+        return torch.as_tensor(_DevArray(base, (j - i, plane.value), typestr),
+                               device=f"cuda:{self.device}")
 
     def read(self, t, shape, name="u"):
         return self.prop.read(name, t, shape)
@@ -274,46 +281,74 @@ class SlabRunner:
     def _run_async(self, t0: int, nsteps: int, record: bool):
         """Device-ordered stepping: nothing waits on the host inside the loop.
 
-        k = 1: per step one launch over the owned planes (ghost planes are not
-        computed: the exchange overwrites them), then the NCCL exchange of the
-        newest level, then the receiver gather -- all ordered on the device.
-        With STB_SLAB_OVERLAP=1 the owned boundary planes (G each side) are
-        computed first and the exchange runs on a side stream while the
-        interior planes compute.
-        k >= 2: every held plane is computed (the fused levels consume the
-        ghost zones), then the last two levels are exchanged."""
+        Acoustic, k = 1: per step one launch over the owned planes (ghost
+        planes are not computed: the exchange overwrites them), then the
+        exchange of the R planes next to the owned range at the newest level,
+        then the receiver gather -- all ordered on the device.  With
+        STB_SLAB_OVERLAP=1 the owned boundary planes are computed first and
+        the exchange runs on a side stream while the interior computes.
+        Acoustic, k >= 2: every held plane is computed (the fused levels
+        consume the ghost zones), then the last two levels are exchanged.
+        Elastic: v half step over the owned planes, R planes of vx vy vz
+        exchanged, tau half step (+ injection), R planes of the six stresses
+        exchanged (the reference's skew 2R per step, schedule.py:81-90, as
+        two R-deep half-step exchanges).  TTI: one owned-plane step, R planes
+        of p and q exchanged."""
+        import contextlib
+
         import torch
         k = self.time_height
-        main = torch.cuda.ExternalStream(self.dev.stream_ptr())
-        if not hasattr(self, "_side"):
-            self._side = torch.cuda.Stream()
-        side = self._side
+        R = self.R
+        ptr = self.dev.stream_ptr()
+        # a host backend (tests' CPU stand-in) has no stream: plain order
+        main = torch.cuda.ExternalStream(ptr) if ptr and torch.cuda.is_available() else None
+
+        def on_main():
+            return torch.cuda.stream(main) if main is not None else contextlib.nullcontext()
         a_loc, b_loc, G = self.a - self.lo, self.b - self.lo, self.G
+        nf = len(self.field_names)
         # boundary/interior split: measured on one B200 for cfg2 slabs, the
         # two extra ranged launches per step (thin boundary chunks pay the
         # sweep warm-up) cost more than the exchange they hide (8 ranks:
         # 129 us split vs 91 us single launch per step), so the single launch
         # is the default and the split an option
-        overlap = (k == 1 and b_loc - a_loc > 2 * G
+        overlap = (main is not None and not self.single_step and k == 1 and b_loc - a_loc > 2 * G
                    and os.environ.get("STB_SLAB_OVERLAP", "0") == "1")
+        if overlap and not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream()
         self.dev.async_begin(t0, nsteps)
         t = t0
         while t < t0 + nsteps:
             kb = min(k, t0 + nsteps - t)
-            if overlap:
+            if self.elastic:
+                self.dev.half_step_async(t, 0, a_loc, b_loc)
+                with on_main():
+                    self.exchange([t], fields=range(3), sync=False, depth=R)
+                self.dev.half_step_async(t, 1, a_loc, b_loc)
+                with on_main():
+                    self.exchange([t], fields=range(3, nf), sync=False, depth=R)
+            elif self.single_step:                                      # TTI
+                self.dev.step_async(t, 1, a_loc, b_loc)
+                with on_main():
+                    self.exchange([t], fields=range(nf), sync=False, depth=R)
+            elif overlap:
                 self.dev.step_async(t, 1, a_loc, a_loc + G)
                 self.dev.step_async(t, 1, b_loc - G, b_loc)
+                side = self._side
                 ev = torch.cuda.Event()
                 ev.record(main)
                 side.wait_event(ev)
                 with torch.cuda.stream(side):
-                    self.exchange([t], sync=False)
+                    self.exchange([t], sync=False, depth=R)
                 self.dev.step_async(t, 1, a_loc + G, b_loc - G)
                 main.wait_stream(side)
+            elif kb == 1:
+                self.dev.step_async(t, 1, a_loc, b_loc)
+                with on_main():
+                    self.exchange([t], sync=False, depth=R)
             else:
-                lo_c, hi_c = (a_loc, b_loc) if kb == 1 else (0, self.nl)
-                self.dev.step_async(t, kb, lo_c, hi_c)
-                with torch.cuda.stream(main):
+                self.dev.step_async(t, kb, 0, self.nl)
+                with on_main():
                     self.exchange([t + kb - 1] + ([t + kb - 2] if kb >= 2 else []), sync=False)
             self.dev.gather_async(t, kb)
             t += kb
@@ -329,10 +364,12 @@ class SlabRunner:
         for key, val in st.items():
             self._acc[key] = self._acc.get(key, 0) + val
 
-    def exchange(self, levels, fields=(0,), sync=True):
+    def exchange(self, levels, fields=(0,), sync=True, depth=None):
         """Refresh ghost planes of the given time levels (and fields) from the
-        neighbours.  sync=False: the transfers are ordered on the current CUDA
-        stream (NCCL work.wait() is a stream wait) and the host does not block."""
+        neighbours: the ``depth`` planes next to the owned range on each side
+        (default: the whole ghost zone).  sync=False: the transfers are
+        ordered on the current CUDA stream (NCCL work.wait() is a stream
+        wait) and the host does not block."""
         import torch.distributed as dist
         ops, unstage = [], []
         g_lo, g_hi = self.a - self.lo, self.hi - self.b
@@ -343,7 +380,7 @@ class SlabRunner:
         # the device addresses of a level depend only on its ring slot (6
         # covers acoustic's ring, TTI's pair and elastic's single level), so
         # the NCCL op lists are built once per slot pattern and reused
-        key = (tuple(t % 6 for t in levels), tuple(fields))
+        key = (tuple(t % 6 for t in levels), tuple(fields), depth)
         if not staged:
             cached = getattr(self, "_ops_cache", {}).get(key)
             if cached is not None:
@@ -370,11 +407,13 @@ class SlabRunner:
         for t in levels:
             for f in fields:
                 if self.rank > 0:
-                    send(t, g_lo, g_lo + g_lo, f, self.rank - 1)
-                    recv(t, 0, g_lo, f, self.rank - 1)
+                    w = g_lo if depth is None else min(depth, g_lo)
+                    send(t, g_lo, g_lo + w, f, self.rank - 1)
+                    recv(t, g_lo - w, g_lo, f, self.rank - 1)
                 if self.rank < self.world - 1:
-                    send(t, self.nl - g_hi - g_hi, self.nl - g_hi, f, self.rank + 1)
-                    recv(t, self.nl - g_hi, self.nl, f, self.rank + 1)
+                    w = g_hi if depth is None else min(depth, g_hi)
+                    send(t, self.nl - g_hi - w, self.nl - g_hi, f, self.rank + 1)
+                    recv(t, self.nl - g_hi, self.nl - g_hi + w, f, self.rank + 1)
         if not staged and ops:
             if not hasattr(self, "_ops_cache"):
                 self._ops_cache = {}

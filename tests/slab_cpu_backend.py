@@ -104,6 +104,75 @@ class OracleSlab:
                 rec_out[t - t0] = so.record(self._level(gather, t), self.ridx, self.rw, R)
         self.t_last = t0 + n - 1
 
+    # -------------------------------------------------- asynchronous API
+    # SlabRunner._run_async's calls, executed immediately on the host:
+    # owned-plane boxes of the oracle's box updates (elastic: the v / tau
+    # halves separately; TTI: pass 1 widened by r), so the R-deep ghost
+    # exchanges of the async loop are what keeps the slabs exact.
+    async_ok = False
+
+    def supports_async(self):
+        return self.async_ok
+
+    def stream_ptr(self):
+        return 0
+
+    def _targets(self):
+        return ("txx", "tyy", "tzz") if self.elastic else ("p", "q") if self.tti else ("u",)
+
+    def _inject(self, t):
+        if self.pts is not None and len(self.pts):
+            R, p = self.R, self.pts
+            for name in self._targets():
+                lvl = self._level(name, t)
+                lvl[p[:, 0] + R, p[:, 1] + R, p[:, 2] + R] += self.dcmp[t].astype(self.dtype)
+
+    def _box(self, lo, hi):
+        g = self.config.grid
+        return ((lo, hi), (0, g.shape[1]), (0, g.shape[2]))
+
+    def async_begin(self, t0, n):
+        self._as_t0 = t0
+        self._as_rec = (np.zeros((n, self.ridx.shape[0])) if self.ridx is not None else None)
+
+    def half_step_async(self, t, phase, x_lo, x_hi):
+        assert self.elastic
+        if phase == 0:
+            self.model._v_box(t, self._box(x_lo, x_hi))
+        else:
+            self.model._tau_box(t, self._box(x_lo, x_hi))
+            self._inject(t)
+        self.t_last = t
+
+    def step_async(self, t, kb, x_lo, x_hi):
+        for j in range(kb):
+            tt = t + j
+            if self.elastic:
+                self.half_step_async(tt, 0, x_lo, x_hi)
+                self.half_step_async(tt, 1, x_lo, x_hi)
+                continue
+            if self.tti:
+                r = self.R
+                self.model._pass1(tt, self._box(max(x_lo - r, 0), min(x_hi + r, self.nl)))
+                self.model._pass2(tt, self._box(x_lo, x_hi))
+            else:
+                self.model._box_update(tt, self._box(x_lo, x_hi))
+            self._inject(tt)
+            self.t_last = tt
+
+    def gather_async(self, t, kb):
+        if self._as_rec is None:
+            return
+        gname = "txx" if self.elastic else "p" if self.tti else "u"
+        gname = getattr(self.config, "receiver_field", None) or gname
+        for j in range(kb):
+            self._as_rec[t + j - self._as_t0] = so.record(self._level(gname, t + j), self.ridx,
+                                                           self.rw, self.R)
+
+    def async_finish(self, rec_out=None):
+        if rec_out is not None and self._as_rec is not None:
+            rec_out[...] = self._as_rec
+
     def planes(self, t, i, j, field=0):
         import torch
         R = self.R

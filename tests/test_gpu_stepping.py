@@ -348,7 +348,12 @@ def step_case(name, schedule):
     deps.inject_fields, deps.gather_field = (("u",), "u") if acoustic else (("tau",), "tau")
     sup = dcmp = rsup = None
     if schedule == "naive":
-        deps.inject_points = deps.gather_points = None
+        # engine.py:397-411: the naive plan's footprints for the validator
+        deps.inject_points = np.array(sorted(stb.find_support(src, grid)),
+                                      dtype=np.int64).reshape(-1, 3)
+        idx, wts = rec.stencils(grid)
+        pts = idx.reshape(-1, 3)[wts.ravel() > 0.0]
+        deps.gather_points = pts[np.lexsort((pts[:, 2], pts[:, 1], pts[:, 0]))]
         plan = stb.naive_plan(deps)
     else:
         sup = compressed_support(src, grid)

@@ -79,7 +79,8 @@ def _make(kind, k):
     return _elastic_case() if kind == "elastic" else _case(k)
 
 
-def _worker(rank, world, port, k, out_path, kind="acoustic", device=False, env=None):
+def _worker(rank, world, port, k, out_path, kind="acoustic", device=False, env=None,
+            async_cpu=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     os.environ.update(env or {})
@@ -88,6 +89,10 @@ def _worker(rank, world, port, k, out_path, kind="acoustic", device=False, env=N
         from paper_2010_10248_b200.slabs import run_distributed
         from slab_cpu_backend import OracleSlab
         factory = None if device else OracleSlab          # None: DeviceSlab (CUDA)
+        if async_cpu:
+            class AsyncOracleSlab(OracleSlab):
+                async_ok = True
+            factory = AsyncOracleSlab
         if device:
             import torch
             torch.cuda.set_device(0)
@@ -114,6 +119,26 @@ def test_xslab_matches_single_domain(kind, world, k, tmp_path):
     np.testing.assert_array_equal(got["traces"], ref.receivers)
 
 
+@pytest.mark.parametrize("kind,world,k", [("acoustic", 2, 1), ("acoustic", 3, 1),
+                                          ("acoustic", 2, 2), ("acoustic_so4", 3, 2),
+                                          ("elastic", 2, 1), ("elastic", 3, 1),
+                                          ("elastic_vz", 2, 1), ("tti", 2, 1), ("tti", 3, 1)])
+def test_xslab_async_loop_matches_single_domain(kind, world, k, tmp_path):
+    """SlabRunner's device-ordered loop (the path every physics takes on GPUs)
+    with the CPU stand-in executing its calls: owned-plane launches,
+    R-deep ghost exchanges (elastic: after each half step), async gathers.
+    Bitwise equal to the single-domain oracle."""
+    from oracle import stencil_oracle as so
+    out = str(tmp_path / "res.npz")
+    mp.start_processes(_worker, args=(world, _free_port(), k, out, kind, False, None, True),
+                       nprocs=world, join=True, start_method="spawn")
+    got = np.load(out)
+    ref = so.run(_make(kind, k))
+    for name, arr in ref.fields.items():
+        np.testing.assert_array_equal(got[name], arr, err_msg=name)
+    np.testing.assert_array_equal(got["traces"], ref.receivers)
+
+
 def test_partition_and_ghosts():
     from paper_2010_10248_b200.slabs import ghost_depth, partition
     for nx in (36, 592, 1024):
@@ -132,8 +157,8 @@ def test_partition_and_ghosts():
                                             ("elastic_vz", 1, "1"), ("tti", 1, "1")])
 def test_xslab_async_device_two_processes_gloo(kind, k, overlap, tmp_path):
     """The multi-rank device path end to end -- DeviceSlab handles, the
-    asynchronous loop (acoustic) or the per-block loop (elastic, TTI) (library stream, side stream, events, boundary /
-    interior split, async gather), result gathering -- with two processes on
+    asynchronous loop (library stream, side stream, events, boundary /
+    interior split, elastic half steps, async gather), result gathering -- with two processes on
     one GPU.  gloo stages ghost planes through host memory, so no kernel waits
     on a peer (NCCL P2P kernels would; they need one GPU per rank).  Fields
     and traces equal the oracle bit for bit."""
