@@ -46,6 +46,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "GPts/s (grid-point updates/s), 512^3 acoustic so=8; % of HBM roofline"
 METRIC_TTI = "GPts/s (grid-point updates/s), 512^3 TTI so=8; % of HBM roofline"
+METRIC_EL = "GPts/s (grid-point updates/s), 1024^3 elastic so=8; % of HBM roofline"
+# cfg5 (BASELINE.json configs[4]): 1024^3 computational grid incl. a 40-point
+# sponge (the sponge lives inside the grid, as in the reference)
+SHAPE_EL = (1024,) * 3
+DT_EL = 0.5e-3
 DT_TTI = 0.5e-3
 PHYS = 512
 BL = 40
@@ -118,8 +123,57 @@ def cfg4_inputs(seed: int = 4):
     return medium, src, rec
 
 
+def cfg5_inputs(seed: int = 5, nx: int | None = None):
+    """Seeded stand-in for BASELINE configs[4] (elastic, 1024^3): smooth vp in
+    [2, 4] km/s, vs = vp / 1.7, rho in [1800, 2500] kg/m^3 (sums of three
+    seeded low-wavenumber separable cosine products, each in [-1, 1], mapped
+    affinely onto the range), an explosive 12 Hz Ricker at a seeded off-grid
+    point, 1024 receivers on a line at 20 m depth.  ``nx``: only the first nx
+    x planes of the media (the CPU baseline's sample)."""
+    rng = np.random.default_rng(seed)
+    n = SHAPE_EL[0]
+    x = np.arange(n, dtype=np.float64) / n
+    nx = n if nx is None else min(nx, n)
+    shape = (nx,) + SHAPE_EL[1:]
+
+    def smooth(lo, hi):
+        f = np.zeros(shape)
+        for _ in range(3):
+            k = rng.uniform(0.5, 2.0, 3)
+            ph = rng.uniform(0, 2 * np.pi, 3)
+            f += (np.cos(2 * np.pi * k[0] * x[:nx] + ph[0])[:, None, None]
+                  * np.cos(2 * np.pi * k[1] * x + ph[1])[None, :, None]
+                  * np.cos(2 * np.pi * k[2] * x + ph[2])[None, None, :])
+        f += 3.0
+        f *= (hi - lo) / 6.0
+        f += lo
+        return f
+    vp = smooth(2000.0, 4000.0)
+    medium = {"vp": vp, "vs": vp / 1.7, "rho": smooth(1800.0, 2500.0)}
+    phys = n - 2 * BL
+    src = rng.uniform(0.0, (phys - 1) * H, size=(1, 3))
+    xs = np.clip(np.arange(phys) * H + rng.uniform(0.0, 9.99, size=phys), 0, (phys - 1) * H)
+    xs = np.concatenate([xs, xs[: 1024 - phys]]) if phys < 1024 else xs[:1024]
+    rec = np.stack([xs, np.full(len(xs), 0.5 * (phys - 1) * H), np.full(len(xs), 20.0)], axis=1)
+    return medium, src, rec
+
+
+def workload_metric(workload: str) -> str:
+    return {"cfg4": METRIC_TTI, "cfg5": METRIC_EL}.get(workload, METRIC)
+
+
+def workload_shape(workload: str) -> tuple:
+    return SHAPE_EL if workload == "cfg5" else SHAPE
+
+
 def make_config(stb, v, src, rec, nt, k, arithmetic="exact", workload="cfg2"):
-    grid = stb.GridSpec(SHAPE, (H, H, H), (-BL * H,) * 3, boundary_layers=BL)
+    grid = stb.GridSpec(workload_shape(workload), (H, H, H), (-BL * H,) * 3, boundary_layers=BL)
+    if workload == "cfg5":
+        cfg = stb.RunConfig(physics="elastic", grid=grid, space_order=SO, nt=nt, dt=DT_EL,
+                            medium=v, sources=stb.SourceSpec(src, f0=12.0),
+                            receiver_coords=rec, schedule=stb.ScheduleSpec("gpu", time_height=1))
+        cfg.receiver_field = "vz"          # BASELINE: receivers interpolate vx/vz
+        return cfg
     if workload == "cfg4":
         return stb.RunConfig(physics="tti", grid=grid, space_order=SO, nt=nt, dt=DT_TTI,
                              medium=v, sources=stb.SourceSpec(src, f0=15.0),
@@ -133,7 +187,7 @@ def make_config(stb, v, src, rec, nt, k, arithmetic="exact", workload="cfg2"):
 
 
 def workload_inputs(workload):
-    return cfg4_inputs() if workload == "cfg4" else cfg2_inputs()
+    return {"cfg4": cfg4_inputs, "cfg5": cfg5_inputs}.get(workload, cfg2_inputs)()
 
 
 def medium_nbytes(v):
@@ -145,6 +199,10 @@ def medium_nbytes(v):
 WORKLOAD_TEXT = {
     "cfg2": "cfg2 (BASELINE configs[1]): 512^3 + 2x40 sponge = 592^3 computational grid, "
             "acoustic so=8, 1 Ricker 15 Hz, 512x512 receivers, dt=0.8 ms",
+    "cfg5": "cfg5 (BASELINE configs[4]): 1024^3 computational grid (incl. 40-point sponge), "
+            "elastic velocity-stress so=8 (9 fields), smooth vp 2-4 km/s, vs = vp/1.7, "
+            "rho 1.8-2.5 g/cc, explosive Ricker 12 Hz into txx/tyy/tzz, 1024 vz receivers, "
+            "dt=0.5 ms",
     "cfg4": "cfg4 (BASELINE configs[3]): 512^3 + 2x40 sponge = 592^3 computational grid, "
             "TTI so=8 (p, q), layered vp/eps/delta, smooth theta/phi, 1 Ricker 15 Hz, "
             "512 receivers on a line, dt=0.5 ms",
@@ -296,14 +354,14 @@ def dist_setup(n_gpus: int):
     return rank, world, local
 
 
-def _x_sample(v, src, rec, nx: int):
+def _x_sample(v, src, rec, nx: int, full=SHAPE):
     """The workload restricted to its first nx x planes (same spacing, origin,
     y/z extent and sponge): the source is moved to the slab's centre plane
     and receivers outside the slab's physical interior are dropped."""
-    if nx >= SHAPE[0]:
-        return v, src, rec, SHAPE
-    shape = (nx,) + tuple(SHAPE[1:])
-    sl = lambda a: np.ascontiguousarray(np.broadcast_to(a, SHAPE)[:nx])  # noqa: E731
+    if nx >= full[0]:
+        return v, src, rec, full
+    shape = (nx,) + tuple(full[1:])
+    sl = lambda a: np.ascontiguousarray(np.broadcast_to(a, full)[:nx])  # noqa: E731
     v = {k: sl(a) for k, a in v.items()} if isinstance(v, dict) else sl(v)
     x_lo, x_hi = -BL * H, -BL * H + (nx - 1 - BL) * H    # grid origin; last interior plane
     src = src.copy()
@@ -317,17 +375,35 @@ def cpu_baseline(steps: int, threads: int, workload: str = "cfg2", nx: int | Non
     sample of the same workload (the first nx x planes, default all)."""
     from types import SimpleNamespace
     from oracle import stencil_oracle as so
-    v, src, rec = workload_inputs(workload)
-    v, src, rec, shape = _x_sample(v, src, rec, nx or SHAPE[0])
+    full = workload_shape(workload)
+    if workload == "cfg5":
+        # only the sampled planes of the 1024^3 media are generated
+        v, src, rec = cfg5_inputs(nx=nx or full[0])
+        v = {key: np.ascontiguousarray(a) for key, a in v.items()}
+        full_s = (v["vp"].shape[0],) + full[1:]
+        v, src, rec, shape = _x_sample(v, src, rec, full_s[0], full_s)
+        if full_s[0] < full[0]:
+            shape = full_s
+            x_lo = -BL * H
+            src = src.copy()
+            src[:, 0] = 0.5 * (x_lo + (shape[0] - 1) * H - BL * H)
+            x_hi = x_lo + (shape[0] - 1 - BL) * H
+            rec = rec[(rec[:, 0] >= x_lo + BL * H) & (rec[:, 0] <= x_hi)]
+    else:
+        v, src, rec = workload_inputs(workload)
+        v, src, rec, shape = _x_sample(v, src, rec, nx or full[0], full)
     grid = SimpleNamespace(shape=shape, spacing=(H,) * 3, origin=(-BL * H,) * 3,
                            boundary_layers=BL)
-    tti = workload == "cfg4"
-    cfg = SimpleNamespace(physics="tti" if tti else "acoustic", grid=grid, space_order=SO,
-                          medium=v if tti else {"velocity": v},
-                          nt=steps, time_ms=None, dt=DT_TTI if tti else DT, cfl_safety=0.9,
-                          sources=SimpleNamespace(coords=src, f0=15.0, t0=None, amplitude=1.0,
-                                                  wavelets=None),
-                          receiver_coords=rec, precision=32, damping_decay=None)
+    physics = {"cfg4": "tti", "cfg5": "elastic"}.get(workload, "acoustic")
+    cfg = SimpleNamespace(physics=physics, grid=grid, space_order=SO,
+                          medium={"velocity": v} if physics == "acoustic" else v,
+                          nt=steps, time_ms=None,
+                          dt={"tti": DT_TTI, "elastic": DT_EL}.get(physics, DT), cfl_safety=0.9,
+                          sources=SimpleNamespace(coords=src,
+                                                  f0=12.0 if physics == "elastic" else 15.0,
+                                                  t0=None, amplitude=1.0, wavelets=None),
+                          receiver_coords=rec, precision=32, damping_decay=None,
+                          receiver_field="vz" if physics == "elastic" else None)
     res = so.run(cfg, threads=threads)
     npts = int(np.prod(shape))
     return npts * res.steps / res.elapsed_s / 1e9, res.elapsed_s, res.steps
@@ -346,23 +422,25 @@ def run_reference_arm(args):
     total = args.warmup + args.steps
     # calibration on a slab large enough to be memory-bound like the sample
     # (small slabs run faster per point); 0.7 safety factor
-    cal_gps, _, _ = cpu_baseline(2, threads, args.workload, nx=96)
-    plane = SHAPE[1] * SHAPE[2]
+    shape = workload_shape(args.workload)
+    cal_gps, _, _ = cpu_baseline(2, threads, args.workload,
+                                 nx=24 if args.workload == "cfg5" else 96)
+    plane = shape[1] * shape[2]
     nx = int(0.7 * REF_BUDGET_S * cal_gps * 1e9 / (total * plane))
-    nx = max(24, min(SHAPE[0], nx))
+    nx = max(16 if args.workload == "cfg5" else 24, min(shape[0], nx))
     gps, elapsed, steps = cpu_baseline(total, threads, args.workload, nx=nx)
-    tti = args.workload == "cfg4"
     line = {
-        "impl": "reference", "metric": METRIC_TTI if tti else METRIC, "value": gps,
+        "impl": "reference", "metric": workload_metric(args.workload), "value": gps,
         "unit": "GPts/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * elapsed / max(steps, 1), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD_TEXT[args.workload], "grid": list(SHAPE)},
+        "config": {"workload": WORKLOAD_TEXT[args.workload], "grid": list(shape)},
         "cpu_baseline": {"value": gps, "unit": "GPts/s", "cores": threads, "kind": "port",
                          **host_cpu_info(),
                          "sample": f"{steps} time steps of {args.workload} on its first "
-                                   f"{nx} of 592 x planes ({nx} x 592 x 592 points per "
+                                   f"{nx} of {shape[0]} x planes ({nx} x {shape[1]} x "
+                                   f"{shape[2]} points per "
                                    f"step) through the oracle port (NumPy, {threads} "
                                    f"threads, x-chunked; warmup included: the port has "
                                    f"no warm-up effect)"},
@@ -384,8 +462,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg4"],
-                    help="cfg2: acoustic headline (default); cfg4: TTI")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg4", "cfg5"],
+                    help="cfg2: acoustic headline (default); cfg4: TTI; cfg5: elastic 1024^3")
     ap.add_argument("--launch-check", action="store_true",
                     help="multi-rank plumbing only (no workload); see launch_check()")
     args = ap.parse_args()
@@ -412,7 +490,8 @@ def main():
     v, src, rec = workload_inputs(wl)
     nt_series = args.warmup + args.steps
     cfg = make_config(stb, v, src, rec, nt_series, args.k, args.arithmetic, wl)
-    npts = int(np.prod(SHAPE))
+    shape = workload_shape(wl)
+    npts = int(np.prod(shape))
 
     # ------------------------------------------------------------ value
     runner = slabs.SlabRunner(cfg, rank=rank, world=world)
@@ -482,7 +561,7 @@ def main():
         t0 = time.perf_counter()
         res = stb.run(cfg_e)
         e2e_s = time.perf_counter() - t0
-        h2d = medium_nbytes(v) + src.nbytes + rec.nbytes + 8 * sum(SHAPE) + 8 * args.steps
+        h2d = medium_nbytes(v) + src.nbytes + rec.nbytes + 8 * sum(shape) + 8 * args.steps
         d2h = sum(f.nbytes for f in res.fields.values()) + res.receivers.nbytes
         e2e = {"value": npts * args.steps / e2e_s / 1e9, "unit": "GPts/s",
                "h2d_bytes_per_step": int(h2d / args.steps),
@@ -501,7 +580,7 @@ def main():
         wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         dist.all_reduce(wall, op=dist.ReduceOp.MAX)
         e2e_s = float(wall.item())
-        h2d = medium_nbytes(v) + src.nbytes + rec.nbytes + 8 * sum(SHAPE) + 8 * args.steps
+        h2d = medium_nbytes(v) + src.nbytes + rec.nbytes + 8 * sum(shape) + 8 * args.steps
         d2h = 4 * npts * len(fields or {"u": 0}) + 8 * args.steps * len(rec)
         e2e = {"value": npts * args.steps / e2e_s / 1e9, "unit": "GPts/s",
                "h2d_bytes_per_step": int(h2d / args.steps),
@@ -522,17 +601,18 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC_TTI if wl == "cfg4" else METRIC, "value": value, "unit": "GPts/s", "n_gpus": world,
+            "metric": workload_metric(wl), "value": value, "unit": "GPts/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT[wl],
-                       "grid": list(SHAPE), "time_height": k_used,
+                       "grid": list(shape), "time_height": k_used,
                        "arithmetic": args.arithmetic,
                        "parallelism": f"x-slab{world}",
                        "l2": "inputs larger than L2 (each 592^3 f32 field ~0.85 GB >> 126 MB)",
                        "gpts_counting": "computational grid incl. sponge (engine.py:445-447)",
-                       "value_physical_512": PHYS ** 3 * args.steps / (t_ms / 1e3) / 1e9,
+                       "value_physical": ((shape[0] - 2 * BL) ** 3 * args.steps
+                                          / (t_ms / 1e3) / 1e9),
                        "kernel": describe},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": st["launches"], "clocks": clocks,

@@ -282,6 +282,11 @@ int stb_prop_describe(stb_prop_t p, int32_t time_height, char* buf, int64_t bufl
  * (schedule.py:171-207) run as consecutive blocks of this depth; run()
  * reports the depth used in RunReport.schedule["time_height"]. */
 int stb_prop_max_time_height(stb_prop_t p, int32_t* k);
+/* max of the velocity array the handle was created from, as np.max
+ * (engine.py:160-169; NaN if it holds a NaN or was not recorded): acoustic
+ * handles reduce it on the device in the kernel that forms inv, so the host
+ * need not read the 1.7 GB velocity a second time for the sponge decay. */
+int stb_prop_velocity_max(stb_prop_t p, double* vmax);
 int stb_prop_destroy(stb_prop_t p);
 
 /* ------------------------------------------------------------------------

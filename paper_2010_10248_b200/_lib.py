@@ -34,7 +34,7 @@ EXPORTS = (
     "stb_prop_set_damping",
     "stb_prop_step_async", "stb_prop_half_step_async", "stb_prop_gather_async", "stb_prop_async_finish", "stb_prop_reset", "stb_prop_stats",
     "stb_prop_describe",
-    "stb_prop_max_time_height",
+    "stb_prop_max_time_height", "stb_prop_velocity_max",
     "stb_prop_destroy",
     "stb_box_acoustic_update", "stb_box_elastic_v", "stb_box_elastic_tau", "stb_box_scatter",
     "stb_box_gather", "stb_record_receivers",
@@ -130,6 +130,7 @@ def _declare(lib):
         "stb_prop_stats": ([P, pi64, pdbl, pi64, pi64, pdbl], C.c_int),
         "stb_prop_describe": ([P, i32, C.c_char_p, i64], C.c_int),
         "stb_prop_max_time_height": ([P, C.POINTER(i32)], C.c_int),
+        "stb_prop_velocity_max": ([P, pdbl], C.c_int),
         "stb_prop_destroy": ([P], C.c_int),
         "stb_box_acoustic_update": ([C.POINTER(Layout), P, P, P, i32, pi32, dbl, pdbl, P, dbl,
                                      P, C.POINTER(Box), P], C.c_int),

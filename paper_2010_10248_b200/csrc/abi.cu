@@ -377,6 +377,13 @@ STB_API int stb_prop_max_time_height(stb_prop_t p, int32_t* k) {
   })
 }
 
+STB_API int stb_prop_velocity_max(stb_prop_t p, double* vmax) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr && vmax != nullptr, STB_ERR_ARG, "NULL argument");
+    *vmax = p->velocity_max();
+  })
+}
+
 STB_API int stb_prop_destroy(stb_prop_t p) {
   STB_GUARD({ delete p; })
 }

@@ -18,6 +18,7 @@
 //   reference  thread-per-point kernel for fp64 and degenerate grids.
 // Time level t lives in buffer t mod NB (NB = 6: distinct inputs/outputs
 // for every K <= 4).
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -37,22 +38,44 @@ namespace {
 
 inline unsigned g1(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
 
+// order-preserving int64 key of a double (signed integer order == numeric
+// order for non-NaN values), for atomicMax
+__device__ __forceinline__ long long dkey(double x) {
+  const long long b = __double_as_longlong(x);
+  return b >= 0 ? b : b ^ 0x7fffffffffffffffLL;
+}
+
 template <typename T>
 __global__ void inv_from_velocity_kernel(const double* __restrict__ v, const double* __restrict__ m,
-                                         double dt2, Dims d, T* __restrict__ inv, int* bad_m) {
+                                         double dt2, Dims d, T* __restrict__ inv, int* bad_m,
+                                         long long* vmax_key, int* v_nan) {
   const int64_t n = d.nx * d.ny * d.nz;
+  long long mk = LLONG_MIN;
+  int nan = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double mm;
     if (v) {
       const double vi = v[i];
       mm = rdiv(1.0, rmul(vi, vi));            // engine.py:243: 1/v**2
+      nan |= vi != vi;
+      mk = max(mk, dkey(vi));                  // max(v) for the sponge decay
     } else {
       mm = m[i];
     }
     if (mm <= 0.0) atomicExch(bad_m, 1);      // physics.py:149-150
     const int64_t z = i % d.nz, xy = i / d.nz;
     inv[xy * d.pitch + z] = from_f64<T>(rdiv(dt2, mm));   // physics.py:151
+  }
+  if (v) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mk = max(mk, __shfl_xor_sync(0xffffffffu, mk, o));
+      nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMax(vmax_key, mk);
+      if (nan) atomicExch(v_nan, 1);
+    }
   }
 }
 
@@ -274,16 +297,29 @@ class AcousticProp final : public stb_prop_s {
       tmp.upload(desc.velocity ? desc.velocity : desc.m, n, st_);
       inv_.alloc(d_.total());
       inv_.zero(st_);
-      DevBuf<int> bad(1);
-      bad.zero(st_);
+      // flags[0]: m <= 0, flags[1]: NaN velocity; vkey: max(v) key
+      DevBuf<int> flags(2);
+      flags.zero(st_);
+      DevBuf<long long> vkey(1);
+      const long long lo = LLONG_MIN;
+      STB_CUDA(cudaMemcpyAsync(vkey.p, &lo, sizeof(lo), cudaMemcpyHostToDevice, st_));
       inv_from_velocity_kernel<T><<<1184, 256, 0, st_>>>(desc.velocity ? tmp.p : nullptr,
                                                          desc.velocity ? nullptr : tmp.p,
-                                                         desc.dt2, d_, inv_.p, bad.p);
+                                                         desc.dt2, d_, inv_.p, flags.p, vkey.p,
+                                                         flags.p + 1);
       STB_CHECK_LAUNCH();
-      int hb = 0;
-      bad.download(&hb, 1, st_);
+      int hf[2] = {0, 0};
+      long long hk = lo;
+      flags.download(hf, 2, st_);
+      vkey.download(&hk, 1, st_);
       STB_CUDA(cudaStreamSynchronize(st_));
-      STB_REQUIRE(hb == 0, STB_ERR_ARG, "m must be positive everywhere");
+      STB_REQUIRE(hf[0] == 0, STB_ERR_ARG, "m must be positive everywhere");
+      if (desc.velocity) {
+        const long long b = hk >= 0 ? hk : hk ^ 0x7fffffffffffffffLL;
+        double vm;
+        std::memcpy(&vm, &b, sizeof(vm));
+        vmax_ = hf[1] ? NAN : vm;             // np.max propagates NaN
+      }
     } else {
       inv_scalar_ = (T)desc.inv_scalar;
     }
@@ -827,6 +863,7 @@ class AcousticProp final : public stb_prop_s {
   }
 
   int max_time_height() const override { return path_ == Path::Fused ? max_k_ : 1; }
+  double velocity_max() const override { return vmax_; }
 
  private:
   enum class Path { Reference, Fused };
@@ -1118,6 +1155,7 @@ class AcousticProp final : public stb_prop_s {
   }
 
   int R_ = 1;
+  double vmax_ = NAN;            // max(velocity), reduced while forming inv
   Dims d_{};
   // async stepping state
   bool as_open_ = false;

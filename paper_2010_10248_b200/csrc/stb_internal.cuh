@@ -5,6 +5,7 @@
 
 #include <atomic>
 
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -209,6 +210,8 @@ struct stb_prop_s {
   // deepest time_height one fused pass supports (requests above it are
   // split into blocks of this depth; schedule.py:171-207 accepts any T)
   virtual int max_time_height() const { return 1; }
+  // max of the velocity the handle was built from (NaN: not known)
+  virtual double velocity_max() const { return NAN; }
   // local field shape (x slab) and element size, for host-side copies
   virtual void field_info(int64_t shape[3], int* elem_bytes) = 0;
   // asynchronous stepping (multi-GPU x slabs): enqueue on stream() without

@@ -361,8 +361,10 @@ class _Prop:
                                            _lib.dptr(rec_out.reshape(-1)) if rec_out is not None
                                            else _lib.dptr(None), C.byref(bad)))
 
-    def read(self, name, t, shape):
-        out = np.empty(shape, dtype=self.dtype)
+    def read(self, name, t, shape, out=None):
+        if out is None:
+            out = np.empty(shape, dtype=self.dtype)
+        assert out.shape == tuple(shape) and out.dtype == self.dtype and out.flags.c_contiguous
         _lib.check(_lib.lib().stb_prop_read_field(self.raw, self.fields.index(name), t,
                                                   out.ctypes.data_as(C.c_void_p)))
         return out
@@ -406,6 +408,11 @@ class _Prop:
                                              C.byref(al), C.byref(rm)))
         return {"stencil_launches": n.value, "stencil_ms": ms.value, "updates": up.value,
                 "launches": al.value, "run_ms": rm.value}
+
+    def velocity_max(self) -> float:
+        v = C.c_double(float("nan"))
+        _lib.check(_lib.lib().stb_prop_velocity_max(self.raw, C.byref(v)))
+        return float(v.value)
 
     def max_time_height(self) -> int:
         k = C.c_int32(1)
@@ -710,11 +717,41 @@ def make_report(config: RunConfig, fields, rec, nt, dt, elapsed, precompute_s, p
     )
 
 
+def _prefault_async(arrays, min_bytes: int = 64 << 20):
+    """Touch the pages of large fresh arrays from host threads in the
+    background; returns a join function."""
+    big = [a for a in arrays if a.nbytes >= min_bytes]
+    if os.environ.get("STB_PREFAULT", "1") == "0":
+        big = []
+    if not big:
+        return lambda: None
+    import threading
+    nthr = max(1, min(16, os.cpu_count() or 1))
+    jobs = []
+    for a in big:
+        flat = a.reshape(-1)
+        step = -(-flat.size // nthr)
+        jobs += [flat[i:i + step] for i in range(0, flat.size, step)]
+    threads = [threading.Thread(target=lambda v=v: v.fill(0), daemon=True) for v in jobs]
+    for th in threads:
+        th.start()
+
+    def join():
+        for th in threads:
+            th.join()
+    return join
+
+
 def run(config: RunConfig) -> RunResult:
     """Execute a configured run on the GPU (engine.py:379-489 semantics).
     ``schedule.n_gpus`` > 1 (or a ``devices`` list) splits the grid in
     x-slabs over that many GPUs of this process (multi.py)."""
     _lib.require_device()
+    marks = [("start", time.perf_counter())] if os.environ.get("STB_TIMING") else None
+
+    def mark(label):
+        if marks is not None:
+            marks.append((label, time.perf_counter()))
     k = _gpu_time_height(config)
     devices = _slab_devices(config)
     if devices is not None:
@@ -740,10 +777,19 @@ def run(config: RunConfig) -> RunResult:
                 if config.physics == "tti":
                     while not host_done.wait(0.005) and not fut.done():
                         pass
-                v_max = medium_velocity_bounds(config.physics, config.medium)
+                # acoustic: the kernel forming inv reduces max(v) on the
+                # device; TTI reads it here
+                device_vmax = config.physics == "acoustic"
+                v_max = (None if device_vmax else
+                         medium_velocity_bounds(config.physics, config.medium))
                 src_prep = _host_sparse_prep(config, dt, nt)
             finally:
                 prop = fut.result()
+        mark("model upload + host prep")
+        if v_max is None:
+            v_max = prop.velocity_max()
+            if not math.isfinite(v_max):        # NaN: not recorded (or NaN input)
+                v_max = medium_velocity_bounds(config.physics, config.medium)
         decay = (config.damping_decay if config.damping_decay is not None
                  else default_damping_decay(grid, v_max))
         prop.set_damping(damping_tables(grid, decay, dt))
@@ -752,6 +798,7 @@ def run(config: RunConfig) -> RunResult:
         dt, nt = resolve_steps(config, v_max)
         prop = build_propagator(config, dt, v_max)
 
+    mark("sponge tables")
     t_pre0 = time.perf_counter()
     nsrc = nrec = 0
     spec = config.sources
@@ -781,17 +828,32 @@ def run(config: RunConfig) -> RunResult:
         for kk in ([min(k, k_max)] if k > 0 else range(1, k_max + 1)):
             _validate_device_plan(config, prop, kk, nt, handle if nsrc else None)
 
-    t0 = time.perf_counter()
-    if nt > 0:
-        prop.run(0, nt, k, rec)
-    elapsed = time.perf_counter() - t0
-
+    mark("sources + receivers (inspector)")
     names = FIELDS[config.physics]
+    # the output arrays are faulted in (the kernel zeroes fresh pages) by
+    # host threads while the GPU steps, not on the download's critical path
+    outs = {n: np.empty(grid.shape, dtype=config.dtype) for n in names} if nt > 0 else {}
+    prefault = _prefault_async(list(outs.values()))
+    t0 = time.perf_counter()
+    try:
+        if nt > 0:
+            prop.run(0, nt, k, rec)
+    finally:
+        prefault()
+    elapsed = time.perf_counter() - t0
+    mark("stepping (+ trace copies)")
+
     t_final = nt - 1 if nt > 0 else 0
     if nt > 0:
-        fields = {n: prop.read(n, t_final, grid.shape) for n in names}
+        fields = {n: prop.read(n, t_final, grid.shape, out=outs[n]) for n in names}
     else:
         fields = {n: np.zeros(grid.shape, dtype=config.dtype) for n in names}
+    mark("field download")
+    if marks is not None:
+        import sys
+        print("run() phases: " + ", ".join(
+            f"{lab} {1e3 * (t1 - t0_):.1f} ms" for (_, t0_), (lab, t1) in zip(marks, marks[1:])),
+            file=sys.stderr)
     plan_text = prop.describe(k)
     m = re.search(r"\bk=(\d+)", plan_text)
     report = make_report(config, fields, rec, nt, dt, elapsed, precompute_s, plan_text,
