@@ -872,7 +872,9 @@ class AcousticProp final : public stb_prop_s {
   // warps -- less y halo per staged plane and room for a deeper prefetch
   // (measured +1 % at so=4/8 and +10 % at so=12 over two 16-row CTAs per
   // SM).
-  static constexpr int fused_ty(int) { return kFusedTY1 > 0 ? kFusedTY1 : kTY; }
+  // R >= 7: 16-row tiles (one CTA of 8 consumer warps): the 2R+1-plane
+  // register queue needs more registers than 16 warps of a 32-row tile get
+  static constexpr int fused_ty(int R) { return R >= 7 ? kTY : (kFusedTY1 > 0 ? kFusedTY1 : kTY); }
   static constexpr int kWtbPF = 3;                // two-level kernel: TMA prefetch depth
   // rows per thread: 2 (measured at R = 2: RY = 1 gives 21 warps instead of
   // 11 but doubles the per-plane bookkeeping per point, 274 vs 328 GPts/s)
@@ -888,7 +890,7 @@ class AcousticProp final : public stb_prop_s {
   // tiles: 3, and 2 at R = 6.
   static constexpr int pf_for(int R) {
     if (fused_ty(R) != kTY) return R >= 6 ? 3 : 4;
-    return R >= 6 ? 2 : 3;
+    return 2;
   }
 
   int slot(int64_t t) const { return (int)(((t % NB) + NB) % NB); }
@@ -965,7 +967,11 @@ class AcousticProp final : public stb_prop_s {
       case 1: return fused_cx_r<1>(L);
       case 2: return fused_cx_r<2>(L);
       case 4: return fused_cx_r<4>(L);
+      case 3: return fused_cx_r<3>(L);
+      case 5: return fused_cx_r<5>(L);
       case 6: return fused_cx_r<6>(L);
+      case 7: return fused_cx_r<7>(L);
+      case 8: return fused_cx_r<8>(L);
       default: return L;
     }
   }
@@ -991,7 +997,7 @@ class AcousticProp final : public stb_prop_s {
     path_ = Path::Reference;
     if constexpr (sizeof(T) == 4) {
       if (!(active_[0] && active_[1] && active_[2])) return;
-      if (R_ != 1 && R_ != 2 && R_ != 4 && R_ != 6) return;
+      if (R_ < 1 || R_ > 8) return;
       const char* e = std::getenv("STB_PATH");
       if (e && std::strcmp(e, "reference") == 0) return;
       tcf_.c0 = cf_.c0;
@@ -1128,7 +1134,11 @@ class AcousticProp final : public stb_prop_s {
                                : launch_fused_rk<2>(t, gflag, gmask, x_lo, x_hi);
         case 4: return kb == 2 ? launch_wtb_rk<4>(t, gflag, gmask, x_lo, x_hi)
                                : launch_fused_rk<4>(t, gflag, gmask, x_lo, x_hi);
+        case 3: return launch_fused_rk<3>(t, gflag, gmask, x_lo, x_hi);
+        case 5: return launch_fused_rk<5>(t, gflag, gmask, x_lo, x_hi);
         case 6: return launch_fused_rk<6>(t, gflag, gmask, x_lo, x_hi);
+        case 7: return launch_fused_rk<7>(t, gflag, gmask, x_lo, x_hi);
+        case 8: return launch_fused_rk<8>(t, gflag, gmask, x_lo, x_hi);
         default: throw Error(STB_ERR_ARG, "no fused kernel for this space order");
       }
     }

@@ -90,7 +90,7 @@ struct FusedCfg {
   static constexpr size_t SMEM = RING1 + RING2 + BUFS + BARS;
   // resident CTAs per SM the launch bounds ask for: two for the 9-warp
   // K = 1 tiles (and the K = 2 R <= 2 kernel), one otherwise
-  static constexpr int MINB = K == 1 ? (NT <= 320 ? 2 : 1) : (R <= 2 ? 2 : 1);
+  static constexpr int MINB = K == 1 ? (NT <= 320 && R <= 6 ? 2 : 1) : (R <= 2 ? 2 : 1);
 };
 
 struct FusedMaps {
