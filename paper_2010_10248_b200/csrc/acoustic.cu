@@ -874,7 +874,7 @@ class AcousticProp final : public stb_prop_s {
   // SM).
   // R >= 7: 16-row tiles (one CTA of 8 consumer warps): the 2R+1-plane
   // register queue needs more registers than 16 warps of a 32-row tile get
-  static constexpr int fused_ty(int R) { return R >= 7 ? kTY : (kFusedTY1 > 0 ? kFusedTY1 : kTY); }
+  static constexpr int fused_ty(int R) { return R >= 7 ? 24 : (kFusedTY1 > 0 ? kFusedTY1 : kTY); }
   static constexpr int kWtbPF = 3;                // two-level kernel: TMA prefetch depth
   // rows per thread: 2 (measured at R = 2: RY = 1 gives 21 warps instead of
   // 11 but doubles the per-plane bookkeeping per point, 274 vs 328 GPts/s)
