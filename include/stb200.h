@@ -165,6 +165,14 @@ typedef struct {
   int64_t x_begin;           /* x slab, as in stb_acoustic_desc (materials are
                                 the local slab; geometry, tables global)     */
   int64_t nx_local;
+  /* from_velocities = 1: lam/mu are formed on the device from vp, vs, rho
+     exactly as engine.py:247-255 does in f64 (mu = rho*vs^2, lam =
+     rho*vp^2 - 2*mu) and checked as physics.py:229-236 does; lam/mu above
+     are ignored.  The handle also records max(vp) (stb_prop_velocity_max). */
+  int32_t from_velocities;
+  const double* vp;          /* per point or NULL -> vp_scalar               */
+  const double* vs;
+  double vp_scalar, vs_scalar;
 } stb_elastic_desc;
 
 /* Pseudo-acoustic TTI, coupled p and q (eq. 2).  Not in

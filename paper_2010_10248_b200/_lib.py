@@ -62,7 +62,9 @@ class ElasticDesc(C.Structure):
                 ("rho", C.POINTER(C.c_double)), ("lam_scalar", C.c_double),
                 ("mu_scalar", C.c_double), ("rho_scalar", C.c_double),
                 ("damp", C.POINTER(C.c_double) * 3), ("x_begin", C.c_int64),
-                ("nx_local", C.c_int64)]
+                ("nx_local", C.c_int64), ("from_velocities", C.c_int32),
+                ("vp", C.POINTER(C.c_double)), ("vs", C.POINTER(C.c_double)),
+                ("vp_scalar", C.c_double), ("vs_scalar", C.c_double)]
 
 
 class Layout(C.Structure):

@@ -18,7 +18,10 @@
 // sweeps of elastic_tiled.cuh; f64 and degenerate grids the thread-per-point
 // kernels below.  Every launch covers a local x range [x_lo, x_hi) (x-slab
 // runs compute owned planes only and exchange R ghost planes per half step).
+#include <climits>
+#include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <memory>
 #include <sstream>
 
@@ -238,6 +241,54 @@ __global__ void elastic_materials_kernel(const double* __restrict__ lam,
   }
 }
 
+// Same from vp, vs, rho (engine.py:247-255 in f64: mu = rho*vs**2,
+// lam = rho*vp**2 - 2*mu), with physics.py:229-236's checks as flag bits
+// (1: rho <= 0, 2: mu < 0, 4: lam + 2*mu <= 0) and max(vp) for the sponge
+// decay (order-preserving int64 key; NaN flagged separately).
+struct MatIn {
+  const double* p;
+  double s;
+  __device__ double at(int64_t i) const { return p ? p[i] : s; }
+};
+
+__device__ __forceinline__ long long el_dkey(double x) {
+  const long long b = __double_as_longlong(x);
+  return b >= 0 ? b : b ^ 0x7fffffffffffffffLL;
+}
+
+template <typename T>
+__global__ void elastic_materials_from_velocity_kernel(MatIn vp, MatIn vs, MatIn rho, double dt,
+                                                       PDims d, T* __restrict__ buoy,
+                                                       T* __restrict__ lam_dt,
+                                                       T* __restrict__ mu_dt, int* flags,
+                                                       long long* vmax_key) {
+  const int64_t n = d.nx * d.ny * d.nz;
+  int f = 0;
+  long long mk = LLONG_MIN;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double p = vp.at(i), sv = vs.at(i), r = rho.at(i);
+    const double mu = rmul(r, rmul(sv, sv));
+    const double lam = rsub(rmul(r, rmul(p, p)), rmul(2.0, mu));
+    f |= (r <= 0.0 ? 1 : 0) | (mu < 0.0 ? 2 : 0) | (radd(lam, rmul(2.0, mu)) <= 0.0 ? 4 : 0);
+    f |= (p != p) ? 8 : 0;
+    mk = max(mk, el_dkey(p));
+    const int64_t z = i % d.nz, xy = i / d.nz;
+    const int64_t o = d.at(xy / d.ny, xy % d.ny, z);
+    buoy[o] = from_f64<T>(rdiv(dt, r));
+    lam_dt[o] = from_f64<T>(rmul(dt, lam));
+    mu_dt[o] = from_f64<T>(rmul(dt, mu));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mk = max(mk, __shfl_xor_sync(0xffffffffu, mk, o));
+    f |= __shfl_xor_sync(0xffffffffu, f, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(vmax_key, mk);
+    if (f) atomicOr(flags, f);
+  }
+}
+
 }  // namespace
 }  // namespace stb
 
@@ -294,8 +345,51 @@ class ElasticProp final : public stb_prop_s {
     const int64_t n = d_.nx * d_.ny * d_.nz;
     const double dt = desc.dt;
     // materials (physics.py:251-257)
-    const bool any_arr = desc.lam || desc.mu || desc.rho;
-    if (any_arr) {
+    const bool any_arr = desc.lam || desc.mu || desc.rho ||
+                         (desc.from_velocities && (desc.vp || desc.vs));
+    if (any_arr && desc.from_velocities) {
+      auto up = [&](DevBuf<double>& b, const double* h) {
+        if (h) {
+          b.alloc(n);
+          b.upload(h, n, st_);
+        }
+      };
+      DevBuf<double> vp, vs, rho;
+      up(vp, desc.vp);
+      up(vs, desc.vs);
+      up(rho, desc.rho);
+      buoy_.alloc(d_.total);
+      lam_.alloc(d_.total);
+      mu_.alloc(d_.total);
+      buoy_.zero(st_);
+      lam_.zero(st_);
+      mu_.zero(st_);
+      DevBuf<int> flags(1);
+      flags.zero(st_);
+      DevBuf<long long> vkey(1);
+      const long long lo = LLONG_MIN;
+      STB_CUDA(cudaMemcpyAsync(vkey.p, &lo, sizeof(lo), cudaMemcpyHostToDevice, st_));
+      elastic_materials_from_velocity_kernel<T><<<1184, 256, 0, st_>>>(
+          MatIn{vp.p, desc.vp_scalar}, MatIn{vs.p, desc.vs_scalar}, MatIn{rho.p, desc.rho_scalar},
+          dt, d_, buoy_.p, lam_.p, mu_.p, flags.p, vkey.p);
+      STB_CHECK_LAUNCH();
+      int hf = 0;
+      long long hk = lo;
+      flags.download(&hf, 1, st_);
+      vkey.download(&hk, 1, st_);
+      STB_CUDA(cudaStreamSynchronize(st_));
+      STB_REQUIRE(!(hf & 1), STB_ERR_ARG, "rho must be positive");
+      STB_REQUIRE(!(hf & 2), STB_ERR_ARG, "mu must be non-negative");
+      STB_REQUIRE(!(hf & 4), STB_ERR_ARG, "lam + 2*mu must be positive");
+      if (desc.vp) {
+        const long long b = hk >= 0 ? hk : hk ^ 0x7fffffffffffffffLL;
+        double vm;
+        std::memcpy(&vm, &b, sizeof(vm));
+        vmax_ = (hf & 8) ? NAN : vm;
+      } else {
+        vmax_ = desc.vp_scalar;
+      }
+    } else if (any_arr) {
       DevBuf<double> lam(n), mu(n), rho(n);
       auto fill = [&](DevBuf<double>& b, const double* h, double s) {
         if (h) {
@@ -324,17 +418,7 @@ class ElasticProp final : public stb_prop_s {
       cf_.lam = (T)(dt * desc.lam_scalar);
       cf_.mu = (T)(dt * desc.mu_scalar);
     }
-    has_fac_ = desc.damp[0] || desc.damp[1] || desc.damp[2];
-    const int64_t n3[3] = {d_.nx, d_.ny, d_.nz};
-    for (int a = 0; a < 3; ++a) {
-      fac_[a].alloc(n3[a]);
-      DevBuf<double> tmp(desc.damp[a] ? n3[a] : 0);
-      if (desc.damp[a]) tmp.upload(desc.damp[a] + (a == 0 ? x_begin_ : 0), n3[a], st_);
-      pad_table_kernel<T><<<g1(n3[a]), 256, 0, st_>>>(desc.damp[a] ? tmp.p : nullptr, n3[a],
-                                                     fac_[a].p);
-      STB_CHECK_LAUNCH();
-      STB_CUDA(cudaStreamSynchronize(st_));
-    }
+    set_damping(desc.damp);
     // TMA-tiled sweeps (elastic_tiled.cuh): f32, 3-D, R <= 4
     tiled_ = sizeof(T) == 4 && cf_.active[0] && cf_.active[1] && cf_.active[2] && R_ <= 4;
     if (const char* e = std::getenv("STB_ELASTIC_PATH")) tiled_ = tiled_ && std::string(e) != "point";
@@ -342,6 +426,23 @@ class ElasticProp final : public stb_prop_s {
     STB_REQUIRE(d_.total < (int64_t)INT32_MAX, STB_ERR_ARG,
                 "elastic slab too large for 32-bit offsets; use more x slabs");
   }
+
+  // sponge tables (also after creation: stb_prop_set_damping)
+  void set_damping(const double* const* damp) override {
+    has_fac_ = damp[0] || damp[1] || damp[2];
+    const int64_t n3[3] = {d_.nx, d_.ny, d_.nz};
+    for (int a = 0; a < 3; ++a) {
+      if (!fac_[a].p) fac_[a].alloc(n3[a]);
+      DevBuf<double> tmp(damp[a] ? n3[a] : 0);
+      if (damp[a]) tmp.upload(damp[a] + (a == 0 ? x_begin_ : 0), n3[a], st_);
+      pad_table_kernel<T><<<g1(n3[a]), 256, 0, st_>>>(damp[a] ? tmp.p : nullptr, n3[a],
+                                                     fac_[a].p);
+      STB_CHECK_LAUNCH();
+      STB_CUDA(cudaStreamSynchronize(st_));
+    }
+  }
+
+  double velocity_max() const override { return vmax_; }
 
   ~ElasticProp() override {
     // drain in-flight work: buffers are freed on stream 0, which a
@@ -777,6 +878,7 @@ class ElasticProp final : public stb_prop_s {
   }
 
   int R_ = 1;
+  double vmax_ = NAN;        // max(vp) when the device formed the materials
   PDims d_{};
   stb_geometry geom_{};
   int64_t x_begin_ = 0;

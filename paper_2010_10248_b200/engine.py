@@ -503,14 +503,19 @@ def build_propagator(config: RunConfig, dt: float, v_max: float | None, x_begin:
     vp = np.asarray(config.medium["vp"], dtype=np.float64)
     vs = np.asarray(config.medium["vs"], dtype=np.float64)
     rho = np.asarray(config.medium["rho"], dtype=np.float64)
-    mu = rho * vs ** 2
-    lam = rho * vp ** 2 - 2.0 * mu
-    if np.any(rho <= 0.0):
-        raise ValueError("rho must be positive")
-    if np.any(mu < 0.0):
-        raise ValueError("mu must be non-negative")
-    if np.any(lam + 2.0 * mu <= 0.0):
-        raise ValueError("lam + 2*mu must be positive")
+    # array media: the device forms lam/mu from vp/vs/rho in f64 with the
+    # same operations (engine.py:247-255) and runs the checks
+    # (physics.py:229-236); scalars are folded here
+    on_device = vp.ndim > 0 or vs.ndim > 0 or rho.ndim > 0
+    if not on_device:
+        mu = rho * vs ** 2
+        lam = rho * vp ** 2 - 2.0 * mu
+        if np.any(rho <= 0.0):
+            raise ValueError("rho must be positive")
+        if np.any(mu < 0.0):
+            raise ValueError("mu must be non-negative")
+        if np.any(lam + 2.0 * mu <= 0.0):
+            raise ValueError("lam + 2*mu must be positive")
     d = _lib.ElasticDesc()
     d.geom = _lib.geometry(grid)
     d.space_order, d.precision, d.dt = config.space_order, config.precision, dt
@@ -520,7 +525,12 @@ def build_propagator(config: RunConfig, dt: float, v_max: float | None, x_begin:
         d.active[a] = int(grid.shape[a] > 1)
         for j in range(8):
             d.d1[a][j] = d1[a, j]
-    for name, arr in (("lam", lam), ("mu", mu), ("rho", rho)):
+    if on_device:
+        d.from_velocities = 1
+        mats = (("vp", vp), ("vs", vs), ("rho", rho))
+    else:
+        mats = (("lam", lam), ("mu", mu), ("rho", rho))
+    for name, arr in mats:
         if arr.ndim == 0:
             setattr(d, f"{name}_scalar", float(arr))
         else:
@@ -534,6 +544,8 @@ def build_propagator(config: RunConfig, dt: float, v_max: float | None, x_begin:
         for a in range(3):
             keep.append(tables[a])
             d.damp[a] = _lib.dptr(tables[a])
+    if host_done is not None:       # host-side prep finished (see the acoustic path)
+        host_done.set()
     raw = C.c_void_p()
     _lib.check(_lib.lib().stb_elastic_create(C.byref(d), C.byref(raw)))
     return _Prop(raw, config.dtype, ELASTIC_FIELDS)
@@ -758,7 +770,7 @@ def run(config: RunConfig) -> RunResult:
         from .multi import run_multi
         return run_multi(config, devices)
     grid = config.grid
-    vkey = {"acoustic": "velocity", "tti": "vp"}.get(config.physics)
+    vkey = {"acoustic": "velocity", "tti": "vp", "elastic": "vp"}.get(config.physics)
     overlap = (vkey is not None and config.dt is not None and config.nt is not None
                and vkey in config.medium and np.ndim(config.medium[vkey]) > 0)
     src_prep = None
@@ -779,7 +791,7 @@ def run(config: RunConfig) -> RunResult:
                         pass
                 # acoustic: the kernel forming inv reduces max(v) on the
                 # device; TTI reads it here
-                device_vmax = config.physics == "acoustic"
+                device_vmax = config.physics in ("acoustic", "elastic")
                 v_max = (None if device_vmax else
                          medium_velocity_bounds(config.physics, config.medium))
                 src_prep = _host_sparse_prep(config, dt, nt)

@@ -124,7 +124,7 @@ def test_repeat_determinism():
     assert a.report.checksum == b.report.checksum
 
 
-@pytest.mark.parametrize("physics", ["acoustic", "tti"])
+@pytest.mark.parametrize("physics", ["acoustic", "tti", "elastic"])
 def test_overlapped_setup_matches_sequential(physics):
     """run() with dt and nt given uploads the model while the host computes
     v_max and checks the sparse inputs, and supplies the sponge tables
@@ -138,6 +138,10 @@ def test_overlapped_setup_matches_sequential(physics):
         medium = {"vp": v, "epsilon": 0.2 * rng.random(shape), "delta": 0.05,
                   "theta": 0.3 * rng.random(shape), "phi": 0.2}
         so_ = 8
+    elif physics == "elastic":
+        # lam/mu formed on the device from vp/vs/rho; max(vp) from the device
+        medium = {"vp": v, "vs": v / 1.8, "rho": 1900.0 + 400.0 * rng.random(shape)}
+        so_ = 4
     else:
         medium = {"velocity": v}
         so_ = 4
@@ -152,6 +156,28 @@ def test_overlapped_setup_matches_sequential(physics):
     for k in seq.fields:
         np.testing.assert_array_equal(ovl.fields[k], seq.fields[k])
     np.testing.assert_array_equal(ovl.receivers, seq.receivers)
+
+
+def test_elastic_medium_errors_from_device_checks():
+    """physics.py:229-236's checks run on the device when lam/mu are formed
+    there: same exception type and message as the reference."""
+    shape = (12, 10, 11)
+    grid = stb.GridSpec(shape, (10.0,) * 3)
+    vp = np.full(shape, 3000.0)
+
+    def cfg(**m):
+        med = {"vp": vp, "vs": vp / 1.7, "rho": np.full(shape, 2000.0)}
+        med.update(m)
+        return stb.RunConfig(physics="elastic", grid=grid, space_order=4, nt=3, dt=1e-4,
+                             medium=med)
+    bad_rho = np.full(shape, 2000.0)
+    bad_rho[3, 4, 5] = 0.0
+    with pytest.raises(ValueError, match="rho must be positive"):
+        stb.run(cfg(rho=bad_rho))
+    bad_vp = vp.copy()
+    bad_vp[1, 1, 1] = 0.0
+    with pytest.raises(ValueError, match="lam \\+ 2\\*mu must be positive"):
+        stb.run(cfg(vp=bad_vp, vs=np.zeros(shape)))
 
 
 def test_in_run_k_measurement_picks_blocking_at_so2():
