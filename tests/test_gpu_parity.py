@@ -554,11 +554,20 @@ def test_async_api_errors():
     with pytest.raises(ValueError):
         prop.step_async(0, 1, 0, 10 ** 6)           # plane range
     prop.async_finish()
+    with pytest.raises(ValueError):
+        prop.half_step_async(0, 0, 0, 4)            # half steps are elastic-only
     el = to_config(build_case("el_so4_24"), stb)
     vmax = medium_velocity_bounds(el.physics, el.medium)
     dt, _ = resolve_steps(el, vmax)
+    ep = build_propagator(el, dt, vmax)
+    ep.async_begin(0, 2)                            # elastic slabs run async too
+    with pytest.raises(stb.InvalidPlanError):
+        ep.step_async(0, 2, 0, 4)                   # one step per pass
     with pytest.raises(ValueError):
-        build_propagator(el, dt, vmax).async_begin(0, 2)
+        ep.half_step_async(0, 2, 0, 4)              # phase is 0 (v) or 1 (tau)
+    ep.half_step_async(0, 0, 0, 24)
+    ep.half_step_async(0, 1, 0, 24)
+    ep.async_finish()
 
 
 @pytest.mark.parametrize("field", [None, "vx", "vz"])
