@@ -47,24 +47,6 @@ __global__ void gather_kernel(const T* __restrict__ u, const int64_t* __restrict
   out_row[r] = pairwise8<T>(ww, v);
 }
 
-// Gather from captured corner values: cap[m] holds u at capture point m,
-// cidx[r*8+c] the capture index of receiver r's corner c.
-template <typename T>
-__global__ void gather_captured_kernel(const T* __restrict__ cap, const int32_t* __restrict__ cidx,
-                                       const double* __restrict__ w, int64_t nrec,
-                                       double* __restrict__ out_row) {
-  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= nrec) return;
-  T v[8];
-  double ww[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    v[c] = cap[cidx[r * 8 + c]];
-    ww[c] = w[r * 8 + c];
-  }
-  out_row[r] = pairwise8<T>(ww, v);
-}
-
 // Non-finite detection (engine.py:354-360) over a pitched interior.
 template <typename T>
 __global__ void nonfinite_kernel(const T* __restrict__ u, Dims d, int* flag) {

@@ -1,4 +1,4 @@
-"""fp64 acoustic so=8 on the cfg2 grid: 2.5-D sweep vs thread-per-point."""
+"""fp64 acoustic on the cfg2 grid (thread-per-point kernel), GPts/s per order."""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -6,9 +6,7 @@ import bench  # noqa: E402
 import paper_2010_10248_b200 as stb  # noqa: E402
 from paper_2010_10248_b200 import slabs  # noqa: E402
 v, src, rec = bench.cfg2_inputs()
-for path in ("sweep", "reference"):
-    if path == "reference":
-        os.environ["STB_PATH"] = "reference"
+for path in ("reference",):
     for so in (4, 8, 16):
         cfg = bench.make_config(stb, v, src, rec, 24, 1)
         cfg.space_order, cfg.precision = so, 64
