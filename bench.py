@@ -158,6 +158,17 @@ def cfg5_inputs(seed: int = 5, nx: int | None = None):
     return medium, src, rec
 
 
+def workload_config(workload: str, world: int) -> dict:
+    """The workload description both arms print (implementation details of
+    this repo's arm go to its "impl_detail")."""
+    shape = workload_shape(workload)
+    return {"workload": WORKLOAD_TEXT[workload], "grid": list(shape),
+            "parallelism": f"x-slab{world}",
+            "l2": f"inputs larger than L2 (each {shape[0]}^3 f32 field "
+                  f"~{4 * shape[0] ** 3 / 1e9:.2f} GB >> 126 MB)",
+            "gpts_counting": "computational grid incl. sponge (engine.py:445-447)"}
+
+
 def workload_metric(workload: str) -> str:
     return {"cfg4": METRIC_TTI, "cfg5": METRIC_EL}.get(workload, METRIC)
 
@@ -435,7 +446,7 @@ def run_reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * elapsed / max(steps, 1), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD_TEXT[args.workload], "grid": list(shape)},
+        "config": workload_config(args.workload, args.gpus),
         "cpu_baseline": {"value": gps, "unit": "GPts/s", "cores": threads, "kind": "port",
                          **host_cpu_info(),
                          "sample": f"{steps} time steps of {args.workload} on its first "
@@ -605,15 +616,11 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD_TEXT[wl],
-                       "grid": list(shape), "time_height": k_used,
-                       "arithmetic": args.arithmetic,
-                       "parallelism": f"x-slab{world}",
-                       "l2": "inputs larger than L2 (each 592^3 f32 field ~0.85 GB >> 126 MB)",
-                       "gpts_counting": "computational grid incl. sponge (engine.py:445-447)",
-                       "value_physical": ((shape[0] - 2 * BL) ** 3 * args.steps
-                                          / (t_ms / 1e3) / 1e9),
-                       "kernel": describe},
+            "config": workload_config(wl, world),
+            "impl_detail": {"time_height": k_used, "arithmetic": args.arithmetic,
+                            "kernel": describe,
+                            "value_physical": ((shape[0] - 2 * BL) ** 3 * args.steps
+                                               / (t_ms / 1e3) / 1e9)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": st["launches"], "clocks": clocks,
         }
