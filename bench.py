@@ -568,6 +568,10 @@ def main():
     torch.cuda.synchronize()
     if not args.no_e2e and world == 1:
         cfg_e = make_config(stb, v, src, rec, args.steps, args.k, args.arithmetic, wl)
+        # one untimed call first (first-use costs: host staging buffers,
+        # tensor maps, kernel attributes), then the timed one
+        del stb.run(make_config(stb, v, src, rec, min(args.steps, 8), args.k, args.arithmetic,
+                                wl)).fields
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = stb.run(cfg_e)
