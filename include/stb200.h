@@ -274,6 +274,21 @@ int stb_prop_step_async(stb_prop_t p, int64_t t, int32_t kb, int64_t x_lo, int64
  * [x_lo, x_hi), so R ghost planes of the half step's fields can be exchanged
  * between the halves (step_async runs both). */
 int stb_prop_half_step_async(stb_prop_t p, int64_t t, int32_t phase, int64_t x_lo, int64_t x_hi);
+/* Fused halo exchange (x slabs, one process driving several GPUs with peer
+ * access): the K = 1 step over [x_lo, x_hi) also stores its boundary planes
+ * straight into the neighbours' ghost planes over NVLink -- local plane
+ * p < lo_end goes to `lo` (the lower neighbour's level-t buffer, from its
+ * stb_prop_level_ptr) at its local plane p + lo_shift; p >= hi_begin to
+ * `hi` at p + hi_shift.  NULL pointers: no neighbour on that side.  The
+ * caller orders the neighbours' next launches after this one (events). */
+typedef struct {
+  void* lo;
+  int64_t lo_end, lo_shift;
+  void* hi;
+  int64_t hi_begin, hi_shift;
+} stb_peer_halo;
+int stb_prop_step_async_peers(stb_prop_t p, int64_t t, int64_t x_lo, int64_t x_hi,
+                              const stb_peer_halo* peers);
 int stb_prop_gather_async(stb_prop_t p, int64_t t, int32_t kb);
 int stb_prop_async_finish(stb_prop_t p, double* rec_out, int64_t* bad_step);
 /* Zero all time levels (reuse a handle for another shot). */

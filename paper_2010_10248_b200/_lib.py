@@ -32,7 +32,7 @@ EXPORTS = (
     "stb_elastic_create", "stb_tti_create", "stb_prop_set_sources", "stb_prop_set_receivers", "stb_prop_run",
     "stb_prop_read_field", "stb_prop_level_ptr", "stb_prop_write_snapshot", "stb_prop_stream", "stb_prop_async_begin", "stb_prop_set_receiver_field",
     "stb_prop_set_damping",
-    "stb_prop_step_async", "stb_prop_half_step_async", "stb_prop_gather_async", "stb_prop_async_finish", "stb_prop_reset", "stb_prop_stats",
+    "stb_prop_step_async", "stb_prop_step_async_peers", "stb_prop_half_step_async", "stb_prop_gather_async", "stb_prop_async_finish", "stb_prop_reset", "stb_prop_stats",
     "stb_prop_describe",
     "stb_prop_max_time_height", "stb_prop_velocity_max",
     "stb_prop_destroy",
@@ -65,6 +65,12 @@ class ElasticDesc(C.Structure):
                 ("nx_local", C.c_int64), ("from_velocities", C.c_int32),
                 ("vp", C.POINTER(C.c_double)), ("vs", C.POINTER(C.c_double)),
                 ("vp_scalar", C.c_double), ("vs_scalar", C.c_double)]
+
+
+class PeerHalo(C.Structure):
+    """stb_peer_halo: fused x-slab halo stores into the neighbours' ghosts."""
+    _fields_ = [("lo", C.c_void_p), ("lo_end", C.c_int64), ("lo_shift", C.c_int64),
+                ("hi", C.c_void_p), ("hi_begin", C.c_int64), ("hi_shift", C.c_int64)]
 
 
 class Layout(C.Structure):
@@ -126,6 +132,7 @@ def _declare(lib):
         "stb_prop_async_begin": ([P, i64, i64], C.c_int),
         "stb_prop_step_async": ([P, i64, i32, i64, i64], C.c_int),
         "stb_prop_half_step_async": ([P, i64, i32, i64, i64], C.c_int),
+        "stb_prop_step_async_peers": ([P, i64, i64, i64, C.POINTER(PeerHalo)], C.c_int),
         "stb_prop_gather_async": ([P, i64, i32], C.c_int),
         "stb_prop_async_finish": ([P, pdbl, pi64], C.c_int),
         "stb_prop_reset": ([P], C.c_int),

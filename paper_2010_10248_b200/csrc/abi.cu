@@ -263,6 +263,14 @@ STB_API int stb_prop_half_step_async(stb_prop_t p, int64_t t, int32_t phase, int
   })
 }
 
+STB_API int stb_prop_step_async_peers(stb_prop_t p, int64_t t, int64_t x_lo, int64_t x_hi,
+                                      const stb_peer_halo* peers) {
+  STB_GUARD({
+    STB_REQUIRE(p != nullptr && peers != nullptr, STB_ERR_ARG, "NULL argument");
+    p->step_async_peers(t, x_lo, x_hi, peers);
+  })
+}
+
 STB_API int stb_prop_gather_async(stb_prop_t p, int64_t t, int32_t kb) {
   STB_GUARD({
     STB_REQUIRE(p != nullptr, STB_ERR_ARG, "NULL handle");

@@ -741,6 +741,21 @@ class AcousticProp final : public stb_prop_s {
   }
 
   // steps [t, t + kb) over local planes [x_lo, x_hi) (stencil + fused injection)
+  // K = 1 step over local planes [x_lo, x_hi) whose boundary planes are
+  // also written into the neighbour slabs' ghost planes (peer memory)
+  void step_async_peers(int64_t t, int64_t x_lo, int64_t x_hi, const stb_peer_halo* peers) override {
+    STB_REQUIRE(path_ == Path::Fused, STB_ERR_ARG, "peer halo stores need the fused path");
+    peers_ = *peers;
+    peers_on_ = true;
+    try {
+      step_async(t, 1, x_lo, x_hi);
+    } catch (...) {
+      peers_on_ = false;
+      throw;
+    }
+    peers_on_ = false;
+  }
+
   void step_async(int64_t t, int kb, int64_t x_lo, int64_t x_hi) override {
     STB_REQUIRE(as_open_, STB_ERR_ARG, "async_begin first");
     STB_REQUIRE(t >= as_t0_ && kb >= 1 && t + kb <= as_t0_ + as_n_, STB_ERR_ARG,
@@ -1048,6 +1063,14 @@ class AcousticProp final : public stb_prop_s {
     FusedArgs a = common_args(t, x_lo, x_hi, cx, gflag, gmask);
     a.out_km1 = nullptr;
     a.out_k = reinterpret_cast<float*>(lvl_[slot(t)].p);
+    if (peers_on_) {
+      a.peer_lo = static_cast<float*>(peers_.lo);
+      a.peer_hi = static_cast<float*>(peers_.hi);
+      a.peer_lo_end = (int)peers_.lo_end;
+      a.peer_hi_begin = (int)peers_.hi_begin;
+      a.peer_lo_shift = (int)peers_.lo_shift;
+      a.peer_hi_shift = (int)peers_.hi_shift;
+    }
     if (K_) {
       const ThrLists* tl = thr_lists<R, 1>();
       a.thr_ptr = tl ? tl->ptr.p : nullptr;
@@ -1169,6 +1192,8 @@ class AcousticProp final : public stb_prop_s {
   Dims d_{};
   // async stepping state
   bool as_open_ = false;
+  bool peers_on_ = false;         // the next K = 1 launch stores into peer ghosts
+  stb_peer_halo peers_{};
   int64_t as_t0_ = 0, as_n_ = 0;
   std::vector<int64_t> as_guard_;
   stb_geometry geom_{};          // GLOBAL grid geometry

@@ -119,6 +119,14 @@ struct FusedArgs {
   int n_src;
   int* nonfinite;
   int guard_mask;        // bit j-1: step t0+j-1 is a guard step
+  // x-slab halo exchange fused into the K = 1 sweep: owned planes p <
+  // peer_lo_end (p >= peer_hi_begin) are also stored, over NVLink peer
+  // memory, into the lower (upper) neighbour slab's ghost planes at its
+  // local plane p + peer_lo_shift (p + peer_hi_shift).  NULL: no peer.
+  float* peer_lo;
+  float* peer_hi;
+  int peer_lo_end, peer_hi_begin;
+  int peer_lo_shift, peer_hi_shift;
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
@@ -491,8 +499,18 @@ acoustic_fused(const __grid_constant__ FusedMaps maps, const __grid_constant__ F
             if constexpr (K <= 2) {
               if (work && tile_owner && p >= x0 && p < x1) {
                 float* dst = (K == 1) ? a.out_k : a.out_km1;
-                *reinterpret_cast<float4*>(dst + (int64_t)p * a.d.plane + gbase) =
-                    make_float4(o[0], o[1], o[2], o[3]);
+                const float4 v4 = make_float4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<float4*>(dst + (int64_t)p * a.d.plane + gbase) = v4;
+                if constexpr (K == 1) {
+                  // fused halo exchange: the boundary planes go straight into
+                  // the neighbours' ghost zones (plane-uniform branches)
+                  if (a.peer_lo && p < a.peer_lo_end)
+                    *reinterpret_cast<float4*>(
+                        a.peer_lo + (int64_t)(p + a.peer_lo_shift) * a.d.plane + gbase) = v4;
+                  if (a.peer_hi && p >= a.peer_hi_begin)
+                    *reinterpret_cast<float4*>(
+                        a.peer_hi + (int64_t)(p + a.peer_hi_shift) * a.d.plane + gbase) = v4;
+                }
               }
             }
           }

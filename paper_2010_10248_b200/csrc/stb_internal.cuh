@@ -221,6 +221,9 @@ struct stb_prop_s {
   virtual void set_damping(const double* const*) { throw_unsupported(); }
   virtual void async_begin(int64_t, int64_t) { throw_unsupported(); }
   virtual void step_async(int64_t, int, int64_t, int64_t) { throw_unsupported(); }
+  virtual void step_async_peers(int64_t, int64_t, int64_t, const stb_peer_halo*) {
+    throw_unsupported();
+  }
   // elastic: one half step (0 = v, 1 = tau + injection) over local planes
   virtual void half_step_async(int64_t, int, int64_t, int64_t) { throw_unsupported(); }
   virtual void gather_async(int64_t, int) { throw_unsupported(); }

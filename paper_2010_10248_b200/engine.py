@@ -381,6 +381,15 @@ class _Prop:
     def step_async(self, t, kb, x_lo, x_hi):
         _lib.check(_lib.lib().stb_prop_step_async(self.raw, t, kb, x_lo, x_hi))
 
+    def step_async_peers(self, t, x_lo, x_hi, peers):
+        _lib.check(_lib.lib().stb_prop_step_async_peers(self.raw, t, x_lo, x_hi, C.byref(peers)))
+
+    def level_address(self, field: int, t: int) -> int:
+        dev, plane, pitch = C.c_void_p(), C.c_int64(), C.c_int64()
+        _lib.check(_lib.lib().stb_prop_level_ptr(self.raw, field, t, C.byref(dev),
+                                                 C.byref(plane), C.byref(pitch)))
+        return int(dev.value or 0)
+
     def half_step_async(self, t, phase, x_lo, x_hi):
         _lib.check(_lib.lib().stb_prop_half_step_async(self.raw, t, phase, x_lo, x_hi))
 

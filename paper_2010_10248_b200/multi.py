@@ -7,11 +7,15 @@ here.  The grid is split in x-slabs exactly as the torchrun path does
 receiver ownership), but one host thread drives every slab handle and the
 halo exchange is a device-to-device copy over NVLink (peer access, enabled
 by torch on the first cross-device copy) instead of NCCL send/recv.  Nothing
-in the step loop waits on the host: per step every slab enqueues its owned-
-plane launch on its own library stream, the R planes next to each slab
-boundary are copied between the neighbouring slabs' streams (events order
-the copy after the source's launch and the source's next write after the
-copy), then the receiver gathers.  Results are bitwise those of the
+in the step loop waits on the host.  Acoustic k = 1 (the default) fuses the
+exchange into the stencil kernel: each slab's launch also stores the R
+boundary planes it computes straight into its neighbours' ghost planes over
+peer memory (`stb_prop_step_async_peers`), so a step is one launch per GPU
+and an event wait per neighbour -- no separate transfer.  Otherwise the R
+planes next to each slab boundary are copied between the neighbouring
+slabs' streams after the launches (events order each copy after the
+source's launch and the source's next write after the copy).  Then the
+receiver gathers.  Results are bitwise those of the
 single-device run: no arithmetic crosses a slab boundary.
 
 ``devices`` (default ``range(n_gpus)``) may repeat a device: several slabs on
@@ -57,6 +61,9 @@ class PeerSlabs:
         self.nf = len(lead.field_names)
         self.streams = [torch.cuda.ExternalStream(rr.dev.stream_ptr(), device=d)
                         for rr, d in zip(self.runners, self.devices)]
+        import os
+        self.fused_halo = (config.physics == "acoustic" and len(self.runners) > 1
+                           and os.environ.get("STB_PEER_FUSED", "1") != "0")
 
     # ------------------------------------------------------------ plumbing
     def _bind(self, r):
@@ -113,6 +120,37 @@ class PeerSlabs:
                 if 0 <= peer < n and copied[peer] is not None:
                     self.streams[r].wait_event(copied[peer])
 
+    def _fused_step(self, t, spans):
+        """One K = 1 step on every slab with the halo exchange inside the
+        kernel: boundary planes are stored into the neighbours' level-t
+        ghost planes; each slab then waits for both neighbours' launches
+        before its gather and its next step."""
+        import torch
+        n, R = len(self.runners), self.R
+        done = []
+        for r, rr in enumerate(self.runners):
+            self._bind(r)
+            ph = _lib.PeerHalo()
+            a_loc, b_loc = spans[r]
+            if r > 0:
+                nb = self.runners[r - 1]
+                ph.lo = nb.dev.level_address(t)
+                ph.lo_end = a_loc + R
+                ph.lo_shift = rr.lo - nb.lo
+            if r < n - 1:
+                nb = self.runners[r + 1]
+                ph.hi = nb.dev.level_address(t)
+                ph.hi_begin = b_loc - R
+                ph.hi_shift = rr.lo - nb.lo
+            rr.dev.step_async_peers(t, a_loc, b_loc, ph)
+            ev = torch.cuda.Event()
+            ev.record(self.streams[r])
+            done.append(ev)
+        for r in range(n):
+            for peer in (r - 1, r + 1):
+                if 0 <= peer < n:
+                    self.streams[r].wait_event(done[peer])
+
     # ------------------------------------------------------------ stepping
     def run(self, t0: int, nsteps: int):
         """Steps [t0, t0 + nsteps) on every slab; returns per-slab traces."""
@@ -128,6 +166,8 @@ class PeerSlabs:
                         self._bind(r)
                         rr.dev.half_step_async(t, phase, *spans[r])
                     self._exchange([t], fields, depth=R)
+            elif kb == 1 and self.fused_halo:
+                self._fused_step(t, spans)
             elif kb == 1:
                 for r, rr in enumerate(self.runners):
                     self._bind(r)
@@ -168,8 +208,9 @@ class PeerSlabs:
         lead = self.runners[0]
         spans = ", ".join(f"[{rr.a},{rr.b})@cuda:{d}" for rr, d in zip(self.runners,
                                                                        self.devices))
-        return (f"{lead.describe()} x-slabs {spans} ghost {self.G} "
-                f"exchange {'R' if self.k == 1 else 'G'}-deep peer copies")
+        how = ("fused into the k=1 kernel (peer stores)" if self.fused_halo and self.k == 1
+               else f"{'R' if self.k == 1 else 'G'}-deep peer copies")
+        return f"{lead.describe()} x-slabs {spans} ghost {self.G} exchange {how}"
 
 
 def run_multi(config, devices):

@@ -120,6 +120,12 @@ class DeviceSlab:
     def half_step_async(self, t, phase, x_lo, x_hi):
         self.prop.half_step_async(t, phase, x_lo, x_hi)
 
+    def step_async_peers(self, t, x_lo, x_hi, peers):
+        self.prop.step_async_peers(t, x_lo, x_hi, peers)
+
+    def level_address(self, t, field=0) -> int:
+        return self.prop.level_address(field, t)
+
     def gather_async(self, t, kb):
         self.prop.gather_async(t, kb)
 

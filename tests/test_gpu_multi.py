@@ -60,3 +60,21 @@ def test_n_gpus_beyond_visible_devices_is_a_config_error():
     n = torch.cuda.device_count() + 1
     with pytest.raises(stb.ConfigError):
         stb.run(to_config(case, stb, schedule=stb.ScheduleSpec("gpu", n_gpus=n)))
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_multi_slab_acoustic_halo_fused_into_kernel(fused, monkeypatch):
+    """Acoustic k = 1 across slabs with the halo exchange fused into the
+    stencil kernel (boundary planes stored into the neighbours' ghost planes
+    by the launch itself) and with separate peer copies: both bitwise equal
+    to the single-device run, 2 and 4 slabs, dense sources and receivers."""
+    monkeypatch.setenv("STB_PEER_FUSED", fused)
+    case = build_case("ac_dense_src")
+    ref = stb.run(to_config(case, stb))
+    for nslab in (2, 4):
+        res = stb.run(to_config(case, stb, schedule=stb.ScheduleSpec("gpu", time_height=1,
+                                                                     devices=(0,) * nslab)))
+        plan = res.report.schedule["device_plan"]
+        assert ("peer stores" in plan) == (fused == "1")
+        _same(res, ref)
+
