@@ -21,7 +21,9 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <sstream>
 #include <unordered_map>
 
@@ -244,6 +246,16 @@ __global__ void wtb_key_kernel(const int4* __restrict__ list, const int* __restr
     val[2 * i + 1] = make_int2(0, 0);
   }
 }
+
+// k measured by time_height = 0, remembered per (device, grid, order,
+// arithmetic, medium kind) for the process: a second handle on the same
+// configuration (a repeated run(), every shot of a survey) skips the trial.
+struct KChoice {
+  int k;
+  float ms1, ms2;
+};
+std::mutex g_kcache_mu;
+std::map<std::string, KChoice> g_kcache;
 
 constexpr int NB = 6;
 #ifndef STB_WTB_RY
@@ -584,6 +596,17 @@ class AcousticProp final : public stb_prop_s {
     // very run (K = 1, 1, 2, 2 -- real steps, the second of each kind timed
     // after its first-use costs) and continue with the faster; short runs
     // use the separate idempotent trial (autotune_k)
+    const bool pinned_k = std::getenv("STB_DEFAULT_K") ||
+                          (std::getenv("STB_AUTOTUNE") && std::atoi(std::getenv("STB_AUTOTUNE")) == 0);
+    if (k == 0 && !tuned_k_ && path_ == Path::Fused && max_k_ >= 2 && !pinned_k) {
+      std::lock_guard<std::mutex> lk(g_kcache_mu);
+      auto it = g_kcache.find(kcache_key());
+      if (it != g_kcache.end()) {
+        tuned_k_ = it->second.k;
+        tune_ms_[0] = it->second.ms1;
+        tune_ms_[1] = it->second.ms2;
+      }
+    }
     bool trial = k == 0 && !tuned_k_ && path_ == Path::Fused && max_k_ >= 2 && nsteps >= 6 &&
                  !std::getenv("STB_DEFAULT_K") &&
                  !(std::getenv("STB_AUTOTUNE") && std::atoi(std::getenv("STB_AUTOTUNE")) == 0);
@@ -677,6 +700,7 @@ class AcousticProp final : public stb_prop_s {
         tune_ms_[0] = m1;
         tune_ms_[1] = m2 / 2;
         tuned_k_ = tune_ms_[1] < 0.95f * tune_ms_[0] ? 2 : 1;
+        remember_k();
         kk = resolve_k(0);
         trial = false;
       }
@@ -939,6 +963,20 @@ class AcousticProp final : public stb_prop_s {
     tune_ms_[0] = m1 / kReps;                   // per step
     tune_ms_[1] = m2 / kReps / 2;
     tuned_k_ = tune_ms_[1] < 0.95f * tune_ms_[0] ? 2 : 1;
+    remember_k();
+  }
+
+  std::string kcache_key() const {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::ostringstream os;
+    os << dev << ':' << d_.nx << 'x' << d_.ny << 'x' << d_.nz << ":R" << R_ << ":f" << fast_
+       << ":i" << (inv_.p != nullptr) << ":s" << (K_ > 0);
+    return os.str();
+  }
+  void remember_k() {
+    std::lock_guard<std::mutex> lk(g_kcache_mu);
+    g_kcache[kcache_key()] = KChoice{tuned_k_, tune_ms_[0], tune_ms_[1]};
   }
 
   // x-chunk length for a launch over L planes: minimise waves x iterations,
