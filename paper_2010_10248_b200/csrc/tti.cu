@@ -54,6 +54,7 @@ struct TtiCoefs {
 }  // namespace stb
 
 #include "tti_fused.cuh"
+#include "tti_fused2.cuh"
 
 namespace stb {
 namespace {
@@ -263,7 +264,11 @@ class TtiProp final : public stb_prop_s {
     fast_ = desc.arithmetic == 1;
     STB_REQUIRE(!fast_ || fused_, STB_ERR_CONFIG,
                 "schedule.arithmetic: 'fma' needs the fused f32 3-D TTI kernel");
-    if (const char* e = std::getenv("STB_TTI_PATH")) fused_ = fused_ && std::string(e) != "twopass";
+    if (const char* e = std::getenv("STB_TTI_PATH")) {
+      fused_ = fused_ && std::string(e) != "twopass";
+      pair_ = std::string(e) != "fused1";
+    }
+    pair_ = pair_ && fused_ && r_ <= 2;
     for (int ax = 0; ax < 3 && !fused_; ++ax) {
       if (!cf_.active[ax]) continue;
       F_[ax].alloc(d_.total);
@@ -652,10 +657,15 @@ class TtiProp final : public stb_prop_s {
     std::ostringstream os;
     if (fused_) {
       const int bpp = (int)sizeof(T) * (2 + 2 + 2 + nmat);
-      os << "tti_fused<f32,r=" << r_ << ",ring=" << m_for_r(r_) << "x" << (2 * r_ + 1)
-         << "," << (fast_ ? "fma" : "exact")
-         << "> (TMA p/q plane ring, 16x32 tile, x chunk " << cx_
-         << ", F/G on chip) k=1 requested_k=" << k << " bytes_per_point=" << bpp;
+      if (pair_)
+        os << "tti_fused2<f32,r=" << r_ << "," << (fast_ ? "fma" : "exact")
+           << "> (TMA p/q plane ring + operand ring, 16x32 tile as z pairs, halo warps, FG ring, x chunk "
+           << cx_ << ") k=1 requested_k=" << k << " bytes_per_point=" << bpp;
+      else
+        os << "tti_fused<f32,r=" << r_ << ",ring=" << m_for_r(r_) << "x" << (2 * r_ + 1)
+           << "," << (fast_ ? "fma" : "exact")
+           << "> (TMA p/q plane ring, 16x32 tile, x chunk " << cx_
+           << ", F/G on chip) k=1 requested_k=" << k << " bytes_per_point=" << bpp;
     } else {
       const int bpp = (int)sizeof(T) * (2 + 2 * na + 2 * na + 4 + 2 + nmat);
       os << "tti_pass1+pass2<" << (sizeof(T) == 4 ? "f32" : "f64") << ",r=" << r_
@@ -671,7 +681,26 @@ class TtiProp final : public stb_prop_s {
   static constexpr int m_for_r(int r) { return r <= 3 ? 2 : 1; }
 
   template <int r>
+  void launch_pair(const TtiFusedArgs& fa, int prev) {
+    using C = Tti2Cfg<r>;
+    dim3 grid((unsigned)((d_.nz + C::TZ - 1) / C::TZ), (unsigned)((d_.ny + C::TY - 1) / C::TY),
+              (unsigned)((fa.x_hi - fa.x_lo + cx_ - 1) / cx_));
+    if (fast_)
+      tti_fused2<r, true><<<grid, C::NT, C::SMEM, st_>>>(maps2_[prev], fa);
+    else
+      tti_fused2<r, false><<<grid, C::NT, C::SMEM, st_>>>(maps2_[prev], fa);
+  }
+
+  template <int r>
   void set_fused_attr() {
+    if constexpr (r <= 2) {
+      STB_CUDA(cudaFuncSetAttribute(tti_fused2<r, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)Tti2Cfg<r>::SMEM));
+      STB_CUDA(cudaFuncSetAttribute(tti_fused2<r, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)Tti2Cfg<r>::SMEM));
+    }
     constexpr int M = m_for_r(r);
     STB_CUDA(cudaFuncSetAttribute(tti_fused<r, M, false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -696,6 +725,23 @@ class TtiProp final : public stb_prop_s {
         maps_[l].p = make_map3d_f32(reinterpret_cast<const float*>(lv_[0][l].p), md, pz, py, 1);
         maps_[l].q = make_map3d_f32(reinterpret_cast<const float*>(lv_[1][l].p), md, pz, py, 1);
       }
+      if (pair_) {
+        // tti_fused2: p/q boxes as above; n boxes over the pass-1 extent,
+        // p/q (t-2) and inv/e2/d2 boxes over the tile
+        const uint32_t ez = kTtiTZ + 2 * ((2 * ((r + 1) / 2) + 3) / 4 * 4), ey = kTtiTY + 2 * r;
+        auto f32p = [](const T* b) { return reinterpret_cast<const float*>(b); };
+        for (int l = 0; l < 2; ++l) {        // l = buffer of level t-1
+          Tti2Maps& m = maps2_[l];
+          m.p = maps_[l].p;
+          m.q = maps_[l].q;
+          for (int ax = 0; ax < 3; ++ax) m.n[ax] = make_map3d_f32(f32p(n_[ax].p), md, ez, ey, 1);
+          m.o[0] = make_map3d_f32(f32p(lv_[0][l ^ 1].p), md, kTtiTZ, kTtiTY, 1);
+          m.o[1] = make_map3d_f32(f32p(lv_[1][l ^ 1].p), md, kTtiTZ, kTtiTY, 1);
+          m.o[2] = make_map3d_f32(f32p(inv_.p), md, kTtiTZ, kTtiTY, 1);
+          m.o[3] = make_map3d_f32(f32p(e2_.p), md, kTtiTZ, kTtiTY, 1);
+          m.o[4] = make_map3d_f32(f32p(d2_.p), md, kTtiTZ, kTtiTY, 1);
+        }
+      }
       switch (r) {
         case 1: set_fused_attr<1>(); break;
         case 2: set_fused_attr<2>(); break;
@@ -711,6 +757,12 @@ class TtiProp final : public stb_prop_s {
     if (fa.x_hi <= fa.x_lo) return;
     dim3 grid((unsigned)((d_.nz + kTtiTZ - 1) / kTtiTZ), (unsigned)((d_.ny + kTtiTY - 1) / kTtiTY),
               (unsigned)((fa.x_hi - fa.x_lo + cx_ - 1) / cx_));
+    if constexpr (r <= 2) {
+      if (pair_) {
+        launch_pair<r>(fa, prev);
+        return;
+      }
+    }
     constexpr int M = m_for_r(r);
     if (fast_)
       tti_fused<r, M, true><<<grid, kTtiThreads, TtiFusedCfg<r, M>::smem_bytes(), st_>>>(
@@ -739,6 +791,7 @@ class TtiProp final : public stb_prop_s {
       fa.x_lo = x_lo;
       fa.x_hi = x_hi;
       fa.nonfinite = A.nonfinite;
+      fa.negz = -0.0f;
       switch (r_) {
         case 1: launch_fused_r<1>(fa, prev); break;
         case 2: launch_fused_r<2>(fa, prev); break;
@@ -766,6 +819,7 @@ class TtiProp final : public stb_prop_s {
 
   int r_ = 1;
   bool fused_ = false;
+  bool pair_ = true;          // tti_fused2 (r <= 2) unless STB_TTI_PATH=fused1
   bool fast_ = false;
   int rec_field_ = 0;        // p
   int cx_ = 150;
@@ -774,6 +828,7 @@ class TtiProp final : public stb_prop_s {
   std::vector<int64_t> as_guard_;
   DevBuf<int> guards_;
   TtiMaps maps_[2];           // [level buffer] p/q tensor maps (fused path)
+  Tti2Maps maps2_[2];         // [level buffer] tti_fused2's operand maps
   PDims d_{};
   stb_geometry geom_{};
   int64_t x_begin_ = 0;

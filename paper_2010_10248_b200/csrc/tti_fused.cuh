@@ -77,6 +77,7 @@ struct TtiFusedArgs {
   int cx;             // x planes per CTA
   int x_lo, x_hi;     // local output planes of this launch (in cx chunks)
   int* nonfinite;
+  float negz;         // -0.0f, opaque to ptxas (exact packed products, f32x2.cuh)
 };
 
 // Loads issued as volatile asm so the compiler cannot sink them next to

@@ -1,36 +1,35 @@
-"""Summarise an .ncu-rep: headline metrics, stall split, hottest SASS lines.
-usage: python tools/ncu_stalls.py report.ncu-rep [n_top]"""
-import csv, io, subprocess, sys
+"""Per-instruction stall attribution from an ncu source-page CSV
+(ncu -i R --page source --csv --print-source sass): top instructions for one
+stall reason, and the reason totals by opcode."""
+import collections
+import csv
+import sys
 
-rep = sys.argv[1]
-ntop = int(sys.argv[2]) if len(sys.argv) > 2 else 12
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                     text=True).stdout
-rows = list(csv.reader(io.StringIO(raw)))
-h, v = rows[0], rows[2]
-want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-        "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
-        "launch__registers_per_thread", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
-for w in want:
-    if w in h:
-        print(f"{w:60s} {v[h.index(w)]}")
-st = {n: float(v[i] or 0) for i, n in enumerate(h) if n.startswith("smsp__pcsamp_warps_issue_stalled_")
-      and not n.endswith("not_issued")}
-tot = sum(st.values()) or 1
-for n, x in sorted(st.items(), key=lambda t: -t[1])[:8]:
-    print(f"  {n.replace('smsp__pcsamp_warps_issue_stalled_', ''):24s} {100 * x / tot:5.1f} %")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True,
-                     text=True).stdout
-rows = list(csv.reader(io.StringIO(src)))
-h = rows[1]
-ix = {n: i for i, n in enumerate(h)}
-data = rows[2:]
-key = "Warp Stall Sampling (All Samples)"
-top = sorted(range(len(data)), key=lambda j: -int(data[j][ix[key]] or 0))[:ntop]
-kinds = [k for k in h if k.startswith("stall_") and "Not Issued" not in k]
-for j in top:
-    r = data[j]
-    worst = max(kinds, key=lambda k: int(r[ix[k]] or 0))
-    print(f"{r[ix[key]]:>7s} {worst:18s} {r[ix['Source']].strip()[:70]}")
+rows = list(csv.reader(open(sys.argv[1])))
+hdr, data = rows[1], rows[2:]
+col = {h: i for i, h in enumerate(hdr)}
+reason = sys.argv[2] if len(sys.argv) > 2 else "stall_long_sb"
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 15
+
+
+def f(r, k):
+    try:
+        return float(r[col[k]] or 0)
+    except ValueError:
+        return 0.0
+
+
+reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+tot = {k: sum(f(r, k) for r in data) for k in reasons}
+all_s = sum(tot.values())
+print("reason totals:", ", ".join(f"{k[6:]} {v / all_s:.1%}" for k, v in
+                                   sorted(tot.items(), key=lambda kv: -kv[1]) if v > 0))
+byop = collections.Counter()
+for r in data:
+    op = r[col["Source"]].split()
+    op = [t for t in op if not t.startswith("@")]
+    byop[op[0].split(".")[0] if op else "?"] += f(r, reason)
+print(f"{reason} by opcode:", ", ".join(f"{k} {v / max(tot[reason], 1):.0%}" for k, v in
+                                        byop.most_common(8)))
+for r in sorted(data, key=lambda r: -f(r, reason))[:n]:
+    print(r[col["Address"]][-5:], f"{f(r, reason) / all_s:6.2%}", r[col["Source"]].strip()[:80])
