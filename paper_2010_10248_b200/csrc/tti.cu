@@ -685,21 +685,26 @@ class TtiProp final : public stb_prop_s {
     using C = Tti2Cfg<r>;
     dim3 grid((unsigned)((d_.nz + C::TZ - 1) / C::TZ), (unsigned)((d_.ny + C::TY - 1) / C::TY),
               (unsigned)((fa.x_hi - fa.x_lo + cx_ - 1) / cx_));
-    if (fast_)
-      tti_fused2<r, true><<<grid, C::NT, C::SMEM, st_>>>(maps2_[prev], fa);
+    const bool g = fa.nonfinite != nullptr;
+    if (fast_ && g)
+      tti_fused2<r, true, true><<<grid, C::NT, C::SMEM, st_>>>(maps2_[prev], fa);
+    else if (fast_)
+      tti_fused2<r, true, false><<<grid, C::NT, C::SMEM, st_>>>(maps2_[prev], fa);
+    else if (g)
+      tti_fused2<r, false, true><<<grid, C::NT, C::SMEM, st_>>>(maps2_[prev], fa);
     else
-      tti_fused2<r, false><<<grid, C::NT, C::SMEM, st_>>>(maps2_[prev], fa);
+      tti_fused2<r, false, false><<<grid, C::NT, C::SMEM, st_>>>(maps2_[prev], fa);
   }
 
   template <int r>
   void set_fused_attr() {
     if constexpr (r <= 2) {
-      STB_CUDA(cudaFuncSetAttribute(tti_fused2<r, false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)Tti2Cfg<r>::SMEM));
-      STB_CUDA(cudaFuncSetAttribute(tti_fused2<r, true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)Tti2Cfg<r>::SMEM));
+      const int sm = (int)Tti2Cfg<r>::SMEM;
+      const auto a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+      STB_CUDA(cudaFuncSetAttribute(tti_fused2<r, false, false>, a, sm));
+      STB_CUDA(cudaFuncSetAttribute(tti_fused2<r, false, true>, a, sm));
+      STB_CUDA(cudaFuncSetAttribute(tti_fused2<r, true, false>, a, sm));
+      STB_CUDA(cudaFuncSetAttribute(tti_fused2<r, true, true>, a, sm));
     }
     constexpr int M = m_for_r(r);
     STB_CUDA(cudaFuncSetAttribute(tti_fused<r, M, false>,

@@ -60,22 +60,23 @@ struct Tti2Cfg {
   static constexpr int NZH = (2 * HZP + 3) / 4 * 4, NEZ = TZ + 2 * NZH;
   static constexpr int NPL = (EY * NEZ + 31) / 32 * 32;
   // operand slot: n_x, n_y, n_z (NPL each), p0, q0, inv, e2, d2 (TPL each), fx
-  static constexpr int NO = 3;
+  static constexpr int NO = 4;
   static constexpr int OBASE = 3 * NPL;
   static constexpr int OSLOT = OBASE + 5 * TPL + 32;
   static constexpr int NCW = TY * P / 32;                     // core warps
   static constexpr int NHY = 2 * r * P, NHZ = TY * 2 * HZP;   // halo pairs
   static constexpr int NHW = (NHY + NHZ + 31) / 32;
   static constexpr int NW = NCW + NHW;                        // consumer warps
-  static constexpr int NT = 32 * (NW + 2);                    // + p/q and operand producers
+  static constexpr int NT = 32 * (NW + 1);                    // + the producer warp
   static constexpr size_t RING = (size_t)2 * NS * SLOT * 4;
   static constexpr size_t FGB = (size_t)4 * NFG * FPL * 4;
   static constexpr size_t OPB = (size_t)NO * OSLOT * 4;
-  static constexpr size_t BARS = (size_t)(2 * NS + 2 * NFG + 2 * NO) * 8;
+  static constexpr size_t BARS = (size_t)(2 * NFG + 2 * NO) * 8;
   static constexpr size_t SMEM = RING + FGB + OPB + BARS + 128;
   static_assert((TY * P) % 32 == 0, "core pairs fill whole warps");
   static_assert(4 * HZP <= ZH, "z windows of the halo pairs stay inside the staged box");
   static_assert(NFG > r, "FG ring holds the planes between pass 1 and pass 2");
+  static_assert(NS >= 2 * r + NO, "a free operand slot implies a free p/q slot");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -136,7 +137,7 @@ __device__ __forceinline__ f2 d1z(const float* c0, const f2* c, f2 nz) {
   return acc;
 }
 
-template <int r, bool FAST>
+template <int r, bool FAST, bool GUARD>
 __global__ void __launch_bounds__(Tti2Cfg<r>::NT, 1)
 tti_fused2(const __grid_constant__ Tti2Maps maps, const __grid_constant__ TtiFusedArgs a) {
   using C = Tti2Cfg<r>;
@@ -146,9 +147,7 @@ tti_fused2(const __grid_constant__ Tti2Maps maps, const __grid_constant__ TtiFus
   float* sp = reinterpret_cast<float*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   float* fg = sp + 2 * NS * C::SLOT;                // [NFG][4 fields][FPL]
   float* opr = fg + 4 * NFG * C::FPL;               // [NO][OSLOT]
-  uint64_t* full = reinterpret_cast<uint64_t*>(opr + NO * C::OSLOT);
-  uint64_t* empty = full + NS;
-  uint64_t* fgfull = empty + NS;
+  uint64_t* fgfull = reinterpret_cast<uint64_t*>(opr + NO * C::OSLOT);
   uint64_t* fgempty = fgfull + NFG;
   uint64_t* ofull = fgempty + NFG;
   uint64_t* oempty = ofull + NO;
@@ -163,10 +162,6 @@ tti_fused2(const __grid_constant__ Tti2Maps maps, const __grid_constant__ TtiFus
   const bool has_fac = a.has_fac != 0;
 
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::NW);
-    }
     for (int g = 0; g < NFG; ++g) {
       mbar_init(&fgfull[g], C::NW * 32);
       mbar_init(&fgempty[g], C::NCW);
@@ -180,24 +175,21 @@ tti_fused2(const __grid_constant__ Tti2Maps maps, const __grid_constant__ TtiFus
   __syncthreads();
 
   // ------------------------------------------------------------ producer
-  // warp NW: p/q planes; warp NW + 1: the operand slot of each iteration
-  if (warp >= C::NW) {
-    const int H = (int)a.d.H, zo = (int)a.d.zoff;
-    if (warp == C::NW && lane == 0) {
+  // One thread, one transaction barrier per iteration i (slot i % NO): the
+  // p/q plane sequence i + 2r (iteration 0 also 0 .. 2r-1), n_x, n_y, n_z
+  // over the pass-1 extent of plane xa, and (output iterations) p, q (t-2),
+  // inv, e2, d2 over the tile at plane xa - r plus fx.  Consumers release
+  // slot i after iteration i; by then they are done with p/q sequence i too,
+  // and NS >= 2r + NO makes a free operand slot imply a free p/q slot.
+  if (warp == C::NW) {
+    if (lane == 0) {
+      const int H = (int)a.d.H, zo = (int)a.d.zoff;
       prefetch_map(&maps.p);
       prefetch_map(&maps.q);
-      const int tc0 = zo + z0 - C::ZH, tc1 = H + y0 - 2 * r;
-      for (int s = 0; s < n_seq; ++s) {
-        const int slot = s % NS;
-        if (s >= NS) mbar_wait_sleep(&empty[slot], (uint32_t)(((s / NS) - 1) & 1));
-        mbar_arrive_expect_tx(&full[slot], 2u * C::PY * C::PZ * 4u);
-        const int xg = H + x0 - 2 * r + s;
-        tma_load_3d(sp + slot * C::SLOT, &maps.p, tc0, tc1, xg, &full[slot]);
-        tma_load_3d(sp + QOFF + slot * C::SLOT, &maps.q, tc0, tc1, xg, &full[slot]);
-      }
-    } else if (warp == C::NW + 1 && lane == 0) {
       for (int k = 0; k < 3; ++k) prefetch_map(&maps.n[k]);
       for (int k = 0; k < 5; ++k) prefetch_map(&maps.o[k]);
+      const int tc0 = zo + z0 - C::ZH, tc1 = H + y0 - 2 * r;
+      constexpr uint32_t pq_bytes = 2u * C::PY * C::PZ * 4u;
       for (int i = 0; i < n_iter; ++i) {
         const int slot = i % NO;
         if (i >= NO) mbar_wait_sleep(&oempty[slot], (uint32_t)(((i / NO) - 1) & 1));
@@ -205,8 +197,16 @@ tti_fused2(const __grid_constant__ Tti2Maps maps, const __grid_constant__ TtiFus
         const int xa = x0 - r + i, x = xa - r;
         const bool out = i >= 2 * r;                // output plane x in [x0, x1)
         if (out) os[C::OBASE + 5 * C::TPL] = has_fac ? __ldg(a.fx + x) : 1.f;
+        const int s0 = i == 0 ? 0 : i + 2 * r;      // p/q sequences of this slot
+        const int s1 = i + 2 * r;
         mbar_arrive_expect_tx(&ofull[slot],
+                              (uint32_t)(s1 - s0 + 1) * pq_bytes +
                               (uint32_t)(3 * C::EY * C::NEZ + (out ? 5 * C::TPL : 0)) * 4u);
+        for (int sq = s0; sq <= s1; ++sq) {
+          const int ps = sq % NS, xg = H + x0 - 2 * r + sq;
+          tma_load_3d(sp + ps * C::SLOT, &maps.p, tc0, tc1, xg, &ofull[slot]);
+          tma_load_3d(sp + QOFF + ps * C::SLOT, &maps.q, tc0, tc1, xg, &ofull[slot]);
+        }
         for (int k = 0; k < 3; ++k)
           tma_load_3d(os + k * C::NPL, &maps.n[k], zo + z0 - C::NZH, H + y0 - r, H + xa,
                       &ofull[slot]);
@@ -281,10 +281,6 @@ tti_fused2(const __grid_constant__ Tti2Maps maps, const __grid_constant__ TtiFus
 #pragma unroll
   for (int j = 0; j < Q; ++j) qF[j] = qG[j] = 0ull;
 
-  // iteration i reads sequences i .. i + 2r and waits for the newest only:
-  // the first window's older planes are waited for here
-  for (int s = 0; s < 2 * r; ++s) mbar_wait(&full[s], 0u);
-
   int os = 0;                                       // operand slot i % NO and its phase
   uint32_t oph = 0;
   bool bad = false;
@@ -293,76 +289,68 @@ tti_fused2(const __grid_constant__ Tti2Maps maps, const __grid_constant__ TtiFus
     const int hc = (k & 1) * Q, hn = Q - hc;
     const float* rc = sp + hc * C::SLOT + soff;
     const float* rn = sp + hn * C::SLOT + soff;
-    const uint32_t pc = (uint32_t)((k >> 1) & 1), pn = (uint32_t)(((k + 1) >> 1) & 1);
     const uint32_t pk_ = (uint32_t)(k & 1);
 #pragma unroll
     for (int u = 0; u < Q; ++u) {
       const int i = i0 + u;
       if (i >= n_iter) break;
       const int xa = x0 - r + i;
-      const int cw = u + 2 * r;                     // newest sequence of the window
-      if (cw < Q) mbar_wait(&full[hc + cw], pc);
-      else mbar_wait(&full[hn + cw - Q], pn);
-      mbar_wait(&ofull[os], oph);
+      mbar_wait(&ofull[os], oph);                   // p/q window and operands of iteration i
       const float* ob = opr + os * C::OSLOT;
 
       // ---- pass 1 at plane xa
-      f2 F[3] = {0ull, 0ull, 0ull}, G[3] = {0ull, 0ull, 0ull};
+      // (computed everywhere; points outside the grid are masked to +0)
+      f2 F[3], G[3];
       f2 p1 = 0ull, q1 = 0ull;
-      if (work) {
+      {
         const float* ps[2 * r + 1];
 #pragma unroll
         for (int dd = 0; dd <= 2 * r; ++dd)
           ps[dd] = (u + dd < Q ? rc : rn) + ((u + dd) % Q) * C::SLOT;
-        if (xa >= 0 && xa < nx && any_in) {
-          const f2 n0 = lds2(ob + noff), n1 = lds2(ob + C::NPL + noff),
-                   n2 = lds2(ob + 2 * C::NPL + noff);
-          f2 gpx = xmul2(sub2(lds2(ps[r + 1]), lds2(ps[r - 1])), cx[0], nzr);
-          f2 gqx = xmul2(sub2(lds2(ps[r + 1] + QOFF), lds2(ps[r - 1] + QOFF)), cx[0], nzr);
+        const f2 m = (xa >= 0 && xa < nx) ? dmask : 0ull;
+        const f2 n0 = lds2(ob + noff), n1 = lds2(ob + C::NPL + noff),
+                 n2 = lds2(ob + 2 * C::NPL + noff);
+        f2 gpx = xmul2(sub2(lds2(ps[r + 1]), lds2(ps[r - 1])), cx[0], nzr);
+        f2 gqx = xmul2(sub2(lds2(ps[r + 1] + QOFF), lds2(ps[r - 1] + QOFF)), cx[0], nzr);
 #pragma unroll
-          for (int kk = 2; kk <= r; ++kk) {
-            gpx = mac2<FAST>(gpx, sub2(lds2(ps[r + kk]), lds2(ps[r - kk])), cx[kk - 1], nzr);
-            gqx = mac2<FAST>(gqx, sub2(lds2(ps[r + kk] + QOFF), lds2(ps[r - kk] + QOFF)),
-                             cx[kk - 1], nzr);
-          }
-          const f2 gpy = d1p<r, FAST>(ps[r], C::PZ, cy, nzr);
-          const f2 gqy = d1p<r, FAST>(ps[r] + QOFF, C::PZ, cy, nzr);
-          const f2 gpz = d1z<r, HZP, FAST>(ps[r], cz, nzr);
-          const f2 gqz = d1z<r, HZP, FAST>(ps[r] + QOFF, cz, nzr);
-          const f2 wp = mac2<FAST>(mac2<FAST>(xmul2(gpx, n0, nzr), gpy, n1, nzr), gpz, n2, nzr);
-          const f2 wq = mac2<FAST>(mac2<FAST>(xmul2(gqx, n0, nzr), gqy, n1, nzr), gqz, n2, nzr);
-          const f2 g[3] = {gpx, gpy, gpz};
-          const f2 n[3] = {n0, n1, n2};
+        for (int kk = 2; kk <= r; ++kk) {
+          gpx = mac2<FAST>(gpx, sub2(lds2(ps[r + kk]), lds2(ps[r - kk])), cx[kk - 1], nzr);
+          gqx = mac2<FAST>(gqx, sub2(lds2(ps[r + kk] + QOFF), lds2(ps[r - kk] + QOFF)),
+                           cx[kk - 1], nzr);
+        }
+        const f2 gpy = d1p<r, FAST>(ps[r], C::PZ, cy, nzr);
+        const f2 gqy = d1p<r, FAST>(ps[r] + QOFF, C::PZ, cy, nzr);
+        const f2 gpz = d1z<r, HZP, FAST>(ps[r], cz, nzr);
+        const f2 gqz = d1z<r, HZP, FAST>(ps[r] + QOFF, cz, nzr);
+        const f2 wp = mac2<FAST>(mac2<FAST>(xmul2(gpx, n0, nzr), gpy, n1, nzr), gpz, n2, nzr);
+        const f2 wq = mac2<FAST>(mac2<FAST>(xmul2(gqx, n0, nzr), gqy, n1, nzr), gqz, n2, nzr);
+        const f2 g[3] = {gpx, gpy, gpz};
+        const f2 n[3] = {n0, n1, n2};
 #pragma unroll
-          for (int ax = 0; ax < 3; ++ax) {
-            if constexpr (FAST) F[ax] = fma2(neg2(wp), n[ax], g[ax]);
-            else F[ax] = sub2(g[ax], xmul2(wp, n[ax], nzr));
-            G[ax] = xmul2(wq, n[ax], nzr);
-            F[ax] &= dmask;
-            G[ax] &= dmask;
-          }
+        for (int ax = 0; ax < 3; ++ax) {
+          if constexpr (FAST) F[ax] = fma2(neg2(wp), n[ax], g[ax]);
+          else F[ax] = sub2(g[ax], xmul2(wp, n[ax], nzr));
+          G[ax] = xmul2(wq, n[ax], nzr);
+          F[ax] &= m;
+          G[ax] &= m;
         }
         if (core) {                                 // p, q (t-1) at the output plane xa - r
           p1 = lds2(ps[0]);
           q1 = lds2(ps[0] + QOFF);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[hc + u]);   // sequence i (plane xa - r) is done
 
       // ---- F_y, G_y, F_z, G_z of plane xa to FG slot u
       if (i >= NFG) mbar_wait(&fgempty[u], pk_ ^ 1u);
       {
         float* fgs = fg + u * 4 * C::FPL + foff;
-        if (work) {
-          if (comp != 2) {
-            sts2(fgs + 0 * C::FPL, F[1]);
-            sts2(fgs + 1 * C::FPL, G[1]);
-          }
-          if (comp != 1) {
-            sts2(fgs + 2 * C::FPL, F[2]);
-            sts2(fgs + 3 * C::FPL, G[2]);
-          }
+        if (comp != 2) {
+          sts2(fgs + 0 * C::FPL, F[1]);
+          sts2(fgs + 1 * C::FPL, G[1]);
+        }
+        if (comp != 1) {
+          sts2(fgs + 2 * C::FPL, F[2]);
+          sts2(fgs + 3 * C::FPL, G[2]);
         }
         mbar_arrive(&fgfull[u]);
         // planes x0-r .. x0-1 only feed the x queues: nobody reads their FG
@@ -430,11 +418,12 @@ tti_fused2(const __grid_constant__ Tti2Maps maps, const __grid_constant__ TtiFus
           if (in1) {
             *reinterpret_cast<f2*>(a.p0 + gi) = op;
             *reinterpret_cast<f2*>(a.q0 + gi) = oq;
-            bad |= !finite(p_lo) || !finite(q_lo) || !finite(p_hi) || !finite(q_hi);
+            if constexpr (GUARD)
+              bad |= !finite(p_lo) || !finite(q_lo) || !finite(p_hi) || !finite(q_hi);
           } else {
             a.p0[gi] = p_lo;
             a.q0[gi] = q_lo;
-            bad |= !finite(p_lo) || !finite(q_lo);
+            if constexpr (GUARD) bad |= !finite(p_lo) || !finite(q_lo);
           }
         }
       } else {
@@ -447,7 +436,9 @@ tti_fused2(const __grid_constant__ Tti2Maps maps, const __grid_constant__ TtiFus
       }
     }
   }
-  if (a.nonfinite && bad) atomicExch(a.nonfinite, 1);
+  if constexpr (GUARD) {
+    if (bad) atomicExch(a.nonfinite, 1);
+  }
 }
 
 }  // namespace
