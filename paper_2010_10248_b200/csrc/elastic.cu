@@ -293,6 +293,7 @@ __global__ void elastic_materials_from_velocity_kernel(MatIn vp, MatIn vs, MatIn
 }  // namespace stb
 
 #include "elastic_tiled.cuh"
+#include "elastic_tiled2.cuh"
 
 namespace stb {
 namespace {
@@ -421,7 +422,11 @@ class ElasticProp final : public stb_prop_s {
     set_damping(desc.damp);
     // TMA-tiled sweeps (elastic_tiled.cuh): f32, 3-D, R <= 4
     tiled_ = sizeof(T) == 4 && cf_.active[0] && cf_.active[1] && cf_.active[2] && R_ <= 4;
-    if (const char* e = std::getenv("STB_ELASTIC_PATH")) tiled_ = tiled_ && std::string(e) != "point";
+    if (const char* e = std::getenv("STB_ELASTIC_PATH")) {
+      tiled_ = tiled_ && std::string(e) != "point";
+      pair_ = std::string(e) != "tiled1";
+    }
+    pair_ = pair_ && tiled_;
     if (tiled_) setup_tiled();
     STB_REQUIRE(d_.total < (int64_t)INT32_MAX, STB_ERR_ARG,
                 "elastic slab too large for 32-bit offsets; use more x slabs");
@@ -479,6 +484,12 @@ class ElasticProp final : public stb_prop_s {
         const uint32_t py = (f >= TXX ? kTYv : kTYt) + 2 * R_;
         fmap_[f] = make_map3d_f32(reinterpret_cast<const float*>(f_[f].p), md, pz, py, 1);
       }
+      // elastic_tiled2: centre-operand boxes over the 16 x 32 tile
+      for (int f = 0; f < NFIELDS; ++f)
+        omap_[f] = make_map3d_f32(reinterpret_cast<const float*>(f_[f].p), md, kElTZ, 16, 1);
+      omap_[NFIELDS + 0] = make_map3d_f32(reinterpret_cast<const float*>(buoy_.p), md, kElTZ, 16, 1);
+      omap_[NFIELDS + 1] = make_map3d_f32(reinterpret_cast<const float*>(lam_.p), md, kElTZ, 16, 1);
+      omap_[NFIELDS + 2] = make_map3d_f32(reinterpret_cast<const float*>(mu_.p), md, kElTZ, 16, 1);
       switch (R_) {
         case 1: set_tiled_attr<1>(); break;
         case 2: set_tiled_attr<2>(); break;
@@ -501,8 +512,18 @@ class ElasticProp final : public stb_prop_s {
   template <int R> using CfgV = ElTiledCfg<R, 6, kTYv, ns_v<R>()>;
   template <int R> using CfgT = ElTiledCfg<R, 3, kTYt, ns_t<R>()>;
 
+  template <int R, int PASS>
+  void set_pair_attr() {
+    const int sm = (int)El2Cfg<R, PASS>::SMEM;
+    const auto at = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    STB_CUDA(cudaFuncSetAttribute(elastic_tiled2<R, PASS, false>, at, sm));
+    STB_CUDA(cudaFuncSetAttribute(elastic_tiled2<R, PASS, true>, at, sm));
+  }
+
   template <int R>
   void set_tiled_attr() {
+    set_pair_attr<R, 0>();
+    set_pair_attr<R, 1>();
     STB_CUDA(cudaFuncSetAttribute(elastic_tiled<R, 0, kTYv, ns_v<R>(), kMBv>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)CfgV<R>::smem_bytes()));
@@ -534,6 +555,36 @@ class ElasticProp final : public stb_prop_s {
     a.x_lo = x_lo;
     a.x_hi = x_hi;
     a.nonfinite = nonfinite;
+    a.negz = -0.0f;
+    if (pair_) {
+      El2Maps m{};
+      const int nin = phase == 0 ? 6 : 3, nout = phase == 0 ? 3 : 6;
+      const int fin = phase == 0 ? TXX : VX, fout = phase == 0 ? VX : TXX;
+      for (int f = 0; f < nin; ++f) m.f[f] = fmap_[fin + f];
+      for (int f = 0; f < nout; ++f) {
+        m.o[f] = omap_[fout + f];
+        a.out[f] = reinterpret_cast<float*>(f_[fout + f].p);
+      }
+      if (phase == 0) {
+        m.o[3] = omap_[NFIELDS + 0];
+      } else {
+        m.o[6] = omap_[NFIELDS + 1];
+        m.o[7] = omap_[NFIELDS + 2];
+      }
+      const dim3 grid = grid_for(16);
+      const bool g = nonfinite != nullptr;
+      if (phase == 0) {
+        using C = El2Cfg<R, 0>;
+        if (g) elastic_tiled2<R, 0, true><<<grid, C::NT, C::SMEM, st_>>>(m, a);
+        else elastic_tiled2<R, 0, false><<<grid, C::NT, C::SMEM, st_>>>(m, a);
+      } else {
+        using C = El2Cfg<R, 1>;
+        if (g) elastic_tiled2<R, 1, true><<<grid, C::NT, C::SMEM, st_>>>(m, a);
+        else elastic_tiled2<R, 1, false><<<grid, C::NT, C::SMEM, st_>>>(m, a);
+      }
+      STB_CHECK_LAUNCH();
+      return;
+    }
     if (phase == 0) {
     // v half step: inputs txx tyy tzz txy txz tyz, updates vx vy vz
     ElTiledMaps mv{};
@@ -856,7 +907,10 @@ class ElasticProp final : public stb_prop_s {
 
   std::string describe(int k) override {
     std::ostringstream os;
-    if (tiled_)
+    if (tiled_ && pair_)
+      os << "elastic_tiled2<f32,R=" << R_ << "> (TMA plane + operand rings, producer warp; "
+         << "16x32 tiles as z pairs; x chunk 256)";
+    else if (tiled_)
       os << "elastic_tiled<f32,R=" << R_ << "> (TMA plane rings; " << kTYv
          << "x32 tiles; x chunk 256)";
     else
@@ -889,8 +943,10 @@ class ElasticProp final : public stb_prop_s {
   DevBuf<T> fac_[3];
   bool has_fac_ = false;
   bool tiled_ = false;
+  bool pair_ = true;          // elastic_tiled2 unless STB_ELASTIC_PATH=tiled1
   int rec_field_ = TXX;      // engine.py:327-332 records txx
   CUtensorMap fmap_[NFIELDS];
+  CUtensorMap omap_[NFIELDS + 3];   // tile boxes of the fields, buoy, lam, mu (tiled2)
   int64_t t_next_ = 0;
   bool as_open_ = false;
   int64_t as_t0_ = 0, as_n_ = 0;

@@ -61,6 +61,7 @@ struct ElTiledArgs {
   int cx;
   int x_lo, x_hi;         // local planes of this launch, in cx chunks
   int* nonfinite;
+  float negz;             // -0.0f, opaque to ptxas (exact packed products, f32x2.cuh)
 };
 
 __device__ __forceinline__ float el_ld_nc(const float* p) {

@@ -1,0 +1,306 @@
+// Elastic half steps, second TMA kernel (f32, 3-D grids, R <= 4): z pairs in
+// packed fp32, a producer warp, no CTA barrier.
+//
+// Same arithmetic and IEEE order as elastic_tiled (and the point kernels,
+// physics.py:287-429): each packed lane is one correctly rounded scalar
+// operation -- sums as FADD2, products as FFMA2 with an opaque -0 addend
+// (f32x2.cuh) -- so results are bitwise those of the scalar kernels.
+//
+// What elastic_tiled's profile showed: 236 (v) / 272 (tau)
+// thread instructions per point, 27-30 % of the stall samples on the
+// per-plane CTA barrier behind which thread 0 refilled the ring, and
+// 17-23 % long-scoreboard on the centre operands loaded from global memory.
+// Here, per CTA (16 x 32 tile, an x chunk):
+//
+//   producer warp  one transaction barrier per iteration n: the NF input
+//                  field planes of sequence n (tile + R halo rows, 16-byte
+//                  aligned z halo, zero fill) into a plane ring of NS = R +
+//                  NO slots, and for output iterations the centre operands
+//                  (old values of the updated fields, materials) over the
+//                  tile plus fx into an NO-slot operand ring.
+//   8 warps        one z pair of the tile per thread: x derivatives from
+//                  register queues (2R+1 planes, pairs), y/z neighbours by
+//                  LDS.64 from the slot of the output plane (R behind the
+//                  newest), the update, 64-bit stores in place.  A warp
+//                  releases iteration n's operand slot after its output;
+//                  with NS = R + NO that also frees the plane slot the
+//                  producer fills next.
+//
+// Compulsory HBM bytes per point unchanged: v pass 52, tau pass 68.
+#pragma once
+
+#include "elastic_tiled.cuh"
+#include "f32x2.cuh"
+
+namespace stb {
+namespace {
+
+template <int R, int PASS>
+struct El2Cfg {
+  static constexpr int TY = 16, TZ = kElTZ, P = TZ / 2;       // 16 pairs per row
+  static constexpr int NF = PASS == 0 ? 6 : 3;                // staged (differentiated) fields
+  static constexpr int NOUT = PASS == 0 ? 3 : 6;              // updated fields
+  static constexpr int NM = PASS == 0 ? 1 : 2;                // materials
+  static constexpr int ZH = (R + 3) / 4 * 4;                  // z halo (16-byte boxes)
+  static constexpr int PY = TY + 2 * R, PZ = TZ + 2 * ZH;
+  static constexpr int FSLOT = (PY * PZ + 31) / 32 * 32;
+  static constexpr int SLOT = NF * FSLOT;
+  static constexpr int Q = 2 * R + 1;
+  static constexpr int NO = 3, NS = R + NO;
+  static constexpr int TPL = TY * TZ;
+  static constexpr int OSLOT = (NOUT + NM) * TPL + 32;        // + fx
+  static constexpr int HW = (R + 1) / 2;                      // z window: pairs -HW .. +HW
+  static constexpr int NCW = TY * P / 32;
+  static constexpr int NT = 32 * (NCW + 1);
+  static constexpr size_t SMEM =
+      (size_t)NS * SLOT * 4 + (size_t)NO * OSLOT * 4 + (size_t)2 * NO * 8 + 128;
+  static_assert(2 * HW <= ZH, "z window inside the staged box");
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+struct El2Maps {
+  CUtensorMap f[6];       // staged inputs (v pass: txx tyy tzz txy txz tyz; tau: vx vy vz)
+  CUtensorMap o[8];       // centre operands: updated fields' old values, then materials
+};
+
+__device__ __forceinline__ f2 el_lds2(const float* p) { return *reinterpret_cast<const f2*>(p); }
+
+// staggered first derivative of pairs: acc = sum_j (g(hi) - g(lo)) * c_j
+template <int R, typename G>
+__device__ __forceinline__ f2 stag2(const G& g, const f2* c, bool fwd, f2 nz) {
+  f2 acc = 0ull;
+#pragma unroll
+  for (int j = 1; j <= R; ++j) {
+    const int hi = fwd ? j : j - 1;
+    const int lo = fwd ? -(j - 1) : -j;
+    const f2 term = xmul2(sub2(g(hi), g(lo)), c[j - 1], nz);
+    acc = (j == 1) ? term : add2(acc, term);
+  }
+  return acc;
+}
+
+// z window of a field around the pair at c0: pairs at offsets -2HW .. +2HW
+template <int HW>
+struct ZWin {
+  f2 pr[2 * HW + 1];
+  float w[4 * HW + 2];
+  __device__ __forceinline__ void load(const float* c0) {
+#pragma unroll
+    for (int j = 0; j <= 2 * HW; ++j) {
+      pr[j] = el_lds2(c0 + 2 * (j - HW));
+      upk(pr[j], w[2 * j], w[2 * j + 1]);
+    }
+  }
+  __device__ __forceinline__ f2 operator()(int o) const {   // (z + o, z + 1 + o)
+    const int m = 2 * HW + o;
+    if (m % 2 == 0) return pr[m / 2];
+    return pk(w[m], w[m + 1]);
+  }
+};
+
+template <int R, int PASS, bool GUARD>
+__global__ void __launch_bounds__(El2Cfg<R, PASS>::NT, 1)
+elastic_tiled2(const __grid_constant__ El2Maps maps, const __grid_constant__ ElTiledArgs a) {
+  using C = El2Cfg<R, PASS>;
+  constexpr int Q = C::Q, NS = C::NS, NO = C::NO, NF = C::NF, NOUT = C::NOUT, NM = C::NM;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* ring = reinterpret_cast<float*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+  float* opr = ring + NS * C::SLOT;
+  uint64_t* ofull = reinterpret_cast<uint64_t*>(opr + NO * C::OSLOT);
+  uint64_t* oempty = ofull + NO;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int z0 = blockIdx.x * C::TZ, y0 = blockIdx.y * C::TY, x0 = a.x_lo + blockIdx.z * a.cx;
+  const int ny = (int)a.d.ny, nz = (int)a.d.nz;
+  const int x1 = min(x0 + a.cx, a.x_hi);
+  const int N = (x1 - x0) + 2 * R;                  // sequence n = plane x0 - R + n
+  const bool has_fac = a.has_fac != 0;
+
+  if (tid == 0) {
+    for (int o = 0; o < NO; ++o) {
+      mbar_init(&ofull[o], 1);
+      mbar_init(&oempty[o], C::NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // ------------------------------------------------------------ producer
+  if (warp == C::NCW) {
+    if (lane == 0) {
+      const int H = (int)a.d.H, zo = (int)a.d.zoff;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) prefetch_map(&maps.f[f]);
+#pragma unroll
+      for (int k = 0; k < NOUT + NM; ++k) prefetch_map(&maps.o[k]);
+      for (int n = 0; n < N; ++n) {
+        const int slot = n % NO;
+        if (n >= NO) mbar_wait_sleep(&oempty[slot], (uint32_t)(((n / NO) - 1) & 1));
+        float* os = opr + slot * C::OSLOT;
+        const bool out = n >= 2 * R;
+        const int x = x0 - 2 * R + n;               // output plane of iteration n
+        if (out) os[(NOUT + NM) * C::TPL] = has_fac ? __ldg(a.fx + x) : 1.f;
+        mbar_arrive_expect_tx(&ofull[slot], (uint32_t)(NF * C::PY * C::PZ +
+                                                       (out ? (NOUT + NM) * C::TPL : 0)) * 4u);
+        float* ps = ring + (n % NS) * C::SLOT;
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+          tma_load_3d(ps + f * C::FSLOT, &maps.f[f], zo + z0 - C::ZH, H + y0 - R, H + x0 - R + n,
+                      &ofull[slot]);
+        if (out) {
+#pragma unroll
+          for (int k = 0; k < NOUT + NM; ++k)
+            tma_load_3d(os + k * C::TPL, &maps.o[k], zo + z0, H + y0, H + x, &ofull[slot]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int ty = tid / C::P, tzp = tid % C::P;
+  const int y = y0 + ty, z = z0 + 2 * tzp;
+  const bool in0 = y < ny && z < nz, in1 = y < ny && z + 1 < nz;
+  const int gcore = in0 ? (int)a.d.at(0, y, z) : 0;
+  const int coff = (ty + R) * C::PZ + (2 * tzp + C::ZH);
+  const int ooff = ty * C::TZ + 2 * tzp;
+  const int plane = (int)a.d.plane;
+  const f2 nzr = bcast(a.negz);
+  f2 cxk[R], cyk[R], czk[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    cxk[k] = bcast(a.cf.d1[0][k]);
+    cyk[k] = bcast(a.cf.d1[1][k]);
+    czk[k] = bcast(a.cf.d1[2][k]);
+  }
+  float fyz0 = 1.f, fyz1 = 1.f;
+  if (has_fac && in0) {
+    const float fyv = __ldg(a.fy + y);
+    fyz0 = tmin(fyv, __ldg(a.fz + z));
+    fyz1 = in1 ? tmin(fyv, __ldg(a.fz + z + 1)) : 1.f;
+  }
+
+  // x queues (position n mod Q): v pass txx, txy, txz; tau pass vx, vy, vz
+  f2 q0[Q], q1[Q], q2[Q];
+#pragma unroll
+  for (int j = 0; j < Q; ++j) q0[j] = q1[j] = q2[j] = 0ull;
+  constexpr int QF0 = 0, QF1 = PASS == 0 ? 3 : 1, QF2 = PASS == 0 ? 4 : 2;
+
+  int os = 0, sn = 0, so = NS - R;                  // n % NO, n % NS, (n - R) % NS
+  uint32_t oph = 0;
+  bool bad = false;
+  for (int n0 = 0; n0 < N; n0 += Q) {
+#pragma unroll
+    for (int u = 0; u < Q; ++u) {
+      const int n = n0 + u;
+      if (n >= N) break;
+      mbar_wait(&ofull[os], oph);
+      const float* sl = ring + sn * C::SLOT + coff;  // newest plane, centre
+      q0[u] = el_lds2(sl + QF0 * C::FSLOT);
+      q1[u] = el_lds2(sl + QF1 * C::FSLOT);
+      q2[u] = el_lds2(sl + QF2 * C::FSLOT);
+      if (n >= 2 * R) {
+        const float* cp = ring + so * C::SLOT + coff;   // output plane (sequence n - R)
+        const float* ob = opr + os * C::OSLOT;
+        auto gq0 = [&](int o) { return q0[el_pmod(u - R + o, Q)]; };
+        auto gq1 = [&](int o) { return q1[el_pmod(u - R + o, Q)]; };
+        auto gq2 = [&](int o) { return q2[el_pmod(u - R + o, Q)]; };
+        auto gy = [&](int f) { return [=](int o) { return el_lds2(cp + f * C::FSLOT + o * C::PZ); }; };
+        f2 res[NOUT];
+        f2 fac = 0ull;
+        if (has_fac) {
+          const float fxv = ob[(NOUT + NM) * C::TPL];
+          fac = pk(tmin(fxv, fyz0), tmin(fxv, fyz1));
+        }
+        if constexpr (PASS == 0) {
+          // fields: 0 txx, 1 tyy, 2 tzz, 3 txy, 4 txz, 5 tyz
+          ZWin<C::HW> w4, w5, w2;
+          w4.load(cp + 4 * C::FSLOT);
+          w5.load(cp + 5 * C::FSLOT);
+          w2.load(cp + 2 * C::FSLOT);
+          f2 d0 = stag2<R>(gq0, cxk, true, nzr);
+          d0 = add2(d0, stag2<R>(gy(3), cyk, false, nzr));
+          d0 = add2(d0, stag2<R>(w4, czk, false, nzr));
+          f2 d1 = stag2<R>(gq1, cxk, false, nzr);
+          d1 = add2(d1, stag2<R>(gy(1), cyk, true, nzr));
+          d1 = add2(d1, stag2<R>(w5, czk, false, nzr));
+          f2 d2 = stag2<R>(gq2, cxk, false, nzr);
+          d2 = add2(d2, stag2<R>(gy(5), cyk, false, nzr));
+          d2 = add2(d2, stag2<R>(w2, czk, true, nzr));
+          const f2 buoy = el_lds2(ob + 3 * C::TPL + ooff);
+          const f2 dd[3] = {d0, d1, d2};
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            f2 o = add2(el_lds2(ob + k * C::TPL + ooff), xmul2(dd[k], buoy, nzr));
+            if (has_fac) o = xmul2(o, fac, nzr);
+            res[k] = o;
+          }
+        } else {
+          // fields: 0 vx, 1 vy, 2 vz; outputs txx tyy tzz txy txz tyz
+          ZWin<C::HW> w0, w1, w2;
+          w0.load(cp + 0 * C::FSLOT);
+          w1.load(cp + 1 * C::FSLOT);
+          w2.load(cp + 2 * C::FSLOT);
+          const f2 lam = el_lds2(ob + 6 * C::TPL + ooff), mu = el_lds2(ob + 7 * C::TPL + ooff);
+          const f2 mu2 = xmul2(mu, bcast(2.f), nzr);
+          const f2 dg0 = stag2<R>(gq0, cxk, false, nzr);
+          const f2 dg1 = stag2<R>(gy(1), cyk, false, nzr);
+          const f2 dg2 = stag2<R>(w2, czk, false, nzr);
+          const f2 tr = add2(add2(dg0, dg1), dg2);
+          const f2 dg[3] = {dg0, dg1, dg2};
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            f2 o = add2(el_lds2(ob + k * C::TPL + ooff),
+                        add2(xmul2(tr, lam, nzr), xmul2(dg[k], mu2, nzr)));
+            if (has_fac) o = xmul2(o, fac, nzr);
+            res[k] = o;
+          }
+          // txy = stag_y(vx, fwd) + stag_x(vy, fwd); txz = stag_z(vx) + stag_x(vz);
+          // tyz = stag_z(vy) + stag_y(vz)   (elastic_tau_point order)
+          const f2 s0 = add2(stag2<R>(gy(0), cyk, true, nzr), stag2<R>(gq1, cxk, true, nzr));
+          const f2 s1 = add2(stag2<R>(w0, czk, true, nzr), stag2<R>(gq2, cxk, true, nzr));
+          const f2 s2 = add2(stag2<R>(w1, czk, true, nzr), stag2<R>(gy(2), cyk, true, nzr));
+          const f2 ss[3] = {s0, s1, s2};
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            f2 o = add2(el_lds2(ob + (3 + k) * C::TPL + ooff), xmul2(ss[k], mu, nzr));
+            if (has_fac) o = xmul2(o, fac, nzr);
+            res[3 + k] = o;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&oempty[os]);
+        if (in0) {
+          const int gi = gcore + (x0 - 2 * R + n) * plane;
+#pragma unroll
+          for (int k = 0; k < NOUT; ++k) {
+            float lo, hi;
+            upk(res[k], lo, hi);
+            if (in1) {
+              *reinterpret_cast<f2*>(a.out[k] + gi) = res[k];
+              if constexpr (GUARD) bad |= !finite(lo) || !finite(hi);
+            } else {
+              a.out[k][gi] = lo;
+              if constexpr (GUARD) bad |= !finite(lo);
+            }
+          }
+        }
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&oempty[os]);
+      }
+      if (++os == NO) {
+        os = 0;
+        oph ^= 1u;
+      }
+      if (++sn == NS) sn = 0;
+      if (++so == NS) so = 0;
+    }
+  }
+  if constexpr (GUARD) {
+    if (bad) atomicExch(a.nonfinite, 1);
+  }
+}
+
+}  // namespace
+}  // namespace stb
