@@ -428,6 +428,27 @@ class ElasticProp final : public stb_prop_s {
     }
     pair_ = pair_ && tiled_;
     if (tiled_) setup_tiled();
+    if (pair_) {
+      // opt-in (STB_EL_STREAM=1): bit-exact and it cuts the DRAM traffic of a
+      // step by 15-20 %, but measured slower than the two launches
+      // (33 vs 25 ms at 1024^3) -- with half the SMs per
+      // sweep, each SM's three-slot TMA pipeline is latency-bound
+      int sms = 148;
+      int dev = 0;
+      STB_CUDA(cudaGetDevice(&dev));
+      STB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      stream_nv_ = sms / 2;
+      stream_nt_ = sms - stream_nv_;
+      if (const char* e = std::getenv("STB_EL_STREAM"))
+        stream_ = std::atoi(e) != 0 && d_.nx + 2 * R_ < (1 << 13) - 1;
+      if (const char* e = std::getenv("STB_EL_NV")) stream_nv_ = std::max(1, std::atoi(e));
+      if (const char* e = std::getenv("STB_EL_NT")) stream_nt_ = std::max(1, std::atoi(e));
+      if (const char* e = std::getenv("STB_EL_LEAD")) stream_lead_ = std::max(1, std::atoi(e));
+      if (const char* e = std::getenv("STB_EL_PUB")) {
+        const int p = std::atoi(e);
+        if (p == 1 || p == 2 || p == 4 || p == 8 || p == 16) stream_pub_ = p;
+      }
+    }
     STB_REQUIRE(d_.total < (int64_t)INT32_MAX, STB_ERR_ARG,
                 "elastic slab too large for 32-bit offsets; use more x slabs");
   }
@@ -518,6 +539,86 @@ class ElasticProp final : public stb_prop_s {
     const auto at = cudaFuncAttributeMaxDynamicSharedMemorySize;
     STB_CUDA(cudaFuncSetAttribute(elastic_tiled2<R, PASS, false>, at, sm));
     STB_CUDA(cudaFuncSetAttribute(elastic_tiled2<R, PASS, true>, at, sm));
+    if (PASS == 0) {
+      const int ss = (int)std::max(El2Cfg<R, 0>::SMEM, El2Cfg<R, 1>::SMEM);
+      STB_CUDA(cudaFuncSetAttribute(elastic_stream<R, false>, at, ss));
+      STB_CUDA(cudaFuncSetAttribute(elastic_stream<R, true>, at, ss));
+    }
+  }
+
+  // The full step in one launch (elastic_tiled2.cuh: elastic_stream).
+  template <int R>
+  void launch_stream_r(int* nonfinite) {
+    const int tiles_z = (int)((d_.nz + kElTZ - 1) / kElTZ);
+    const int tiles_yv = (int)((d_.ny + 15) / 16), tiles_yt = (int)((d_.ny + R + 15) / 16);
+    const size_t nvt = (size_t)tiles_yv * tiles_z, ntt = (size_t)tiles_yt * tiles_z;
+    if (prog_v_.n < nvt || prog_t_.n < ntt || !stream_err_.p || epoch_ >= (1u << 18)) {
+      prog_v_.alloc(nvt);
+      prog_t_.alloc(ntt);
+      stream_err_.alloc(1);
+      STB_CUDA(cudaMemsetAsync(prog_v_.p, 0, nvt * sizeof(unsigned), st_));
+      STB_CUDA(cudaMemsetAsync(prog_t_.p, 0, ntt * sizeof(unsigned), st_));
+      STB_CUDA(cudaMemsetAsync(stream_err_.p, 0, sizeof(int), st_));
+      epoch_ = 0;
+    }
+    ElTiledArgs a{};
+    a.fx = reinterpret_cast<const float*>(fac_[0].p);
+    a.fy = reinterpret_cast<const float*>(fac_[1].p);
+    a.fz = reinterpret_cast<const float*>(fac_[2].p);
+    a.has_fac = has_fac_ ? 1 : 0;
+    for (int ax = 0; ax < 3; ++ax)
+      for (int j = 0; j < 8; ++j) a.cf.d1[ax][j] = (float)cf_.d1[ax][j];
+    a.d = d_;
+    a.cx = (int)d_.nx;
+    a.x_lo = 0;
+    a.x_hi = (int)d_.nx;
+    a.nonfinite = nonfinite;
+    a.negz = -0.0f;
+    ElTiledArgs av = a, at = a;
+    El2Maps mv{}, mt{};
+    for (int f = 0; f < 6; ++f) mv.f[f] = fmap_[TXX + f];
+    for (int f = 0; f < 3; ++f) {
+      mv.o[f] = omap_[VX + f];
+      av.out[f] = reinterpret_cast<float*>(f_[VX + f].p);
+    }
+    mv.o[3] = omap_[NFIELDS + 0];
+    for (int f = 0; f < 3; ++f) mt.f[f] = fmap_[VX + f];
+    for (int f = 0; f < 6; ++f) {
+      mt.o[f] = omap_[TXX + f];
+      at.out[f] = reinterpret_cast<float*>(f_[TXX + f].p);
+    }
+    mt.o[6] = omap_[NFIELDS + 1];
+    mt.o[7] = omap_[NFIELDS + 2];
+    ElStream sc{};
+    sc.prog_v = prog_v_.p;
+    sc.prog_t = prog_t_.p;
+    sc.err = stream_err_.p;
+    sc.epoch = ++epoch_;
+    sc.nv = (int)std::min<size_t>((size_t)stream_nv_, nvt);
+    sc.nt = (int)std::min<size_t>((size_t)stream_nt_, ntt);
+    sc.tiles_z = tiles_z;
+    sc.tiles_yv = tiles_yv;
+    sc.tiles_yt = tiles_yt;
+    sc.lead = stream_lead_;
+    sc.pub = stream_pub_;
+    const int ss = (int)std::max(El2Cfg<R, 0>::SMEM, El2Cfg<R, 1>::SMEM);
+    const unsigned grid = (unsigned)(sc.nv + sc.nt);
+    if (nonfinite) elastic_stream<R, true><<<grid, El2Cfg<R, 0>::NT + 32, ss, st_>>>(mv, mt, av, at, sc);
+    else elastic_stream<R, false><<<grid, El2Cfg<R, 0>::NT + 32, ss, st_>>>(mv, mt, av, at, sc);
+    STB_CHECK_LAUNCH();
+  }
+
+  void launch_stream(int* nonfinite) {
+    if constexpr (sizeof(T) == 4) {
+      switch (R_) {
+        case 1: return launch_stream_r<1>(nonfinite);
+        case 2: return launch_stream_r<2>(nonfinite);
+        case 3: return launch_stream_r<3>(nonfinite);
+        case 4: return launch_stream_r<4>(nonfinite);
+        default: break;
+      }
+    }
+    throw Error(STB_ERR_ARG, "no streamed elastic kernel for this configuration");
   }
 
   template <int R>
@@ -750,11 +851,15 @@ class ElasticProp final : public stb_prop_s {
       // which flags the same blow-ups one half step later.
       int* nf = guard_now ? guards.p + gi : nullptr;
       STB_CUDA(cudaEventRecord(events_[2 * launches_], st_));
-      launch_half(0, 0, (int)d_.nx, nf);
-      launch_half(1, 0, (int)d_.nx, nf);
+      if (stream_) {
+        launch_stream(nf);
+      } else {
+        launch_half(0, 0, (int)d_.nx, nf);
+        launch_half(1, 0, (int)d_.nx, nf);
+      }
       STB_CUDA(cudaEventRecord(events_[2 * launches_ + 1], st_));
       ++launches_;
-      all_launches_ += 2;
+      all_launches_ += stream_ ? 1 : 2;
       if (guard_now) ++gi;
       inject(t);
       gather(t - t0);
@@ -765,10 +870,14 @@ class ElasticProp final : public stb_prop_s {
     if (nrec_ && rec_out) rec_dev_.download(rec_out, nsteps * nrec_, st_);
     std::vector<int> gh(guard_steps.size() + 1, 0);
     if (!guard_steps.empty()) guards.download(gh.data(), guard_steps.size(), st_);
+    int serr = 0;
+    if (stream_ && stream_err_.p) stream_err_.download(&serr, 1, st_);
     STB_CUDA(cudaStreamSynchronize(st_));
     float rm = 0.f;
     STB_CUDA(cudaEventElapsedTime(&rm, run_ev_[0], run_ev_[1]));
     run_ms_ = rm;
+    STB_REQUIRE(serr == 0, STB_ERR_CUDA,
+                "elastic_stream: a tau tile gave up waiting for its v tiles (results invalid)");
     for (size_t i = 0; i < guard_steps.size(); ++i) {
       if (gh[i]) {
         if (bad_step) *bad_step = guard_steps[i];
@@ -907,7 +1016,11 @@ class ElasticProp final : public stb_prop_s {
 
   std::string describe(int k) override {
     std::ostringstream os;
-    if (tiled_ && pair_)
+    if (tiled_ && pair_ && stream_)
+      os << "elastic_stream<f32,R=" << R_ << "> (one launch per step: " << stream_nv_
+         << " v-sweep + " << stream_nt_ << " tau-sweep CTAs streaming through L2; "
+         << "16x32 tiles as z pairs)";
+    else if (tiled_ && pair_)
       os << "elastic_tiled2<f32,R=" << R_ << "> (TMA plane + operand rings, producer warp; "
          << "16x32 tiles as z pairs; x chunk 256)";
     else if (tiled_)
@@ -916,7 +1029,8 @@ class ElasticProp final : public stb_prop_s {
     else
       os << "elastic_point<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
          << "> (v + tau, thread per point, zero-haloed layout)";
-    os << " k=1 requested_k=" << k << " bytes_per_point=" << 30 * sizeof(T);
+    os << " k=1 requested_k=" << k
+       << " bytes_per_point=" << (tiled_ && pair_ && stream_ ? 21 : 30) * sizeof(T);
     return os.str();
   }
 
@@ -944,6 +1058,13 @@ class ElasticProp final : public stb_prop_s {
   bool has_fac_ = false;
   bool tiled_ = false;
   bool pair_ = true;          // elastic_tiled2 unless STB_ELASTIC_PATH=tiled1
+  // elastic_stream: the full step as one launch (v and tau sweeps streaming
+  // behind each other through L2); STB_EL_STREAM=0/1 overrides the size rule
+  bool stream_ = false;
+  int stream_nv_ = 0, stream_nt_ = 0, stream_lead_ = 24, stream_pub_ = 8;
+  DevBuf<unsigned> prog_v_, prog_t_;
+  DevBuf<int> stream_err_;
+  unsigned epoch_ = 0;
   int rec_field_ = TXX;      // engine.py:327-332 records txx
   CUtensorMap fmap_[NFIELDS];
   CUtensorMap omap_[NFIELDS + 3];   // tile boxes of the fields, buoy, lam, mu (tiled2)

@@ -53,7 +53,7 @@ struct El2Cfg {
   static constexpr int NCW = TY * P / 32;
   static constexpr int NT = 32 * (NCW + 1);
   static constexpr size_t SMEM =
-      (size_t)NS * SLOT * 4 + (size_t)NO * OSLOT * 4 + (size_t)2 * NO * 8 + 128;
+      (size_t)NS * SLOT * 4 + (size_t)NO * OSLOT * 4 + (size_t)2 * NO * 8 + 64 + 128;
   static_assert(2 * HW <= ZH, "z window inside the staged box");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
@@ -62,6 +62,51 @@ struct El2Maps {
   CUtensorMap f[6];       // staged inputs (v pass: txx tyy tzz txy txz tyz; tau: vx vy vz)
   CUtensorMap o[8];       // centre operands: updated fields' old values, then materials
 };
+
+// Control block of the streamed full step (elastic_stream below).  Progress
+// words are (epoch << 13) | planes; a word of another epoch reads as 0.
+struct ElStream {
+  unsigned* prog_v;       // per v tile: x planes stored and visible
+  unsigned* prog_t;       // per tau tile: x planes issued (throttle hint only)
+  int* err;               // set when a dependency wait gave up
+  unsigned epoch;
+  int nv, nt;             // CTAs per role
+  int tiles_z, tiles_yv, tiles_yt;
+  int lead;               // planes a v tile may run ahead of the tau tile under it
+  int pub;                // planes per published group (power of 2)
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_all() {
+  asm volatile("fence.proxy.async;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta_s32(const volatile int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];"
+               : "=r"(v) : "r"(smem_u32(const_cast<const int*>(p))) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_s32(volatile int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;"
+               ::"r"(smem_u32(const_cast<int*>(p))), "r"(v) : "memory");
+}
+constexpr int kElTauSeen = 8, kElHave = 9;          // wprog slots after the per-warp words
+constexpr unsigned kElPlaneBits = 13, kElPlaneMask = (1u << kElPlaneBits) - 1u;
 
 __device__ __forceinline__ f2 el_lds2(const float* p) { return *reinterpret_cast<const f2*>(p); }
 
@@ -98,32 +143,21 @@ struct ZWin {
   }
 };
 
-template <int R, int PASS, bool GUARD>
-__global__ void __launch_bounds__(El2Cfg<R, PASS>::NT, 1)
-elastic_tiled2(const __grid_constant__ El2Maps maps, const __grid_constant__ ElTiledArgs a) {
+// One tile (16 x 32 in y, z; x planes [x0, x1)) of one half step.  The caller
+// has initialised the barriers; every thread returns.  STREAM adds the
+// cross-CTA protocol of elastic_stream (publish / dependency waits / throttle).
+template <int R, int PASS, bool GUARD, bool STREAM>
+__device__ __forceinline__ void el2_tile(const El2Maps& maps, const ElTiledArgs& a,
+                                         const ElStream& sc, float* ring, float* opr,
+                                         uint64_t* ofull, uint64_t* oempty, volatile int* wprog,
+                                         const int y0, const int z0, const int x0, const int x1,
+                                         const int tile) {
   using C = El2Cfg<R, PASS>;
   constexpr int Q = C::Q, NS = C::NS, NO = C::NO, NF = C::NF, NOUT = C::NOUT, NM = C::NM;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* ring = reinterpret_cast<float*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
-  float* opr = ring + NS * C::SLOT;
-  uint64_t* ofull = reinterpret_cast<uint64_t*>(opr + NO * C::OSLOT);
-  uint64_t* oempty = ofull + NO;
-
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int z0 = blockIdx.x * C::TZ, y0 = blockIdx.y * C::TY, x0 = a.x_lo + blockIdx.z * a.cx;
   const int ny = (int)a.d.ny, nz = (int)a.d.nz;
-  const int x1 = min(x0 + a.cx, a.x_hi);
   const int N = (x1 - x0) + 2 * R;                  // sequence n = plane x0 - R + n
   const bool has_fac = a.has_fac != 0;
-
-  if (tid == 0) {
-    for (int o = 0; o < NO; ++o) {
-      mbar_init(&ofull[o], 1);
-      mbar_init(&oempty[o], C::NCW);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
 
   // ------------------------------------------------------------ producer
   if (warp == C::NCW) {
@@ -133,8 +167,32 @@ elastic_tiled2(const __grid_constant__ El2Maps maps, const __grid_constant__ ElT
       for (int f = 0; f < NF; ++f) prefetch_map(&maps.f[f]);
 #pragma unroll
       for (int k = 0; k < NOUT + NM; ++k) prefetch_map(&maps.o[k]);
+      int have = 0;                                 // tau role: planes stored on every dependency
+      int budget = 8000;                            // v role: throttle polls left for this tile
       for (int n = 0; n < N; ++n) {
         const int slot = n % NO;
+        if constexpr (STREAM && PASS == 1) {
+          // plane x0 - R + n of vx, vy, vz must be stored by every dependency
+          // (which also means their sweeps have read the stress planes this
+          // iteration's output overwrites, R behind); the sync warp polls the
+          // dependencies and posts what it has acquired
+          const int need = min(x0 - R + n + 1, x1) - x0;
+          if (need > have) {
+            while ((have = ld_acquire_cta_s32(&wprog[kElHave])) < need) __nanosleep(32);
+            fence_proxy_async_all();                // their generic stores before our TMA reads
+          }
+          if ((n & 3) == 0)
+            st_relaxed_u32(sc.prog_t + tile, (sc.epoch << kElPlaneBits) | (unsigned)n);
+        }
+        if constexpr (STREAM && PASS == 0) {
+          // hold back while the tau tile under this tile is more than `lead`
+          // planes behind, so what this sweep reads and writes is still in L2
+          // when the tau sweep comes for it (bounded: a hint, not a dependency)
+          while (budget > 0 && n - sc.lead > wprog[kElTauSeen]) {
+            --budget;
+            __nanosleep(128);
+          }
+        }
         if (n >= NO) mbar_wait_sleep(&oempty[slot], (uint32_t)(((n / NO) - 1) & 1));
         float* os = opr + slot * C::OSLOT;
         const bool out = n >= 2 * R;
@@ -153,6 +211,76 @@ elastic_tiled2(const __grid_constant__ El2Maps maps, const __grid_constant__ ElT
             tma_load_3d(os + k * C::TPL, &maps.o[k], zo + z0, H + y0, H + x, &ofull[slot]);
         }
       }
+      if constexpr (STREAM && PASS == 1)
+        st_relaxed_u32(sc.prog_t + tile, (sc.epoch << kElPlaneBits) | kElPlaneMask);
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ sync warp
+  // (elastic_stream only) one thread that does the global-memory side of the
+  // protocol, so neither the consumers nor the TMA-issuing thread wait on it.
+  if (warp == C::NCW + 1) {
+    if constexpr (STREAM) {
+      if (lane == 0) {
+        const int total = x1 - x0;
+        const unsigned ep = sc.epoch << kElPlaneBits;
+        if constexpr (PASS == 0) {
+          // publish the planes every consumer warp has stored (the warps post
+          // them with release.cta; the gpu-scope fence here is cumulative),
+          // and keep the tau tile's progress at hand for the throttle
+          int pubd = 0;
+          for (unsigned it = 0; pubd < total; ++it) {
+            int m = 1 << 30;
+#pragma unroll
+            for (int w = 0; w < C::NCW; ++w) m = min(m, ld_acquire_cta_s32(&wprog[w]));
+            if (m >= pubd + sc.pub || (m >= total && pubd < total)) {
+              __threadfence();
+              st_relaxed_u32(sc.prog_v + tile, ep | (unsigned)m);
+              pubd = m;
+            }
+            if ((it & 3) == 0) {
+              const unsigned w = ld_relaxed_u32(sc.prog_t + tile);
+              wprog[kElTauSeen] = (w >> kElPlaneBits) == sc.epoch ? (int)(w & kElPlaneMask) : 0;
+            }
+            __nanosleep(64);
+          }
+        } else {
+          // the v tiles whose planes this tile stages (and whose sweeps read
+          // the stresses this tile overwrites): rows ty-1, ty x columns
+          // tz-1 .. tz+1 of the v tiling
+          int dep[6];
+          const int ty = tile / sc.tiles_z, tz = tile % sc.tiles_z;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            const int dy = ty - 1 + k / 3, dz = tz - 1 + k % 3;
+            dep[k] = (dy >= 0 && dy < sc.tiles_yv && dz >= 0 && dz < sc.tiles_z)
+                         ? dy * sc.tiles_z + dz : -1;
+          }
+          int have = 0;
+          for (unsigned spins = 0; have < total; ++spins) {
+            unsigned w[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k)             // six independent loads in flight
+              w[k] = dep[k] >= 0 ? ld_relaxed_u32(sc.prog_v + dep[k]) : (ep | kElPlaneMask);
+            int m = 1 << 30;
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+              m = min(m, (w[k] >> kElPlaneBits) == sc.epoch ? (int)(w[k] & kElPlaneMask) : 0);
+            if (spins > (1u << 23)) {               // ~ seconds without progress: give up, report
+              *sc.err = 1;
+              m = total;
+            }
+            if (m > have) {
+              __threadfence();                      // acquire: relaxed loads, then the fence
+              st_release_cta_s32(&wprog[kElHave], m);
+              have = m;
+              spins = 0;
+            }
+            __nanosleep(64);
+          }
+        }
+      }
     }
     return;
   }
@@ -160,7 +288,7 @@ elastic_tiled2(const __grid_constant__ El2Maps maps, const __grid_constant__ ElT
   // ------------------------------------------------------------ consumers
   const int ty = tid / C::P, tzp = tid % C::P;
   const int y = y0 + ty, z = z0 + 2 * tzp;
-  const bool in0 = y < ny && z < nz, in1 = y < ny && z + 1 < nz;
+  const bool in0 = y >= 0 && y < ny && z < nz, in1 = y >= 0 && y < ny && z + 1 < nz;
   const int gcore = in0 ? (int)a.d.at(0, y, z) : 0;
   const int coff = (ty + R) * C::PZ + (2 * tzp + C::ZH);
   const int ooff = ty * C::TZ + 2 * tzp;
@@ -285,6 +413,11 @@ elastic_tiled2(const __grid_constant__ El2Maps maps, const __grid_constant__ ElT
             }
           }
         }
+        if constexpr (STREAM && PASS == 0) {
+          // post the planes this warp has stored (the sync warp publishes them)
+          __syncwarp();
+          if (lane == 0) st_release_cta_s32(&wprog[warp], n - 2 * R + 1);
+        }
       } else {
         __syncwarp();
         if (lane == 0) mbar_arrive(&oempty[os]);
@@ -299,6 +432,107 @@ elastic_tiled2(const __grid_constant__ El2Maps maps, const __grid_constant__ ElT
   }
   if constexpr (GUARD) {
     if (bad) atomicExch(a.nonfinite, 1);
+  }
+}
+
+// shared memory of one pass: plane ring, operand ring, barriers, warp progress
+template <int R, int PASS>
+struct El2Smem {
+  using C = El2Cfg<R, PASS>;
+  float* ring;
+  float* opr;
+  uint64_t* ofull;
+  uint64_t* oempty;
+  volatile int* wprog;
+  __device__ __forceinline__ explicit El2Smem(unsigned char* raw) {
+    ring = reinterpret_cast<float*>(raw + ((128u - (smem_u32(raw) & 127u)) & 127u));
+    opr = ring + C::NS * C::SLOT;
+    ofull = reinterpret_cast<uint64_t*>(opr + C::NO * C::OSLOT);
+    oempty = ofull + C::NO;
+    wprog = reinterpret_cast<volatile int*>(oempty + C::NO);
+  }
+  // barriers for one tile; `again`: they carry a finished tile's phases
+  __device__ __forceinline__ void init(bool again) {
+    if (threadIdx.x == 0) {
+      for (int o = 0; o < C::NO; ++o) {
+        if (again) {
+          mbar_inval(&ofull[o]);
+          mbar_inval(&oempty[o]);
+        }
+        mbar_init(&ofull[o], 1);
+        mbar_init(&oempty[o], C::NCW);
+      }
+      fence_mbar_init();
+    }
+    if (threadIdx.x < 16) wprog[threadIdx.x] = 0;
+    __syncthreads();
+  }
+};
+
+// One half step as its own launch: a CTA per (tile, x chunk).
+template <int R, int PASS, bool GUARD>
+__global__ void __launch_bounds__(El2Cfg<R, PASS>::NT, 1)
+elastic_tiled2(const __grid_constant__ El2Maps maps, const __grid_constant__ ElTiledArgs a) {
+  using C = El2Cfg<R, PASS>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  El2Smem<R, PASS> sm(smem_raw);
+  sm.init(false);
+  const int x0 = a.x_lo + blockIdx.z * a.cx;
+  const ElStream none{};
+  el2_tile<R, PASS, GUARD, false>(maps, a, none, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
+                                  blockIdx.y * C::TY, blockIdx.x * C::TZ, x0,
+                                  min(x0 + a.cx, a.x_hi), 0);
+}
+
+// The full step (v sweep, then tau sweep) as ONE launch, the two sweeps
+// streaming through L2 behind each other -- the reference's wavefront over
+// the two half steps (schedule.py:81-90: tau follows v with an offset of R),
+// with B200's L2 in the role of the CPU's last-level cache.
+//
+// CTAs [0, nv) run the v sweep, CTAs [nv, nv + nt) the tau sweep, each CTA
+// taking tiles rank, rank + n_role, ... and streaming the whole x extent per
+// tile.  The tau tiling is shifted by -R rows in y, so a tau tile only
+// overwrites stress rows no later v tile reads, and it trails the v tiles it
+// depends on by R planes in x plus the publish granularity: what the v sweep
+// read (six stresses) and wrote (three velocities) a few microseconds earlier
+// is what the tau sweep reads next, out of L2.  DRAM then sees ~84 B per point
+// per step (each field read and written once, three materials) instead of the
+// two launches' 120 B.
+//
+// v tiles never wait on anything but a bounded throttle, and they are the
+// lower block indices, so the dependency waits of the tau role cannot
+// deadlock whatever the residency of the grid.
+template <int R, bool GUARD>
+__global__ void __launch_bounds__(El2Cfg<R, 0>::NT + 32, 1)
+elastic_stream(const __grid_constant__ El2Maps mv, const __grid_constant__ El2Maps mt,
+               const __grid_constant__ ElTiledArgs av, const __grid_constant__ ElTiledArgs at,
+               const __grid_constant__ ElStream sc) {
+  static_assert(El2Cfg<R, 0>::NT == El2Cfg<R, 1>::NT, "both roles share the thread layout");
+  static_assert(2 * R <= El2Cfg<R, 0>::TY, "tau rows shifted by R stay clear of the next v row");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const bool tau = (int)blockIdx.x >= sc.nv;
+  const int rank = tau ? (int)blockIdx.x - sc.nv : (int)blockIdx.x;
+  bool again = false;
+  if (!tau) {
+    using C = El2Cfg<R, 0>;
+    El2Smem<R, 0> sm(smem_raw);
+    for (int t = rank; t < sc.tiles_yv * sc.tiles_z; t += sc.nv, again = true) {
+      sm.init(again);
+      el2_tile<R, 0, GUARD, true>(mv, av, sc, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
+                                  (t / sc.tiles_z) * C::TY, (t % sc.tiles_z) * C::TZ, av.x_lo,
+                                  av.x_hi, t);
+      __syncthreads();
+    }
+  } else {
+    using C = El2Cfg<R, 1>;
+    El2Smem<R, 1> sm(smem_raw);
+    for (int t = rank; t < sc.tiles_yt * sc.tiles_z; t += sc.nt, again = true) {
+      sm.init(again);
+      el2_tile<R, 1, GUARD, true>(mt, at, sc, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
+                                  (t / sc.tiles_z) * C::TY - R, (t % sc.tiles_z) * C::TZ, at.x_lo,
+                                  at.x_hi, t);
+      __syncthreads();
+    }
   }
 }
 

@@ -515,8 +515,12 @@ class SlabRunner:
         item = np.dtype(self.config.dtype).itemsize
         if self.elastic:
             # separate v and tau launches: (6 tau + 3 v + buoy) reads + 3 v
-            # writes, then (3 v + 6 tau + lam + mu) reads + 6 tau writes
-            return 30 * item
+            # writes, then (3 v + 6 tau + lam + mu) reads + 6 tau writes = 30
+            # values; the streamed single launch (elastic_stream) reads and
+            # writes every field once plus three materials = 21.  The device
+            # reports the path it chose.
+            m = re.search(r"bytes_per_point=(\d+)", self.describe())
+            return int(m.group(1)) if m else 30 * item
         if self.config.physics == "tti":
             # the device reports the path it chose (fused: 48 B f32)
             m = re.search(r"bytes_per_point=(\d+)", self.describe())

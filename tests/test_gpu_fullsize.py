@@ -222,8 +222,34 @@ def test_elastic_512_tiled_vs_point_full_size():
                         sources=stb.SourceSpec([[2555.0, 2555.0, 2000.0]], f0=12.0),
                         receiver_coords=rec, receiver_field="vz")
     a = stb.run(cfg)
-    assert "elastic_tiled" in a.report.schedule["device_plan"]
+    plan = a.report.schedule["device_plan"]
+    assert "elastic_tiled" in plan or "elastic_stream" in plan
     b = _with_env({"STB_ELASTIC_PATH": "point"}, lambda: stb.run(cfg))
     assert "elastic_point" in b.report.schedule["device_plan"]
     _same(a, b)
+    assert np.abs(a.fields["vz"]).max() > 0
+
+
+def test_elastic_streamed_single_launch_matches_two_launches():
+    """STB_EL_STREAM=1 (elastic_stream: the v and tau sweeps of a step in one
+    launch, coupled through progress words in global memory) == the two
+    launches, bit for bit, on a grid of many tiles per role (240 x 208 x 200:
+    13 x 7 v tiles, 14 x 7 tau tiles, heterogeneous medium, sponge, 12 steps)."""
+    shape = (240, 208, 200)
+    rng = np.random.default_rng(11)
+    vp = 2000.0 + 2000.0 * rng.random(shape)
+    grid = stb.GridSpec(shape, (10.0,) * 3, boundary_layers=16)
+    rec = np.stack([np.linspace(100.0, 2000.0, 64), np.full(64, 955.0), np.full(64, 300.0)],
+                   axis=1)
+    cfg = stb.RunConfig(physics="elastic", grid=grid, space_order=8, nt=12, dt=0.5e-3,
+                        medium={"vp": vp, "vs": vp / 1.7, "rho": 2100.0},
+                        sources=stb.SourceSpec([[1155.0, 955.0, 900.0]], f0=12.0),
+                        receiver_coords=rec, receiver_field="vz")
+    a = stb.run(cfg)
+    assert "elastic_tiled2" in a.report.schedule["device_plan"]
+    for env in ({"STB_EL_STREAM": "1"}, {"STB_EL_STREAM": "1", "STB_EL_NV": "5", "STB_EL_NT": "3",
+                                         "STB_EL_LEAD": "12", "STB_EL_PUB": "2"}):
+        b = _with_env(env, lambda: stb.run(cfg))
+        assert "elastic_stream" in b.report.schedule["device_plan"]
+        _same(a, b)
     assert np.abs(a.fields["vz"]).max() > 0
