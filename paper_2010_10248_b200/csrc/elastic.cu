@@ -505,6 +505,15 @@ class ElasticProp final : public stb_prop_s {
         const uint32_t py = (f >= TXX ? kTYv : kTYt) + 2 * R_;
         fmap_[f] = make_map3d_f32(reinterpret_cast<const float*>(f_[f].p), md, pz, py, 1);
       }
+      // elastic_tiled2 v pass: per-stress boxes with only the halo the field
+      // is differentiated along (El2Cfg::fhy / fhz)
+      switch (R_) {
+        case 1: set_stress_maps<1>(md); break;
+        case 2: set_stress_maps<2>(md); break;
+        case 3: set_stress_maps<3>(md); break;
+        case 4: set_stress_maps<4>(md); break;
+        default: break;
+      }
       // elastic_tiled2: centre-operand boxes over the 16 x 32 tile
       for (int f = 0; f < NFIELDS; ++f)
         omap_[f] = make_map3d_f32(reinterpret_cast<const float*>(f_[f].p), md, kElTZ, 16, 1);
@@ -532,6 +541,14 @@ class ElasticProp final : public stb_prop_s {
   template <int R> static constexpr int ns_t() { return 2 * R + 1; }
   template <int R> using CfgV = ElTiledCfg<R, 6, kTYv, ns_v<R>()>;
   template <int R> using CfgT = ElTiledCfg<R, 3, kTYt, ns_t<R>()>;
+
+  template <int R>
+  void set_stress_maps(const Dims& md) {
+    using C = El2Cfg<R, 0>;
+    for (int f = 0; f < 6; ++f)
+      smap_[f] = make_map3d_f32(reinterpret_cast<const float*>(f_[TXX + f].p), md,
+                                (uint32_t)C::fbz(f), (uint32_t)C::fby(f), 1);
+  }
 
   template <int R, int PASS>
   void set_pair_attr() {
@@ -576,7 +593,7 @@ class ElasticProp final : public stb_prop_s {
     a.negz = -0.0f;
     ElTiledArgs av = a, at = a;
     El2Maps mv{}, mt{};
-    for (int f = 0; f < 6; ++f) mv.f[f] = fmap_[TXX + f];
+    for (int f = 0; f < 6; ++f) mv.f[f] = smap_[f];
     for (int f = 0; f < 3; ++f) {
       mv.o[f] = omap_[VX + f];
       av.out[f] = reinterpret_cast<float*>(f_[VX + f].p);
@@ -661,7 +678,7 @@ class ElasticProp final : public stb_prop_s {
       El2Maps m{};
       const int nin = phase == 0 ? 6 : 3, nout = phase == 0 ? 3 : 6;
       const int fin = phase == 0 ? TXX : VX, fout = phase == 0 ? VX : TXX;
-      for (int f = 0; f < nin; ++f) m.f[f] = fmap_[fin + f];
+      for (int f = 0; f < nin; ++f) m.f[f] = phase == 0 ? smap_[f] : fmap_[fin + f];
       for (int f = 0; f < nout; ++f) {
         m.o[f] = omap_[fout + f];
         a.out[f] = reinterpret_cast<float*>(f_[fout + f].p);
@@ -1068,6 +1085,7 @@ class ElasticProp final : public stb_prop_s {
   int rec_field_ = TXX;      // engine.py:327-332 records txx
   CUtensorMap fmap_[NFIELDS];
   CUtensorMap omap_[NFIELDS + 3];   // tile boxes of the fields, buoy, lam, mu (tiled2)
+  CUtensorMap smap_[6];             // per-stress boxes of the tiled2 v pass
   int64_t t_next_ = 0;
   bool as_open_ = false;
   int64_t as_t0_ = 0, as_n_ = 0;

@@ -43,8 +43,28 @@ struct El2Cfg {
   static constexpr int NM = PASS == 0 ? 1 : 2;                // materials
   static constexpr int ZH = (R + 3) / 4 * 4;                  // z halo (16-byte boxes)
   static constexpr int PY = TY + 2 * R, PZ = TZ + 2 * ZH;
-  static constexpr int FSLOT = (PY * PZ + 31) / 32 * 32;
-  static constexpr int SLOT = NF * FSLOT;
+  // Per staged field, only the halo it is differentiated along: in the v pass
+  // txx feeds the x queue alone (no halo), tyy / txy are differenced along y
+  // (halo rows), tzz / txz along z (halo columns), tyz along both; in the tau
+  // pass every velocity along both.  (Full boxes for all six cost 2.25 x the
+  // tile's sectors per field, "Elastic".)
+  static constexpr int fhy(int f) { return PASS == 1 || f == 1 || f == 3 || f == 5 ? R : 0; }
+  static constexpr int fhz(int f) { return PASS == 1 || f == 2 || f == 4 || f == 5 ? ZH : 0; }
+  static constexpr int fby(int f) { return TY + 2 * fhy(f); }
+  static constexpr int fbz(int f) { return TZ + 2 * fhz(f); }
+  static constexpr int fsz(int f) { return (fby(f) * fbz(f) + 31) / 32 * 32; }
+  static constexpr int foff(int f) {
+    int s = 0;
+    for (int i = 0; i < f; ++i) s += fsz(i);
+    return s;
+  }
+  static constexpr int boxf(int f) {                          // staged floats of fields [0, f)
+    int s = 0;
+    for (int i = 0; i < f; ++i) s += fby(i) * fbz(i);
+    return s;
+  }
+  static constexpr int SLOT = foff(NF);
+  static constexpr int BOXF = boxf(NF);
   static constexpr int Q = 2 * R + 1;
   static constexpr int NO = 3, NS = R + NO;
   static constexpr int TPL = TY * TZ;
@@ -91,9 +111,6 @@ __device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
 }
 __device__ __forceinline__ void fence_proxy_async_all() {
   asm volatile("fence.proxy.async;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
-  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ int ld_acquire_cta_s32(const volatile int* p) {
   int v;
@@ -144,14 +161,17 @@ struct ZWin {
 };
 
 // One tile (16 x 32 in y, z; x planes [x0, x1)) of one half step.  The caller
-// has initialised the barriers; every thread returns.  STREAM adds the
+// has initialised the barriers ONCE: g0 counts the iterations this CTA ran on
+// earlier tiles, and ring slots and barrier phases continue from there (an
+// mbarrier.inval + init between tiles misbehaved on B200 whenever slot 0 had
+// completed an odd number of phases).  Every thread returns.  STREAM adds the
 // cross-CTA protocol of elastic_stream (publish / dependency waits / throttle).
 template <int R, int PASS, bool GUARD, bool STREAM>
 __device__ __forceinline__ void el2_tile(const El2Maps& maps, const ElTiledArgs& a,
                                          const ElStream& sc, float* ring, float* opr,
                                          uint64_t* ofull, uint64_t* oempty, volatile int* wprog,
                                          const int y0, const int z0, const int x0, const int x1,
-                                         const int tile) {
+                                         const int tile, const int g0) {
   using C = El2Cfg<R, PASS>;
   constexpr int Q = C::Q, NS = C::NS, NO = C::NO, NF = C::NF, NOUT = C::NOUT, NM = C::NM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -170,7 +190,8 @@ __device__ __forceinline__ void el2_tile(const El2Maps& maps, const ElTiledArgs&
       int have = 0;                                 // tau role: planes stored on every dependency
       int budget = 8000;                            // v role: throttle polls left for this tile
       for (int n = 0; n < N; ++n) {
-        const int slot = n % NO;
+        const int g = g0 + n;
+        const int slot = g % NO;
         if constexpr (STREAM && PASS == 1) {
           // plane x0 - R + n of vx, vy, vz must be stored by every dependency
           // (which also means their sweeps have read the stress planes this
@@ -193,18 +214,18 @@ __device__ __forceinline__ void el2_tile(const El2Maps& maps, const ElTiledArgs&
             __nanosleep(128);
           }
         }
-        if (n >= NO) mbar_wait_sleep(&oempty[slot], (uint32_t)(((n / NO) - 1) & 1));
+        if (g >= NO) mbar_wait_sleep(&oempty[slot], (uint32_t)(((g / NO) - 1) & 1));
         float* os = opr + slot * C::OSLOT;
         const bool out = n >= 2 * R;
         const int x = x0 - 2 * R + n;               // output plane of iteration n
         if (out) os[(NOUT + NM) * C::TPL] = has_fac ? __ldg(a.fx + x) : 1.f;
-        mbar_arrive_expect_tx(&ofull[slot], (uint32_t)(NF * C::PY * C::PZ +
+        mbar_arrive_expect_tx(&ofull[slot], (uint32_t)(C::BOXF +
                                                        (out ? (NOUT + NM) * C::TPL : 0)) * 4u);
-        float* ps = ring + (n % NS) * C::SLOT;
+        float* ps = ring + (g % NS) * C::SLOT;
 #pragma unroll
         for (int f = 0; f < NF; ++f)
-          tma_load_3d(ps + f * C::FSLOT, &maps.f[f], zo + z0 - C::ZH, H + y0 - R, H + x0 - R + n,
-                      &ofull[slot]);
+          tma_load_3d(ps + C::foff(f), &maps.f[f], zo + z0 - C::fhz(f), H + y0 - C::fhy(f),
+                      H + x0 - R + n, &ofull[slot]);
         if (out) {
 #pragma unroll
           for (int k = 0; k < NOUT + NM; ++k)
@@ -290,7 +311,11 @@ __device__ __forceinline__ void el2_tile(const El2Maps& maps, const ElTiledArgs&
   const int y = y0 + ty, z = z0 + 2 * tzp;
   const bool in0 = y >= 0 && y < ny && z < nz, in1 = y >= 0 && y < ny && z + 1 < nz;
   const int gcore = in0 ? (int)a.d.at(0, y, z) : 0;
-  const int coff = (ty + R) * C::PZ + (2 * tzp + C::ZH);
+  // centre of field f in a ring slot: rows are TZ or PZ floats long
+  const int b32 = ty * C::TZ + 2 * tzp, b40 = ty * C::PZ + 2 * tzp;
+  auto cen = [&](int f) {
+    return (C::fbz(f) == C::TZ ? b32 : b40) + (C::fhy(f) * C::fbz(f) + C::fhz(f) + C::foff(f));
+  };
   const int ooff = ty * C::TZ + 2 * tzp;
   const int plane = (int)a.d.plane;
   const f2 nzr = bcast(a.negz);
@@ -314,8 +339,8 @@ __device__ __forceinline__ void el2_tile(const El2Maps& maps, const ElTiledArgs&
   for (int j = 0; j < Q; ++j) q0[j] = q1[j] = q2[j] = 0ull;
   constexpr int QF0 = 0, QF1 = PASS == 0 ? 3 : 1, QF2 = PASS == 0 ? 4 : 2;
 
-  int os = 0, sn = 0, so = NS - R;                  // n % NO, n % NS, (n - R) % NS
-  uint32_t oph = 0;
+  int os = g0 % NO, sn = g0 % NS, so = (g0 + NS - R) % NS;   // g % NO, g % NS, (g - R) % NS
+  uint32_t oph = (uint32_t)((g0 / NO) & 1);
   bool bad = false;
   for (int n0 = 0; n0 < N; n0 += Q) {
 #pragma unroll
@@ -323,17 +348,20 @@ __device__ __forceinline__ void el2_tile(const El2Maps& maps, const ElTiledArgs&
       const int n = n0 + u;
       if (n >= N) break;
       mbar_wait(&ofull[os], oph);
-      const float* sl = ring + sn * C::SLOT + coff;  // newest plane, centre
-      q0[u] = el_lds2(sl + QF0 * C::FSLOT);
-      q1[u] = el_lds2(sl + QF1 * C::FSLOT);
-      q2[u] = el_lds2(sl + QF2 * C::FSLOT);
+      const float* sl = ring + sn * C::SLOT;         // newest plane
+      q0[u] = el_lds2(sl + cen(QF0));
+      q1[u] = el_lds2(sl + cen(QF1));
+      q2[u] = el_lds2(sl + cen(QF2));
       if (n >= 2 * R) {
-        const float* cp = ring + so * C::SLOT + coff;   // output plane (sequence n - R)
+        const float* cp = ring + so * C::SLOT;          // output plane (sequence n - R)
         const float* ob = opr + os * C::OSLOT;
         auto gq0 = [&](int o) { return q0[el_pmod(u - R + o, Q)]; };
         auto gq1 = [&](int o) { return q1[el_pmod(u - R + o, Q)]; };
         auto gq2 = [&](int o) { return q2[el_pmod(u - R + o, Q)]; };
-        auto gy = [&](int f) { return [=](int o) { return el_lds2(cp + f * C::FSLOT + o * C::PZ); }; };
+        auto gy = [&](int f) {
+          const float* c0 = cp + cen(f);
+          return [=](int o) { return el_lds2(c0 + o * C::fbz(f)); };
+        };
         f2 res[NOUT];
         f2 fac = 0ull;
         if (has_fac) {
@@ -343,9 +371,9 @@ __device__ __forceinline__ void el2_tile(const El2Maps& maps, const ElTiledArgs&
         if constexpr (PASS == 0) {
           // fields: 0 txx, 1 tyy, 2 tzz, 3 txy, 4 txz, 5 tyz
           ZWin<C::HW> w4, w5, w2;
-          w4.load(cp + 4 * C::FSLOT);
-          w5.load(cp + 5 * C::FSLOT);
-          w2.load(cp + 2 * C::FSLOT);
+          w4.load(cp + cen(4));
+          w5.load(cp + cen(5));
+          w2.load(cp + cen(2));
           f2 d0 = stag2<R>(gq0, cxk, true, nzr);
           d0 = add2(d0, stag2<R>(gy(3), cyk, false, nzr));
           d0 = add2(d0, stag2<R>(w4, czk, false, nzr));
@@ -366,9 +394,9 @@ __device__ __forceinline__ void el2_tile(const El2Maps& maps, const ElTiledArgs&
         } else {
           // fields: 0 vx, 1 vy, 2 vz; outputs txx tyy tzz txy txz tyz
           ZWin<C::HW> w0, w1, w2;
-          w0.load(cp + 0 * C::FSLOT);
-          w1.load(cp + 1 * C::FSLOT);
-          w2.load(cp + 2 * C::FSLOT);
+          w0.load(cp + cen(0));
+          w1.load(cp + cen(1));
+          w2.load(cp + cen(2));
           const f2 lam = el_lds2(ob + 6 * C::TPL + ooff), mu = el_lds2(ob + 7 * C::TPL + ooff);
           const f2 mu2 = xmul2(mu, bcast(2.f), nzr);
           const f2 dg0 = stag2<R>(gq0, cxk, false, nzr);
@@ -451,14 +479,10 @@ struct El2Smem {
     oempty = ofull + C::NO;
     wprog = reinterpret_cast<volatile int*>(oempty + C::NO);
   }
-  // barriers for one tile; `again`: they carry a finished tile's phases
-  __device__ __forceinline__ void init(bool again) {
-    if (threadIdx.x == 0) {
+  // barriers: once per CTA; the per-tile progress words: before every tile
+  __device__ __forceinline__ void init(bool first) {
+    if (first && threadIdx.x == 0) {
       for (int o = 0; o < C::NO; ++o) {
-        if (again) {
-          mbar_inval(&ofull[o]);
-          mbar_inval(&oempty[o]);
-        }
         mbar_init(&ofull[o], 1);
         mbar_init(&oempty[o], C::NCW);
       }
@@ -476,12 +500,12 @@ elastic_tiled2(const __grid_constant__ El2Maps maps, const __grid_constant__ ElT
   using C = El2Cfg<R, PASS>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   El2Smem<R, PASS> sm(smem_raw);
-  sm.init(false);
+  sm.init(true);
   const int x0 = a.x_lo + blockIdx.z * a.cx;
   const ElStream none{};
   el2_tile<R, PASS, GUARD, false>(maps, a, none, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
                                   blockIdx.y * C::TY, blockIdx.x * C::TZ, x0,
-                                  min(x0 + a.cx, a.x_hi), 0);
+                                  min(x0 + a.cx, a.x_hi), 0, 0);
 }
 
 // The full step (v sweep, then tau sweep) as ONE launch, the two sweeps
@@ -512,25 +536,26 @@ elastic_stream(const __grid_constant__ El2Maps mv, const __grid_constant__ El2Ma
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const bool tau = (int)blockIdx.x >= sc.nv;
   const int rank = tau ? (int)blockIdx.x - sc.nv : (int)blockIdx.x;
-  bool again = false;
+  const int N = (av.x_hi - av.x_lo) + 2 * R;         // iterations per tile
+  int g0 = 0;
   if (!tau) {
     using C = El2Cfg<R, 0>;
     El2Smem<R, 0> sm(smem_raw);
-    for (int t = rank; t < sc.tiles_yv * sc.tiles_z; t += sc.nv, again = true) {
-      sm.init(again);
+    for (int t = rank; t < sc.tiles_yv * sc.tiles_z; t += sc.nv, g0 += N) {
+      sm.init(g0 == 0);
       el2_tile<R, 0, GUARD, true>(mv, av, sc, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
                                   (t / sc.tiles_z) * C::TY, (t % sc.tiles_z) * C::TZ, av.x_lo,
-                                  av.x_hi, t);
+                                  av.x_hi, t, g0);
       __syncthreads();
     }
   } else {
     using C = El2Cfg<R, 1>;
     El2Smem<R, 1> sm(smem_raw);
-    for (int t = rank; t < sc.tiles_yt * sc.tiles_z; t += sc.nt, again = true) {
-      sm.init(again);
+    for (int t = rank; t < sc.tiles_yt * sc.tiles_z; t += sc.nt, g0 += N) {
+      sm.init(g0 == 0);
       el2_tile<R, 1, GUARD, true>(mt, at, sc, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
                                   (t / sc.tiles_z) * C::TY - R, (t % sc.tiles_z) * C::TZ, at.x_lo,
-                                  at.x_hi, t);
+                                  at.x_hi, t, g0);
       __syncthreads();
     }
   }

@@ -239,13 +239,13 @@ def test_elastic_streamed_single_launch_matches_two_launches():
     rng = np.random.default_rng(11)
     vp = 2000.0 + 2000.0 * rng.random(shape)
     grid = stb.GridSpec(shape, (10.0,) * 3, boundary_layers=16)
-    rec = np.stack([np.linspace(100.0, 2000.0, 64), np.full(64, 955.0), np.full(64, 300.0)],
+    rec = np.stack([np.linspace(200.0, 2000.0, 64), np.full(64, 955.0), np.full(64, 300.0)],
                    axis=1)
     cfg = stb.RunConfig(physics="elastic", grid=grid, space_order=8, nt=12, dt=0.5e-3,
                         medium={"vp": vp, "vs": vp / 1.7, "rho": 2100.0},
                         sources=stb.SourceSpec([[1155.0, 955.0, 900.0]], f0=12.0),
                         receiver_coords=rec, receiver_field="vz")
-    a = stb.run(cfg)
+    a = _with_env({"STB_EL_STREAM": "0"}, lambda: stb.run(cfg))
     assert "elastic_tiled2" in a.report.schedule["device_plan"]
     for env in ({"STB_EL_STREAM": "1"}, {"STB_EL_STREAM": "1", "STB_EL_NV": "5", "STB_EL_NT": "3",
                                          "STB_EL_LEAD": "12", "STB_EL_PUB": "2"}):
