@@ -163,6 +163,17 @@ def cfg5_inputs(seed: int = 5, nx: int | None = None):
     return medium, src, rec
 
 
+def pin_medium(stb, medium, limit: int = 2 << 30):
+    """The medium with its large arrays copied into page-locked host memory."""
+    def pin(a):
+        if isinstance(a, np.ndarray) and (64 << 20) <= a.nbytes <= limit:
+            return stb.pinned_copy(a)
+        return a
+    if isinstance(medium, dict):
+        return {k: pin(a) for k, a in medium.items()}
+    return pin(medium)
+
+
 def workload_config(workload: str, world: int) -> dict:
     """The workload description both arms print (implementation details of
     this repo's arm go to its "impl_detail")."""
@@ -572,6 +583,11 @@ def main():
     del runner                        # its device buffers go back to the pool
     torch.cuda.synchronize()
     if not args.no_e2e and world == 1:
+        # the step's inputs sit in pinned host memory (the contract's e2e rule):
+        # media arrays up to 2 GB each are copied into page-locked arrays once,
+        # outside the timed region (cfg5's 8.6 GB arrays stay pageable and are
+        # staged by the library)
+        v = pin_medium(stb, v)
         cfg_e = make_config(stb, v, src, rec, args.steps, args.k, args.arithmetic, wl)
         # one untimed call first (first-use costs: host staging buffers,
         # tensor maps, kernel attributes), then the timed one
@@ -587,7 +603,8 @@ def main():
         e2e = {"value": npts * args.steps / e2e_s / 1e9, "unit": "GPts/s",
                "h2d_bytes_per_step": int(h2d / args.steps),
                "d2h_bytes_per_step": int(d2h / args.steps),
-               "wall_s": e2e_s, "api": "paper_2010_10248_b200.run(RunConfig) (host numpy in/out)",
+               "wall_s": e2e_s, "api": "paper_2010_10248_b200.run(RunConfig) (host numpy in/out; "
+                                       "media in page-locked arrays from stb.pinned_copy)",
                "note": "includes model upload, GPU inspector, stepping, field+trace download"}
         del res
     elif not args.no_e2e and world > 1:

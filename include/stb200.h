@@ -52,6 +52,15 @@ const char* stb_last_error(void);
 int stb_device_count(int* count);
 int stb_set_device(int device);
 
+/* Page-locked host memory for the arrays that cross the boundary (media in,
+ * fields and traces out).  No reference counterpart: stencil_tb's arrays are
+ * plain NumPy (grid.py:173-198, engine.py:430-447).  Every entry point takes
+ * pageable memory too (staged through the library's own pinned ring); arrays
+ * from stb_host_alloc are read and written by the copy engine directly.
+ * Freed blocks are cached by size (the cache holds at most 6 GiB). */
+int stb_host_alloc(int64_t bytes, void** out);
+int stb_host_free(void* p);
+
 /* ------------------------------------------------------------------------
  * Geometry of a regular grid: index i sits at origin + i * spacing
  * (grid.py:22-74).

@@ -33,4 +33,6 @@ from .stepping import (AcousticModel, ElasticModel, TimeBufferedField, acoustic_
                        fused_inject_row, gather_box, inject_direct, record_receivers,
                        scatter_all, scatter_box)
 
+from ._lib import pinned_copy, pinned_empty
+
 __version__ = "0.1.0"

@@ -26,6 +26,7 @@ STB_OK, STB_ERR_ARG, STB_ERR_DOMAIN, STB_ERR_CUDA, STB_ERR_UNSTABLE, STB_ERR_PLA
 # Every symbol include/stb200.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "stb_abi_version", "stb_last_error", "stb_device_count", "stb_set_device",
+    "stb_host_alloc", "stb_host_free",
     "stb_interp_stencils", "stb_support_create", "stb_support_from_points", "stb_support_info", "stb_support_points",
     "stb_support_compress", "stb_support_masks", "stb_support_entries",
     "stb_support_decompose", "stb_support_destroy", "stb_acoustic_create",
@@ -107,6 +108,8 @@ def _declare(lib):
         "stb_last_error": ([], C.c_char_p),
         "stb_device_count": ([C.POINTER(C.c_int)], C.c_int),
         "stb_set_device": ([C.c_int], C.c_int),
+        "stb_host_alloc": ([i64, C.POINTER(P)], C.c_int),
+        "stb_host_free": ([P], C.c_int),
         "stb_interp_stencils": ([pdbl, i64, C.POINTER(Geometry), i64, pi64, pdbl], C.c_int),
         "stb_support_create": ([pdbl, i64, C.POINTER(Geometry), i32, C.POINTER(P)], C.c_int),
         "stb_support_from_points": ([pi64, i64, C.POINTER(Geometry), C.POINTER(P)], C.c_int),
@@ -204,6 +207,39 @@ def device_count() -> int:
 def require_device():
     if device_count() == 0:
         raise DeviceError("no CUDA device is visible; paper_2010_10248_b200 has no CPU fallback")
+
+
+def _host_free(address: int):
+    try:
+        lib().stb_host_free(C.c_void_p(address))
+    except Exception:      # interpreter shutdown
+        pass
+
+
+def pinned_empty(shape, dtype=np.float32) -> np.ndarray:
+    """Uninitialised C-contiguous array in page-locked host memory
+    (stb_host_alloc): the copy engine reads and writes it directly, where a
+    pageable array is staged through the library's pinned ring.  The block
+    goes back to the library's cache when the last view of the array dies."""
+    import weakref
+    dt = np.dtype(dtype)
+    shape = tuple(int(v) for v in np.atleast_1d(shape))
+    nbytes = int(np.prod(shape, dtype=np.int64)) * dt.itemsize
+    if nbytes == 0:
+        return np.empty(shape, dtype=dt)
+    p = C.c_void_p()
+    check(lib().stb_host_alloc(nbytes, C.byref(p)))
+    buf = (C.c_char * nbytes).from_address(p.value)
+    weakref.finalize(buf, _host_free, p.value)
+    return np.frombuffer(buf, dtype=dt).reshape(shape)
+
+
+def pinned_copy(a) -> np.ndarray:
+    """A page-locked copy of an array (see pinned_empty)."""
+    a = np.asarray(a)
+    out = pinned_empty(a.shape, a.dtype)
+    out[...] = a
+    return out
 
 
 def dptr(a: np.ndarray | None):

@@ -84,6 +84,22 @@ STB_API int stb_set_device(int device) {
   STB_GUARD({ STB_CUDA(cudaSetDevice(device)); })
 }
 
+STB_API int stb_host_alloc(int64_t bytes, void** out) {
+  STB_GUARD({
+    STB_REQUIRE(out != nullptr && bytes > 0, STB_ERR_ARG, "stb_host_alloc: bad arguments");
+    require_device();
+    *out = stb::host_pinned_alloc((size_t)bytes);
+    STB_REQUIRE(*out != nullptr, STB_ERR_NOMEM, "page-locked host allocation failed");
+  })
+}
+
+STB_API int stb_host_free(void* p) {
+  STB_GUARD({
+    STB_REQUIRE(p == nullptr || stb::host_pinned_free(p), STB_ERR_ARG,
+                "stb_host_free: not a block of stb_host_alloc");
+  })
+}
+
 STB_API int stb_interp_stencils(const double* coords, int64_t n, const stb_geometry* g,
                                 int64_t margin, int64_t* idx_out, double* w_out) {
   STB_GUARD({

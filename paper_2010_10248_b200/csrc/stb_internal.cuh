@@ -73,6 +73,9 @@ inline bool first_use_on_device(std::atomic<uint64_t>& mask) {
 // host_to_device is stream-ordered (returns once the host array may be
 // reused); the device_to_host variants return when the data is on the host.
 void host_to_device(void* dev, const void* host, size_t bytes, cudaStream_t st);
+// page-locked host blocks from a size-keyed cache (hostio.cu)
+void* host_pinned_alloc(size_t bytes);
+bool host_pinned_free(void* p);
 void device_to_host(void* host, const void* dev, size_t bytes, cudaStream_t st);
 // dense (nx, ny, row bytes) host array <- rows at dev + x*plane + y*pitch bytes
 void device_to_host_3d(void* host, const void* dev, size_t row, size_t ny, size_t nx,
