@@ -62,6 +62,9 @@ def test_no_cpu_fallback_without_device():
         stb.run(cfg)
     with pytest.raises(Exception):
         stb.interp_stencil((10.0, 10.0, 10.0), grid)
+    with pytest.raises(errors.DeviceError):        # page-locked arrays need the driver too
+        stb.pinned_empty((16, 16))
+    assert stb.pinned_empty((0, 4)).shape == (0, 4)   # empty: plain NumPy, no device call
 
 
 def test_product_does_not_import_oracle():
