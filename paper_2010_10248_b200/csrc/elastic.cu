@@ -431,7 +431,7 @@ class ElasticProp final : public stb_prop_s {
     if (pair_) {
       // opt-in (STB_EL_STREAM=1): bit-exact and it cuts the DRAM traffic of a
       // step by 15-20 %, but measured slower than the two launches
-      // (33 vs 25 ms at 1024^3) -- with half the SMs per
+      // (29 vs 24.6 ms at 1024^3) -- with half the SMs per
       // sweep, each SM's three-slot TMA pipeline is latency-bound
       int sms = 148;
       int dev = 0;
@@ -557,7 +557,7 @@ class ElasticProp final : public stb_prop_s {
     STB_CUDA(cudaFuncSetAttribute(elastic_tiled2<R, PASS, false>, at, sm));
     STB_CUDA(cudaFuncSetAttribute(elastic_tiled2<R, PASS, true>, at, sm));
     if (PASS == 0) {
-      const int ss = (int)std::max(El2Cfg<R, 0>::SMEM, El2Cfg<R, 1>::SMEM);
+      const int ss = (int)std::max(El2Cfg<R, 0, kSNOv>::SMEM, El2Cfg<R, 1, kSNOt>::SMEM);
       STB_CUDA(cudaFuncSetAttribute(elastic_stream<R, false>, at, ss));
       STB_CUDA(cudaFuncSetAttribute(elastic_stream<R, true>, at, ss));
     }
@@ -618,7 +618,7 @@ class ElasticProp final : public stb_prop_s {
     sc.tiles_yt = tiles_yt;
     sc.lead = stream_lead_;
     sc.pub = stream_pub_;
-    const int ss = (int)std::max(El2Cfg<R, 0>::SMEM, El2Cfg<R, 1>::SMEM);
+    const int ss = (int)std::max(El2Cfg<R, 0, kSNOv>::SMEM, El2Cfg<R, 1, kSNOt>::SMEM);
     const unsigned grid = (unsigned)(sc.nv + sc.nt);
     if (nonfinite) elastic_stream<R, true><<<grid, El2Cfg<R, 0>::NT + 32, ss, st_>>>(mv, mt, av, at, sc);
     else elastic_stream<R, false><<<grid, El2Cfg<R, 0>::NT + 32, ss, st_>>>(mv, mt, av, at, sc);
@@ -1078,7 +1078,7 @@ class ElasticProp final : public stb_prop_s {
   // elastic_stream: the full step as one launch (v and tau sweeps streaming
   // behind each other through L2); STB_EL_STREAM=0/1 overrides the size rule
   bool stream_ = false;
-  int stream_nv_ = 0, stream_nt_ = 0, stream_lead_ = 24, stream_pub_ = 8;
+  int stream_nv_ = 0, stream_nt_ = 0, stream_lead_ = 32, stream_pub_ = 8;
   DevBuf<unsigned> prog_v_, prog_t_;
   DevBuf<int> stream_err_;
   unsigned epoch_ = 0;

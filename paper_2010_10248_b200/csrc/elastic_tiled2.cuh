@@ -35,7 +35,7 @@
 namespace stb {
 namespace {
 
-template <int R, int PASS>
+template <int R, int PASS, int NO_ = 3>
 struct El2Cfg {
   static constexpr int TY = 16, TZ = kElTZ, P = TZ / 2;       // 16 pairs per row
   static constexpr int NF = PASS == 0 ? 6 : 3;                // staged (differentiated) fields
@@ -66,7 +66,7 @@ struct El2Cfg {
   static constexpr int SLOT = foff(NF);
   static constexpr int BOXF = boxf(NF);
   static constexpr int Q = 2 * R + 1;
-  static constexpr int NO = 3, NS = R + NO;
+  static constexpr int NO = NO_, NS = R + NO;
   static constexpr int TPL = TY * TZ;
   static constexpr int OSLOT = (NOUT + NM) * TPL + 32;        // + fx
   static constexpr int HW = (R + 1) / 2;                      // z window: pairs -HW .. +HW
@@ -166,13 +166,13 @@ struct ZWin {
 // mbarrier.inval + init between tiles misbehaved on B200 whenever slot 0 had
 // completed an odd number of phases).  Every thread returns.  STREAM adds the
 // cross-CTA protocol of elastic_stream (publish / dependency waits / throttle).
-template <int R, int PASS, bool GUARD, bool STREAM>
+template <int R, int PASS, bool GUARD, bool STREAM, int NO_ = 3>
 __device__ __forceinline__ void el2_tile(const El2Maps& maps, const ElTiledArgs& a,
                                          const ElStream& sc, float* ring, float* opr,
                                          uint64_t* ofull, uint64_t* oempty, volatile int* wprog,
                                          const int y0, const int z0, const int x0, const int x1,
                                          const int tile, const int g0) {
-  using C = El2Cfg<R, PASS>;
+  using C = El2Cfg<R, PASS, NO_>;
   constexpr int Q = C::Q, NS = C::NS, NO = C::NO, NF = C::NF, NOUT = C::NOUT, NM = C::NM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ny = (int)a.d.ny, nz = (int)a.d.nz;
@@ -464,9 +464,9 @@ __device__ __forceinline__ void el2_tile(const El2Maps& maps, const ElTiledArgs&
 }
 
 // shared memory of one pass: plane ring, operand ring, barriers, warp progress
-template <int R, int PASS>
+template <int R, int PASS, int NO_ = 3>
 struct El2Smem {
-  using C = El2Cfg<R, PASS>;
+  using C = El2Cfg<R, PASS, NO_>;
   float* ring;
   float* opr;
   uint64_t* ofull;
@@ -526,6 +526,11 @@ elastic_tiled2(const __grid_constant__ El2Maps maps, const __grid_constant__ ElT
 // v tiles never wait on anything but a bounded throttle, and they are the
 // lower block indices, so the dependency waits of the tau role cannot
 // deadlock whatever the residency of the grid.
+// operand slots per sweep in the streamed launch: with half the SMs per sweep
+// a deeper TMA pipeline per SM keeps the sweep fed (1024^3: 3 slots 33.0 ms,
+// 5 slots 29.0 ms, 6 slots 29.1 ms; the two launches: 24.6 ms)
+constexpr int kSNOv = 5, kSNOt = 5;
+
 template <int R, bool GUARD>
 __global__ void __launch_bounds__(El2Cfg<R, 0>::NT + 32, 1)
 elastic_stream(const __grid_constant__ El2Maps mv, const __grid_constant__ El2Maps mt,
@@ -539,21 +544,21 @@ elastic_stream(const __grid_constant__ El2Maps mv, const __grid_constant__ El2Ma
   const int N = (av.x_hi - av.x_lo) + 2 * R;         // iterations per tile
   int g0 = 0;
   if (!tau) {
-    using C = El2Cfg<R, 0>;
-    El2Smem<R, 0> sm(smem_raw);
+    using C = El2Cfg<R, 0, kSNOv>;
+    El2Smem<R, 0, kSNOv> sm(smem_raw);
     for (int t = rank; t < sc.tiles_yv * sc.tiles_z; t += sc.nv, g0 += N) {
       sm.init(g0 == 0);
-      el2_tile<R, 0, GUARD, true>(mv, av, sc, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
+      el2_tile<R, 0, GUARD, true, kSNOv>(mv, av, sc, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
                                   (t / sc.tiles_z) * C::TY, (t % sc.tiles_z) * C::TZ, av.x_lo,
                                   av.x_hi, t, g0);
       __syncthreads();
     }
   } else {
-    using C = El2Cfg<R, 1>;
-    El2Smem<R, 1> sm(smem_raw);
+    using C = El2Cfg<R, 1, kSNOt>;
+    El2Smem<R, 1, kSNOt> sm(smem_raw);
     for (int t = rank; t < sc.tiles_yt * sc.tiles_z; t += sc.nt, g0 += N) {
       sm.init(g0 == 0);
-      el2_tile<R, 1, GUARD, true>(mt, at, sc, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
+      el2_tile<R, 1, GUARD, true, kSNOt>(mt, at, sc, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
                                   (t / sc.tiles_z) * C::TY - R, (t % sc.tiles_z) * C::TZ, at.x_lo,
                                   at.x_hi, t, g0);
       __syncthreads();
