@@ -230,7 +230,8 @@ def pinned_empty(shape, dtype=np.float32) -> np.ndarray:
     p = C.c_void_p()
     check(lib().stb_host_alloc(nbytes, C.byref(p)))
     buf = (C.c_char * nbytes).from_address(p.value)
-    weakref.finalize(buf, _host_free, p.value)
+    fin = weakref.finalize(buf, _host_free, p.value)
+    fin.atexit = False      # at interpreter exit the driver reclaims the block itself
     return np.frombuffer(buf, dtype=dt).reshape(shape)
 
 
