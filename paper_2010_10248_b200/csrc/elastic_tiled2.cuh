@@ -13,9 +13,9 @@
 // Here, per CTA (16 x 32 tile, an x chunk):
 //
 //   producer warp  one transaction barrier per iteration n: the NF input
-//                  field planes of sequence n (tile + R halo rows, 16-byte
-//                  aligned z halo, zero fill) into a plane ring of NS = R +
-//                  NO slots, and for output iterations the centre operands
+//                  field planes of sequence n (tile + the halo the field is
+//                  differentiated along: R rows, 16-byte aligned z columns,
+//                  zero fill) into a plane ring of NS = R + NO slots, and for output iterations the centre operands
 //                  (old values of the updated fields, materials) over the
 //                  tile plus fx into an NO-slot operand ring.
 //   8 warps        one z pair of the tile per thread: x derivatives from
@@ -27,6 +27,10 @@
 //                  producer fills next.
 //
 // Compulsory HBM bytes per point unchanged: v pass 52, tau pass 68.
+//
+// el2_tile is one tile of one half step; elastic_tiled2 launches it per
+// (tile, x chunk), elastic_stream (opt-in) runs both half steps of a step in
+// one launch with the tau sweep trailing the v sweep through L2.
 #pragma once
 
 #include "elastic_tiled.cuh"
@@ -96,11 +100,6 @@ struct ElStream {
   int pub;                // planes per published group (power of 2)
 };
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
