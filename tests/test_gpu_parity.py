@@ -106,6 +106,31 @@ def test_nan_guard_trips():
         stb.run(cfg)
 
 
+@pytest.mark.parametrize("stream", ["0", "1"])
+def test_elastic_nan_guard_trips_and_guarded_steps_are_exact(stream, monkeypatch):
+    """The guard variants of the elastic sweeps (compiled only into steps
+    t % 32 == 0): an unstable run raises StabilityError at step 32, and a
+    stable 40-step run crossing a guard step equals the oracle bit for bit --
+    for the two launches and for the streamed single launch."""
+    monkeypatch.setenv("STB_EL_STREAM", stream)
+    g = stb.GridSpec((40, 36, 40), (10.0,) * 3)
+    c = [[g.origin[a] + 17 * 10.0 + 3.0 for a in range(3)]]
+    med = {"vp": np.full(g.shape, 3000.0), "vs": 1700.0, "rho": 2100.0}
+    bad = stb.RunConfig(physics="elastic", grid=g, space_order=8, nt=40, dt=0.5,
+                        medium=med, sources=stb.SourceSpec(c, f0=12.0))
+    with pytest.raises(stb.StabilityError):
+        stb.run(bad)
+    good = dict(physics="elastic", grid=g, space_order=8, nt=40, dt=0.5e-3, medium=med,
+                receiver_coords=np.array(c) + 20.0)
+    res = stb.run(stb.RunConfig(sources=stb.SourceSpec(c, f0=12.0), **good))
+    want = "elastic_stream" if stream == "1" else "elastic_tiled2"
+    assert want in res.report.schedule["device_plan"]
+    ref = so.run(stb.RunConfig(sources=stb.SourceSpec(c, f0=12.0), **good))
+    for k in ref.fields:
+        assert np.array_equal(res.fields[k], ref.fields[k]), k
+    assert np.array_equal(res.receivers, ref.receivers)
+
+
 def test_domain_errors():
     g = stb.GridSpec((24, 24, 24), (10.0,) * 3, boundary_layers=8)
     cfg = stb.RunConfig(physics="acoustic", grid=g, space_order=4, nt=4,
