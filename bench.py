@@ -167,7 +167,10 @@ def pin_medium(stb, medium, limit: int = 2 << 30):
     """The medium with its large arrays copied into page-locked host memory."""
     def pin(a):
         if isinstance(a, np.ndarray) and (64 << 20) <= a.nbytes <= limit:
-            return stb.pinned_copy(a)
+            try:
+                return stb.pinned_copy(a)
+            except MemoryError:          # no page-locked memory left: stay pageable
+                return a
         return a
     if isinstance(medium, dict):
         return {k: pin(a) for k, a in medium.items()}
