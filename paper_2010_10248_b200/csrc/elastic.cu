@@ -422,13 +422,9 @@ class ElasticProp final : public stb_prop_s {
     set_damping(desc.damp);
     // TMA-tiled sweeps (elastic_tiled.cuh): f32, 3-D, R <= 4
     tiled_ = sizeof(T) == 4 && cf_.active[0] && cf_.active[1] && cf_.active[2] && R_ <= 4;
-    if (const char* e = std::getenv("STB_ELASTIC_PATH")) {
-      tiled_ = tiled_ && std::string(e) != "point";
-      pair_ = std::string(e) != "tiled1";
-    }
-    pair_ = pair_ && tiled_;
+    if (const char* e = std::getenv("STB_ELASTIC_PATH")) tiled_ = tiled_ && std::string(e) != "point";
     if (tiled_) setup_tiled();
-    if (pair_) {
+    if (tiled_) {
       // opt-in (STB_EL_STREAM=1): bit-exact and it cuts the DRAM traffic of a
       // step by 15-20 %, but measured slower than the two launches
       // (29 vs 24.6 ms at 1024^3) -- with half the SMs per
@@ -499,12 +495,11 @@ class ElasticProp final : public stb_prop_s {
       md.nz = d_.pitch;
       md.pitch = d_.pitch;
       md.plane = d_.plane;
-      // tau fields feed the v pass (kTYv tiles), v fields the tau pass (kTYt)
+      // tau pass: the three velocities with the full halo of a 16 x 32 tile
       const uint32_t pz = kElTZ + 2 * ((R_ + 3) / 4 * 4);
-      for (int f = 0; f < NFIELDS; ++f) {
-        const uint32_t py = (f >= TXX ? kTYv : kTYt) + 2 * R_;
-        fmap_[f] = make_map3d_f32(reinterpret_cast<const float*>(f_[f].p), md, pz, py, 1);
-      }
+      for (int f = VX; f < TXX; ++f)
+        fmap_[f] = make_map3d_f32(reinterpret_cast<const float*>(f_[f].p), md, pz,
+                                  (uint32_t)(16 + 2 * R_), 1);
       // elastic_tiled2 v pass: per-stress boxes with only the halo the field
       // is differentiated along (El2Cfg::fhy / fhz)
       switch (R_) {
@@ -529,18 +524,6 @@ class ElasticProp final : public stb_prop_s {
       }
     }
   }
-
-  // tile / ring per radius: 8 x 32 tiles, two CTAs per SM (independent
-  // per-plane barriers); the R = 4 v pass keeps 6 slots so two fit
-  // 16 x 32 tiles, one CTA/SM for both passes.  Measured alternatives
-  // (512^3 so=8): 8 x 32 tiles with two CTAs/SM for both passes (6-slot v
-  // ring) 35.4 Gpts/s, for the tau pass only 36.3, vs 36.4 here -- the
-  // per-plane barrier is not what bounds these sweeps.
-  static constexpr int kTYv = 16, kTYt = 16, kMBv = 1, kMBt = 1;
-  template <int R> static constexpr int ns_v() { return 2 * R + 1; }
-  template <int R> static constexpr int ns_t() { return 2 * R + 1; }
-  template <int R> using CfgV = ElTiledCfg<R, 6, kTYv, ns_v<R>()>;
-  template <int R> using CfgT = ElTiledCfg<R, 3, kTYt, ns_t<R>()>;
 
   template <int R>
   void set_stress_maps(const Dims& md) {
@@ -642,12 +625,6 @@ class ElasticProp final : public stb_prop_s {
   void set_tiled_attr() {
     set_pair_attr<R, 0>();
     set_pair_attr<R, 1>();
-    STB_CUDA(cudaFuncSetAttribute(elastic_tiled<R, 0, kTYv, ns_v<R>(), kMBv>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)CfgV<R>::smem_bytes()));
-    STB_CUDA(cudaFuncSetAttribute(elastic_tiled<R, 1, kTYt, ns_t<R>(), kMBt>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)CfgT<R>::smem_bytes()));
   }
 
   template <int R>
@@ -674,55 +651,31 @@ class ElasticProp final : public stb_prop_s {
     a.x_hi = x_hi;
     a.nonfinite = nonfinite;
     a.negz = -0.0f;
-    if (pair_) {
-      El2Maps m{};
-      const int nin = phase == 0 ? 6 : 3, nout = phase == 0 ? 3 : 6;
-      const int fin = phase == 0 ? TXX : VX, fout = phase == 0 ? VX : TXX;
-      for (int f = 0; f < nin; ++f) m.f[f] = phase == 0 ? smap_[f] : fmap_[fin + f];
-      for (int f = 0; f < nout; ++f) {
-        m.o[f] = omap_[fout + f];
-        a.out[f] = reinterpret_cast<float*>(f_[fout + f].p);
-      }
-      if (phase == 0) {
-        m.o[3] = omap_[NFIELDS + 0];
-      } else {
-        m.o[6] = omap_[NFIELDS + 1];
-        m.o[7] = omap_[NFIELDS + 2];
-      }
-      const dim3 grid = grid_for(16);
-      const bool g = nonfinite != nullptr;
-      if (phase == 0) {
-        using C = El2Cfg<R, 0>;
-        if (g) elastic_tiled2<R, 0, true><<<grid, C::NT, C::SMEM, st_>>>(m, a);
-        else elastic_tiled2<R, 0, false><<<grid, C::NT, C::SMEM, st_>>>(m, a);
-      } else {
-        using C = El2Cfg<R, 1>;
-        if (g) elastic_tiled2<R, 1, true><<<grid, C::NT, C::SMEM, st_>>>(m, a);
-        else elastic_tiled2<R, 1, false><<<grid, C::NT, C::SMEM, st_>>>(m, a);
-      }
-      STB_CHECK_LAUNCH();
-      return;
+    El2Maps m{};
+    const int nin = phase == 0 ? 6 : 3, nout = phase == 0 ? 3 : 6;
+    const int fout = phase == 0 ? VX : TXX;
+    for (int f = 0; f < nin; ++f) m.f[f] = phase == 0 ? smap_[f] : fmap_[VX + f];
+    for (int f = 0; f < nout; ++f) {
+      m.o[f] = omap_[fout + f];
+      a.out[f] = reinterpret_cast<float*>(f_[fout + f].p);
     }
     if (phase == 0) {
-    // v half step: inputs txx tyy tzz txy txz tyz, updates vx vy vz
-    ElTiledMaps mv{};
-    for (int f = 0; f < 6; ++f) mv.f[f] = fmap_[TXX + f];
-    for (int f = 0; f < 3; ++f) a.out[f] = reinterpret_cast<float*>(f_[VX + f].p);
-    a.m0 = reinterpret_cast<const float*>(buoy_.p);
-    a.m1 = nullptr;
-    elastic_tiled<R, 0, kTYv, ns_v<R>(), kMBv>
-        <<<grid_for(kTYv), CfgV<R>::THREADS, CfgV<R>::smem_bytes(), st_>>>(mv, a);
-    STB_CHECK_LAUNCH();
-    return;
+      m.o[3] = omap_[NFIELDS + 0];
+    } else {
+      m.o[6] = omap_[NFIELDS + 1];
+      m.o[7] = omap_[NFIELDS + 2];
     }
-    // tau half step: inputs vx vy vz, updates the six stresses
-    ElTiledMaps mt{};
-    for (int f = 0; f < 3; ++f) mt.f[f] = fmap_[VX + f];
-    for (int f = 0; f < 6; ++f) a.out[f] = reinterpret_cast<float*>(f_[TXX + f].p);
-    a.m0 = reinterpret_cast<const float*>(lam_.p);
-    a.m1 = reinterpret_cast<const float*>(mu_.p);
-    elastic_tiled<R, 1, kTYt, ns_t<R>(), kMBt>
-        <<<grid_for(kTYt), CfgT<R>::THREADS, CfgT<R>::smem_bytes(), st_>>>(mt, a);
+    const dim3 grid = grid_for(16);
+    const bool g = nonfinite != nullptr;
+    if (phase == 0) {
+      using C = El2Cfg<R, 0>;
+      if (g) elastic_tiled2<R, 0, true><<<grid, C::NT, C::SMEM, st_>>>(m, a);
+      else elastic_tiled2<R, 0, false><<<grid, C::NT, C::SMEM, st_>>>(m, a);
+    } else {
+      using C = El2Cfg<R, 1>;
+      if (g) elastic_tiled2<R, 1, true><<<grid, C::NT, C::SMEM, st_>>>(m, a);
+      else elastic_tiled2<R, 1, false><<<grid, C::NT, C::SMEM, st_>>>(m, a);
+    }
     STB_CHECK_LAUNCH();
   }
 
@@ -1033,21 +986,18 @@ class ElasticProp final : public stb_prop_s {
 
   std::string describe(int k) override {
     std::ostringstream os;
-    if (tiled_ && pair_ && stream_)
+    if (tiled_ && stream_)
       os << "elastic_stream<f32,R=" << R_ << "> (one launch per step: " << stream_nv_
          << " v-sweep + " << stream_nt_ << " tau-sweep CTAs streaming through L2; "
          << "16x32 tiles as z pairs)";
-    else if (tiled_ && pair_)
+    else if (tiled_)
       os << "elastic_tiled2<f32,R=" << R_ << "> (TMA plane + operand rings, producer warp; "
          << "16x32 tiles as z pairs; x chunk 256)";
-    else if (tiled_)
-      os << "elastic_tiled<f32,R=" << R_ << "> (TMA plane rings; " << kTYv
-         << "x32 tiles; x chunk 256)";
     else
       os << "elastic_point<" << (sizeof(T) == 4 ? "f32" : "f64") << ",R=" << R_
          << "> (v + tau, thread per point, zero-haloed layout)";
     os << " k=1 requested_k=" << k
-       << " bytes_per_point=" << (tiled_ && pair_ && stream_ ? 21 : 30) * sizeof(T);
+       << " bytes_per_point=" << (tiled_ && stream_ ? 21 : 30) * sizeof(T);
     return os.str();
   }
 
@@ -1074,7 +1024,6 @@ class ElasticProp final : public stb_prop_s {
   DevBuf<T> fac_[3];
   bool has_fac_ = false;
   bool tiled_ = false;
-  bool pair_ = true;          // elastic_tiled2 unless STB_ELASTIC_PATH=tiled1
   // elastic_stream: the full step as one launch (v and tau sweeps streaming
   // behind each other through L2); STB_EL_STREAM=0/1 overrides the size rule
   bool stream_ = false;
