@@ -158,7 +158,7 @@ tti_fused2(const __grid_constant__ Tti2Maps maps, const __grid_constant__ TtiFus
   const int nx = (int)a.d.nx, ny = (int)a.d.ny, nz = (int)a.d.nz;
   const int x1 = min(x0 + a.cx, a.x_hi);
   const int n_iter = (x1 - x0) + 2 * r;             // pass-1 planes x0-r .. x1-1+r
-  const int n_seq = n_iter + 2 * r;                 // p/q planes x0-2r .. x1-1+2r
+                                                    // (p/q planes x0-2r .. x1-1+2r)
   const bool has_fac = a.has_fac != 0;
 
   if (tid == 0) {
