@@ -535,7 +535,7 @@ class ElasticProp final : public stb_prop_s {
 
   template <int R, int PASS>
   void set_pair_attr() {
-    const int sm = (int)El2Cfg<R, PASS>::SMEM;
+    const int sm = (int)El2Two<R, PASS>::SMEM;
     const auto at = cudaFuncAttributeMaxDynamicSharedMemorySize;
     STB_CUDA(cudaFuncSetAttribute(elastic_tiled2<R, PASS, false>, at, sm));
     STB_CUDA(cudaFuncSetAttribute(elastic_tiled2<R, PASS, true>, at, sm));
@@ -668,11 +668,11 @@ class ElasticProp final : public stb_prop_s {
     const dim3 grid = grid_for(16);
     const bool g = nonfinite != nullptr;
     if (phase == 0) {
-      using C = El2Cfg<R, 0>;
+      using C = El2Two<R, 0>;
       if (g) elastic_tiled2<R, 0, true><<<grid, C::NT, C::SMEM, st_>>>(m, a);
       else elastic_tiled2<R, 0, false><<<grid, C::NT, C::SMEM, st_>>>(m, a);
     } else {
-      using C = El2Cfg<R, 1>;
+      using C = El2Two<R, 1>;
       if (g) elastic_tiled2<R, 1, true><<<grid, C::NT, C::SMEM, st_>>>(m, a);
       else elastic_tiled2<R, 1, false><<<grid, C::NT, C::SMEM, st_>>>(m, a);
     }

@@ -492,17 +492,24 @@ struct El2Smem {
   }
 };
 
+// operand slots of the two-launch path per pass.  Since the v pass stages
+// per-field boxes its ring has room for five (1024^3: 3 / 4 / 5 / 6 slots 43.7 /
+// 45.4 / 45.9 / 45.7 GPts/s); the tau pass is best at three (2: 40.6, 4: 44.1
+// with five v slots).
+template <int PASS> constexpr int el2_two_no() { return PASS == 0 ? 5 : 3; }
+template <int R, int PASS> using El2Two = El2Cfg<R, PASS, el2_two_no<PASS>()>;
+
 // One half step as its own launch: a CTA per (tile, x chunk).
 template <int R, int PASS, bool GUARD>
 __global__ void __launch_bounds__(El2Cfg<R, PASS>::NT, 1)
 elastic_tiled2(const __grid_constant__ El2Maps maps, const __grid_constant__ ElTiledArgs a) {
-  using C = El2Cfg<R, PASS>;
+  using C = El2Two<R, PASS>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  El2Smem<R, PASS> sm(smem_raw);
+  El2Smem<R, PASS, C::NO> sm(smem_raw);
   sm.init(true);
   const int x0 = a.x_lo + blockIdx.z * a.cx;
   const ElStream none{};
-  el2_tile<R, PASS, GUARD, false>(maps, a, none, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
+  el2_tile<R, PASS, GUARD, false, C::NO>(maps, a, none, sm.ring, sm.opr, sm.ofull, sm.oempty, sm.wprog,
                                   blockIdx.y * C::TY, blockIdx.x * C::TZ, x0,
                                   min(x0 + a.cx, a.x_hi), 0, 0);
 }
