@@ -494,8 +494,9 @@ struct El2Smem {
 
 // operand slots of the two-launch path per pass.  Since the v pass stages
 // per-field boxes its ring has room for five (1024^3: 3 / 4 / 5 / 6 slots 43.7 /
-// 45.4 / 45.9 / 45.7 GPts/s); the tau pass is best at three (2: 40.6, 4: 44.1
-// with five v slots).
+// 45.4 / 45.9 / 45.7 GPts/s); the tau pass is best at three (2: 40.6, 4: 44.1,
+// 5: 43.1 with five v slots -- its DRAM reads GROW with depth: 54.6 / 63.9 /
+// 66.0 GB at 3 / 4 / 5 slots).
 template <int PASS> constexpr int el2_two_no() { return PASS == 0 ? 5 : 3; }
 template <int R, int PASS> using El2Two = El2Cfg<R, PASS, el2_two_no<PASS>()>;
 
